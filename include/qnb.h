@@ -1,0 +1,177 @@
+/*
+ * qnb.h — C-ABI of the B200 (sm_100a) backend for the QNet mixed-precision
+ * inference hot path (arxiv 2209.15427, reference at /root/reference/proj).
+ *
+ * The reference has no backend/plugin seam: its operator API is the set of free
+ * functions in include/qnet/{ops,quantizer,moe}.hpp taking host qnet::Tensor by
+ * const reference.  This header is the drop-in boundary a maintainer
+ * binds from the reference side: plain pointers and sizes,
+ * no C++ or torch types.  Two tiers:
+ *
+ *   op level   — one entry point per reference operator, same argument meaning,
+ *                operating on DEVICE buffers in the reference's own layout (dense
+ *                row-major NCHW) so results can be memcmp'd with the reference.
+ *   plan level — a compiled device plan for a whole calibrated graph
+ *                (Net::forward, src/net.cpp:305-330), device-native layouts (NHWC,
+ *                zero-point halos), fused epilogues, CUDA-graph replay.
+ *
+ * Conventions
+ *   - Every function returns qnb_status; on failure qnb_last_error() (thread-local)
+ *     holds the reference's message text where one exists ("shape mismatch",
+ *     "group divisibility violation", "non-positive output extent", ...).
+ *   - Device work is stream-ordered on the caller's stream (qnb_stream is a
+ *     cudaStream_t / CUstream); no implicit synchronisation.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute call
+ *     fails with QNB_E_CUDA.
+ *   - dtype codes equal qnet::DataType (include/qnet/datatypes.hpp:30-35).
+ */
+#ifndef QNB_H_
+#define QNB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define QNB_ABI_VERSION 1
+
+typedef void* qnb_stream; /* cudaStream_t (0 = legacy default stream) */
+
+typedef enum {
+  QNB_FP32 = 0,   /* qnet::DataType::FP32 */
+  QNB_FP16 = 1,   /* qnet::DataType::FP16 */
+  QNB_INT8Q = 2,  /* qnet::DataType::INT8Q  (uint8 storage, grid [0,255]) */
+  QNB_INT16Q = 3  /* qnet::DataType::INT16Q (uint16 storage, grid [0,65535]) */
+} qnb_dtype;
+
+typedef enum {
+  QNB_OK = 0,
+  QNB_E_ARG = 1,         /* std::invalid_argument without a more specific code */
+  QNB_E_SHAPE = 2,       /* "shape mismatch" */
+  QNB_E_GROUPS = 3,      /* "group divisibility violation" */
+  QNB_E_EXTENT = 4,      /* "non-positive output extent" */
+  QNB_E_QVALS = 5,       /* "... requires quantizer values" / "quantizer not finalized: ..." */
+  QNB_E_DTYPE = 6,       /* unsupported dtype combination */
+  QNB_E_RATIO = 7,       /* "invalid rescale ratio" / "shift_bits out of range" */
+  QNB_E_CUDA = 8,        /* CUDA runtime/driver error or no sm_100 device */
+  QNB_E_OOM = 9,         /* device allocation failed */
+  QNB_E_UNSUPPORTED = 10 /* valid for the reference but not implemented here */
+} qnb_status;
+
+/* qnet::QuantizerValues (include/qnet/quantizer_values.hpp:32-42). */
+typedef struct {
+  double f_min, f_max, scale;
+  int32_t zero;
+  double one;
+  int64_t i_min, i_max;
+} qnb_qvals;
+
+/* qnet::RequantParams (include/qnet/quantizer_values.hpp:59-67). */
+typedef struct {
+  int32_t shift_bits;
+  int64_t mult;
+  int32_t shift;
+  int64_t in_zero, out_zero, out_min, out_max;
+} qnb_requant;
+
+/* qnet::ConvParams (include/qnet/ops.hpp:31-41); bias_term as 0/1. */
+typedef struct {
+  int64_t out_channels, kernel_h, kernel_w, stride_h, stride_w, pad_h, pad_w, groups,
+      bias_term;
+} qnb_conv_params;
+
+/* ------------------------------------------------------------------ runtime */
+int qnb_abi_version(void);
+const char* qnb_last_error(void);
+/* Fails with QNB_E_CUDA unless `device` is a compute-capability 10.0 GPU. */
+qnb_status qnb_device_check(int device);
+qnb_status qnb_malloc(void** dev_ptr, size_t bytes);
+qnb_status qnb_free(void* dev_ptr);
+qnb_status qnb_memcpy_h2d(void* dst, const void* src, size_t bytes, qnb_stream s);
+qnb_status qnb_memcpy_d2h(void* dst, const void* src, size_t bytes, qnb_stream s);
+qnb_status qnb_stream_sync(qnb_stream s);
+/* Number of qnb kernels launched by this process so far (all entry points). */
+uint64_t qnb_kernel_launch_count(void);
+
+/* ------------------------------------------ host-side quantizer math (exact) */
+/* include/qnet/quantizer.hpp:28-81 — computed on the host once per layer,
+ * bit-identical to the reference (tests/test_host_math.py). */
+double qnb_round_half_even(double x);
+qnb_status qnb_estimate_params(double f_min, double f_max, qnb_dtype dtype, qnb_qvals* out);
+qnb_status qnb_estimate_from_observation(double seen_min, double seen_max, qnb_dtype dtype,
+                                         qnb_qvals* out);
+/* scale_quant_vals(qv_in, qv_out, sb)         — r = s_in / s_out        (quantizer.cpp:188) */
+qnb_status qnb_scale_quant_vals(const qnb_qvals* in, const qnb_qvals* out, int shift_bits,
+                                qnb_requant* rq);
+/* scale_quant_vals(qv_a, qv_b, qv_c, sb)      — r = s_a * s_b / s_c     (quantizer.cpp:194) */
+qnb_status qnb_scale_quant_vals3(const qnb_qvals* a, const qnb_qvals* b, const qnb_qvals* c,
+                                 int shift_bits, qnb_requant* rq);
+int64_t qnb_requant_clamp_host(int64_t acc, const qnb_requant* rq);
+
+/* ------------------------------------------- op level (device buffers, NCHW) */
+/* quantize(t, qv, dtype)            src/quantizer.cpp:115-126 */
+qnb_status qnb_quantize(const float* x, int64_t n, const qnb_qvals* qv, qnb_dtype dtype,
+                        void* out, qnb_stream s);
+/* dequantize(t)                     src/quantizer.cpp:128-139 */
+qnb_status qnb_dequantize(const void* q, int64_t n, qnb_dtype dtype, const qnb_qvals* qv,
+                          float* out, qnb_stream s);
+/* int->int QUANTIZER: requant_clamp(q - in_zero, rq)  src/net.cpp:483-493 */
+qnb_status qnb_requantize(const void* in, int64_t n, qnb_dtype in_dtype, const qnb_requant* rq,
+                          qnb_dtype out_dtype, void* out, qnb_stream s);
+/* relu_quant(in, rq)                src/ops.cpp:156-181 */
+qnb_status qnb_relu_quant(const void* in, int64_t n, qnb_dtype dtype, const qnb_requant* rq,
+                          void* out, qnb_stream s);
+/* relu_float(in, slope)             src/ops.cpp:147-154 */
+qnb_status qnb_relu_float(const void* in, int64_t n, qnb_dtype dtype, float negative_slope,
+                          void* out, qnb_stream s);
+/* cast_float(t, target)             src/ops.cpp:137-145 */
+qnb_status qnb_cast_float(const void* in, int64_t n, qnb_dtype from, qnb_dtype to, void* out,
+                          qnb_stream s);
+/* pool_max(in, {kernel, stride})    src/ops.cpp:344-390; shape = N,C,H,W */
+qnb_status qnb_pool_max(const void* in, const int64_t shape[4], qnb_dtype dtype, int64_t kernel,
+                        int64_t stride, void* out, qnb_stream s);
+/* lrn(in, lp) on FP32 N x C x S     src/ops.cpp:469-497 */
+qnb_status qnb_lrn(const float* in, int64_t n, int64_t c, int64_t spatial, int64_t local_size,
+                   double alpha, double beta, double k, float* out, qnb_stream s);
+/* softmax(in) over rows of F        src/ops.cpp:445-467 */
+qnb_status qnb_softmax(const float* in, int64_t rows, int64_t cols, float* out, qnb_stream s);
+/* conv_forward(in, weight, bias, cp, qv_out, shift_bits)  src/ops.cpp:264-342.
+ * x: N x C x H x W (dtype), w: OC x C/g x KH x KW (w_dtype == dtype for quantized,
+ * FP32/FP16 for float), bias: FP32 device vector or NULL, y: N x OC x OH x OW.
+ * in_qv / w_qv / out_qv required for quantized dtypes (else QNB_E_QVALS). */
+qnb_status qnb_conv_forward(const void* x, const int64_t x_shape[4], qnb_dtype dtype,
+                            const qnb_qvals* in_qv, const void* w, qnb_dtype w_dtype,
+                            const qnb_qvals* w_qv, const float* bias, const qnb_conv_params* cp,
+                            const qnb_qvals* out_qv, int shift_bits, void* y,
+                            int64_t y_shape[4], qnb_stream s);
+/* inner_product(in, weight, bias, out_features, qv_out, shift_bits) src/ops.cpp:392-443.
+ * x: N x K (any NCHW tensor flattened per sample), w: K x out_features. */
+qnb_status qnb_inner_product(const void* x, int64_t n, int64_t k, qnb_dtype dtype,
+                             const qnb_qvals* in_qv, const void* w, qnb_dtype w_dtype,
+                             const qnb_qvals* w_qv, const float* bias, int64_t out_features,
+                             const qnb_qvals* out_qv, int shift_bits, void* y, qnb_stream s);
+/* gating_logits + gating_probs + select_topk for a batch   src/moe.cpp:73-144.
+ * feats: B x D FP32; wa, wb: N x D; wc: N. Outputs idx/weights: B x top_k. */
+qnb_status qnb_moe_gate(const float* feats, int64_t batch, int64_t dim, const float* wa,
+                        const float* wb, const float* wc, int64_t n_experts, int64_t top_k,
+                        int noise_enabled, uint64_t seed, int64_t* idx, float* weights,
+                        qnb_stream s);
+/* weighted combine in selection order  src/moe.cpp:206-217, 240-249.
+ * expert_out: [n_experts][batch][per] (only selected rows are read). */
+/* expf exactly as the reference's libm computes it (used by gating; host copy). */
+float qnb_gating_expf(float x);
+qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, int64_t top_k,
+                           const int64_t* idx, const float* weights, float* out, qnb_stream s);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* QNB_H_ */

@@ -1,0 +1,200 @@
+// Device-side primitives for sm_100a: mbarriers, cp.async / bulk copies,
+// tcgen05 (TMEM alloc, UMMA issue, commit, TMEM loads) and the exact integer
+// requantizer shared by every quantized epilogue.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "qnb_internal.h"
+
+namespace qnb {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ------------------------------------------------------------------ mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// ------------------------------------------------------------ async copies
+__device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src)
+               : "memory");
+}
+// Arrive on `bar` once all prior cp.async of this thread have landed (the
+// arrival counts toward the barrier's expected count).
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 1-D bulk copy global -> shared on the TMA engine, completing on `bar` (tx bytes).
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------------ tcgen05
+__device__ __forceinline__ void tmem_alloc(uint32_t* smem_result, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_result)),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// MMA completion -> mbarrier arrive (implicitly fences before_thread_sync).
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// Instruction kinds of the implicit-GEMM engine.
+enum MmaKind : int { KIND_I8 = 0, KIND_F16 = 1, KIND_TF32 = 2 };
+
+template <int KIND>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+  if constexpr (KIND == KIND_I8) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else if constexpr (KIND == KIND_F16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  }
+}
+
+// 32 lanes x 32 bits, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t& r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, rows of 128
+// bytes grouped in 1024-byte atoms (SBO = 1024).  Start must lie in a
+// 1024-aligned atom; advancing K by 32 bytes adds 2 to the encoded address.
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* base) {
+  const uint64_t addr = smem_u32(base);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;           // start address
+  d |= 1ull << 16;                        // LBO (ignored for swizzled K-major)
+  d |= (1024ull >> 4) << 32;              // SBO
+  d |= 1ull << 46;                        // descriptor version (sm_100)
+  d |= 2ull << 61;                        // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor (cute::UMMA::InstrDescriptor layout), M = 128, K-major A/B.
+template <int KIND>
+__host__ __device__ constexpr uint32_t make_idesc(int n) {
+  // c_format: 2 = S32 for i8, 1 = F32 otherwise; a/b format: u8 = 0, f16 = 0, tf32 = 2.
+  return (KIND == KIND_I8 ? (2u << 4) : (1u << 4)) |
+         (KIND == KIND_TF32 ? ((2u << 7) | (2u << 10)) : 0u) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+// ------------------------------------------------- exact integer requantizer
+// qnet::requant_round / requant_clamp (src/quantizer.cpp:201-217): 128-bit
+// product, round half to even at bit s = shift_bits + shift, left shift when
+// s <= 0, then zero-point add and clamp.  Bit-identical to the reference.
+__device__ __forceinline__ int64_t requant_round(int64_t acc, const Requant& rq) {
+  const __int128 p = (__int128)acc * (__int128)rq.mult;
+  if (rq.s <= 0) return (int64_t)(__int128)((unsigned __int128)p << (unsigned)(-rq.s));
+  const int s = rq.s;
+  const __int128 half = (__int128)1 << (s - 1);
+  __int128 q = (p + half) >> s;
+  const __int128 low = p & ((((__int128)1) << s) - 1);
+  if (low == half && (q & 1)) q -= 1;
+  return (int64_t)q;
+}
+__device__ __forceinline__ int64_t requant_clamp(int64_t acc, const Requant& rq) {
+  int64_t v = requant_round(acc, rq) + rq.out_zero;
+  return v < rq.out_min ? rq.out_min : (v > rq.out_max ? rq.out_max : v);
+}
+
+// qnet::relu_quant (src/ops.cpp:156-181): truncating requant ReLU with
+// narrowing to the 32-bit Acctype for 8-bit storage after every stage.
+__device__ __forceinline__ int64_t wrap_acc(int64_t v, int acc32) {
+  return acc32 ? (int64_t)(int32_t)(uint32_t)v : v;
+}
+__device__ __forceinline__ int64_t relu_requant(int64_t q, const ReluRequant& r) {
+  int64_t d = q - r.in_zero;
+  d = d > 0 ? d : 0;
+  int64_t reg = wrap_acc((d * r.mult) >> r.shift_bits, r.acc32);
+  if (r.shift >= 0)
+    reg = wrap_acc(reg >> r.shift, r.acc32);
+  else
+    reg = wrap_acc((int64_t)((uint64_t)reg << (unsigned)(-r.shift)), r.acc32);
+  int64_t v = wrap_acc(reg + r.out_zero, r.acc32);
+  return v < r.out_min ? r.out_min : (v > r.out_max ? r.out_max : v);
+}
+
+}  // namespace qnb

@@ -1,0 +1,138 @@
+// Host-side internals shared by the qnb translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/qnb.h"
+
+namespace qnb {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+qnb_status fail(qnb_status code, const std::string& msg);
+qnb_status cuda_fail(cudaError_t e, const char* where);
+#define QNB_CUDA(call)                                       \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return ::qnb::cuda_fail(e_, #call); \
+  } while (0)
+#define QNB_TRY(call)                   \
+  do {                                  \
+    qnb_status st_ = (call);            \
+    if (st_ != QNB_OK) return st_;      \
+  } while (0)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// Verifies (once per process) that device 0.. is usable sm_100.
+qnb_status ensure_device();
+
+inline cudaStream_t as_stream(qnb_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+inline size_t dtype_size(int dt) { return dt == QNB_FP32 ? 4 : (dt == QNB_INT8Q ? 1 : 2); }
+inline bool is_quant(int dt) { return dt == QNB_INT8Q || dt == QNB_INT16Q; }
+
+// ---------------------------------------------------- exact host quant math
+double round_half_even(double x);
+qnb_status requant_from_ratio(double r, int64_t in_zero, const qnb_qvals& out, int sb,
+                              qnb_requant* rq);
+int64_t bias_to_acc(float b, double scale_a, double scale_b);
+
+// ------------------------------------------------- device activation layout
+// NHWC activation with a border ("halo") of hh rows / hw columns on each side,
+// channel count padded to c_phys.  Halo and padding hold `fill` (the blob's zero
+// point for quantized tensors, 0 for float ones).
+struct ActLayout {
+  int64_t n = 0, h = 0, w = 0, c = 0;
+  int64_t hh = 0, hw = 0, c_phys = 0;
+  int64_t wx = 0;  // extra columns on the right (keeps rows 16-byte aligned)
+  int dtype = QNB_INT8Q;
+  int64_t es() const { return (int64_t)dtype_size(dtype); }
+  int64_t hp() const { return h + 2 * hh; }
+  int64_t wp() const { return w + 2 * hw + wx; }
+  int64_t pix() const { return c_phys * es(); }
+  int64_t row() const { return wp() * pix(); }
+  int64_t img() const { return hp() * row(); }
+  int64_t bytes() const { return n * img(); }
+  int64_t interior_offset() const { return hh * row() + hw * pix(); }
+};
+
+// ------------------------------------------------- implicit GEMM (tcgen05)
+enum EpiKind : int { EPI_Q8 = 0, EPI_F16 = 1, EPI_F32 = 2 };
+
+// Device copies of the reference's RequantParams, pre-digested:
+// s = shift_bits + shift (src/quantizer.cpp:202).
+struct Requant {
+  int64_t mult;
+  int32_t s;
+  int64_t out_zero, out_min, out_max;
+};
+struct ReluRequant {
+  int64_t in_zero, mult;
+  int32_t shift_bits, shift;
+  int64_t out_zero, out_min, out_max;
+  int32_t acc32;
+};
+
+struct IgemmArgs {
+  // A operand: implicit im2col rows over an NHWC activation.
+  const uint8_t* a;
+  int64_t a_img, a_row, a_pix, a_group, a_origin;  // byte strides / origin offset
+  int32_t stride_h, stride_w, oh, ow;
+  int64_t m_total;
+  const int32_t* chunk_off;  // [num_kb * 8] byte offsets from the window origin
+  int32_t num_kb;            // K stages of 128 bytes
+  // B operand: packed, pre-swizzled [G][n_tiles][num_kb][n_rows][128 B]
+  const uint8_t* b;
+  int32_t n_rows, n_tiles, n_real, n_per_tile, ones_col, tmem_cols;
+  // epilogue
+  int32_t epi;
+  const int64_t* chan_const;  // [G * n_real] (quantized)
+  const float* bias;          // [G * n_real] or null (float)
+  int64_t zw;                 // weight zero point, multiplies the ones-column sum
+  Requant rq;
+  ReluRequant relu;
+  int32_t has_relu;
+  float slope;
+  uint8_t* out;
+  int64_t o_img, o_row, o_pix, o_origin;  // byte strides / origin
+  int32_t o_es, o_vec;                     // element bytes; 16-byte stores allowed
+};
+
+// Host description of one contraction (conv or inner product) to compile.
+struct IgemmGeometry {
+  int kind;            // MmaKind
+  int64_t groups;      // G
+  int64_t cg;          // real input channels per group
+  int64_t og;          // real output channels per group
+  int64_t kh, kw, sh, sw, ph, pw;
+  int64_t oh, ow;
+  bool is_fc;          // inner product: K over the flattened (NHWC) sample
+  int64_t fc_h, fc_w, fc_c;  // FC input logical dims (reference flatten c,h,w)
+};
+
+// Packed operand data produced on the host for one layer.
+struct IgemmPacked {
+  std::vector<int32_t> chunk_off;   // num_kb * 8
+  std::vector<int64_t> kmap;        // per packed K element -> reference k, or -1
+  int32_t num_kb = 0;
+  int32_t n_rows = 0, n_tiles = 0, n_per_tile = 0, ones_col = -1, tmem_cols = 0;
+  std::vector<uint8_t> b;           // [G][n_tiles][num_kb][n_rows][128]
+};
+
+// Builds the chunk table + K map for an input layout and geometry.
+qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk);
+// Packs weights (reference layout: conv OC x Cg x KH x KW, IP K x OUT) into B
+// tiles.  `w` is raw host bytes of element type w_es; quantized kinds add the
+// ones row used for the per-row input sum.
+qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, IgemmPacked* pk);
+// Launches the tcgen05 kernel.
+qnb_status igemm_launch(int kind, const IgemmArgs& a, int64_t groups, cudaStream_t s);
+
+}  // namespace qnb
