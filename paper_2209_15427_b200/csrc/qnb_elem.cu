@@ -50,7 +50,12 @@ __device__ __forceinline__ uint16_t f32_to_f16_bits(float x) {
   }
   return __half_as_ushort(__float2half_rn(x));
 }
-__device__ __forceinline__ float f16_bits_to_f32(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+// qnet::fp16_decode (src/half.cpp:73-95): exact, NaN payload kept.
+__device__ __forceinline__ float f16_bits_to_f32(uint16_t h) {
+  if ((h & 0x7C00u) == 0x7C00u && (h & 0x3FFu) != 0)
+    return __uint_as_float(((uint32_t)(h & 0x8000u) << 16) | 0x7F800000u | ((uint32_t)(h & 0x3FFu) << 13));
+  return __half2float(__ushort_as_half(h));
+}
 
 template <typename T>
 __device__ __forceinline__ int64_t qld(const void* p, int64_t i) {
@@ -94,15 +99,24 @@ __global__ void relu_quant_kernel(const T* __restrict__ in, int64_t n, ReluRequa
     out[i] = (T)relu_requant((int64_t)in[i], r);
 }
 
+// IEEE multiply with the host's (SSE) NaN rules, so NaN bits match the reference:
+// a NaN operand propagates quieted, an invalid product is the default NaN 0xFFC00000.
+__device__ __forceinline__ float host_fmul(float a, float b) {
+  if (isnan(a)) return __uint_as_float(__float_as_uint(a) | 0x400000u);
+  if (isnan(b)) return __uint_as_float(__float_as_uint(b) | 0x400000u);
+  const float r = __fmul_rn(a, b);
+  return isnan(r) ? __uint_as_float(0xFFC00000u) : r;
+}
+
 __global__ void relu_float_kernel(const void* __restrict__ in, int64_t n, int dtype, float slope,
                                   void* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (dtype == QNB_FP32) {
       const float x = reinterpret_cast<const float*>(in)[i];
-      reinterpret_cast<float*>(out)[i] = x > 0.0f ? x : __fmul_rn(x, slope);
+      reinterpret_cast<float*>(out)[i] = x > 0.0f ? x : host_fmul(x, slope);
     } else {
       const float x = f16_bits_to_f32(reinterpret_cast<const uint16_t*>(in)[i]);
-      reinterpret_cast<uint16_t*>(out)[i] = f32_to_f16_bits(x > 0.0f ? x : __fmul_rn(x, slope));
+      reinterpret_cast<uint16_t*>(out)[i] = f32_to_f16_bits(x > 0.0f ? x : host_fmul(x, slope));
     }
   }
 }

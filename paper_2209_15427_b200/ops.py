@@ -55,7 +55,17 @@ class DeviceArray:
 def _qv(qv) -> QVals:
     if qv is None or isinstance(qv, QVals):
         return qv
+    if hasattr(qv, "as_tuple"):
+        return QVals(*qv.as_tuple())
     return QVals(*qv)
+
+
+def _rq(rq) -> Requant:
+    if isinstance(rq, Requant):
+        return rq
+    if hasattr(rq, "as_tuple"):
+        return Requant(*rq.as_tuple())
+    return Requant(*rq)
 
 
 def _ref(x):
@@ -91,7 +101,7 @@ def scale_quant_vals(*args) -> Requant:
 
 
 def requant_clamp(acc: int, rq: Requant) -> int:
-    return L.lib().qnb_requant_clamp_host(int(acc), C.byref(rq))
+    return L.lib().qnb_requant_clamp_host(int(acc), C.byref(_rq(rq)))
 
 
 # ------------------------------------------------------------------ ops
@@ -114,14 +124,14 @@ def requantize(q: np.ndarray, in_dtype: int, rq: Requant, out_dtype: int) -> np.
     """The int -> int QUANTIZER layer (src/net.cpp:483-493)."""
     dq = DeviceArray.from_numpy(q)
     dy = DeviceArray(q.size * (1 if out_dtype == INT8Q else 2))
-    check(L.lib().qnb_requantize(dq.ptr, q.size, in_dtype, C.byref(rq), out_dtype, dy.ptr, None))
+    check(L.lib().qnb_requantize(dq.ptr, q.size, in_dtype, C.byref(_rq(rq)), out_dtype, dy.ptr, None))
     return dy.to_numpy(NP_OF[out_dtype], q.shape)
 
 
 def relu_quant(q: np.ndarray, dtype: int, rq: Requant) -> np.ndarray:
     dq = DeviceArray.from_numpy(q)
     dy = DeviceArray(q.nbytes)
-    check(L.lib().qnb_relu_quant(dq.ptr, q.size, dtype, C.byref(rq), dy.ptr, None))
+    check(L.lib().qnb_relu_quant(dq.ptr, q.size, dtype, C.byref(_rq(rq)), dy.ptr, None))
     return dy.to_numpy(q.dtype, q.shape)
 
 
