@@ -168,6 +168,82 @@ float qnb_gating_expf(float x);
 qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, int64_t top_k,
                            const int64_t* idx, const float* weights, float* out, qnb_stream s);
 
+/* ------------------------------------------------------------- plan level */
+/* Layer kinds: qnet::LayerKind codes (include/qnet/graph.hpp:33-44). */
+typedef enum {
+  QNB_LAYER_INPUT = 0,
+  QNB_LAYER_CONV = 1,
+  QNB_LAYER_POOL = 2,
+  QNB_LAYER_INNER_PRODUCT = 3,
+  QNB_LAYER_RELU = 4,
+  QNB_LAYER_LRN = 5,
+  QNB_LAYER_SOFTMAX = 6,
+  QNB_LAYER_QUANTIZER = 7,
+  QNB_LAYER_DROPOUT = 8,
+  QNB_LAYER_MOE = 9
+} qnb_layer_kind;
+
+/* One layer of a finalized (calibrated) qnet::Net, as the reference's public API
+ * exposes it: LayerSpec fields (include/qnet/graph.hpp:69-89), the parameter
+ * tensors from Net::param (already on their integer grid after
+ * finalize_quantizers, src/net.cpp:211-234) and the top blob's QuantizerValues from
+ * Net::blob_qvals (src/net.cpp:277-280).  Blobs are numbered by the caller; the
+ * graph must be a chain in declaration order (one bottom, one top per layer,
+ * src/graph.cpp:136-143).  All host pointers are read during qnb_plan_create only. */
+typedef struct {
+  int32_t kind;                       /* qnb_layer_kind */
+  int32_t mi_type, d_type, mo_type;   /* bottom / compute / top qnb_dtype */
+  int32_t bottom, top;                /* blob ids; bottom = -1 for INPUT */
+  int32_t input_ndim;                 /* INPUT: rank of input_shape */
+  int64_t input_shape[4];             /* INPUT: declared shape (batch may differ) */
+  qnb_conv_params conv;               /* CONV */
+  int64_t pool_kernel, pool_stride;   /* POOL */
+  int64_t lrn_local_size;             /* LRN */
+  double lrn_alpha, lrn_beta, lrn_k;
+  float negative_slope;               /* RELU */
+  int64_t num_output;                 /* INNER_PRODUCT */
+  int32_t bias_term;                  /* CONV, INNER_PRODUCT */
+  const void* weight;                 /* CONV: OC x C/g x KH x KW; IP: K x OUT (reference layout) */
+  int32_t weight_dtype;               /* qnb_dtype of `weight` */
+  int32_t weight_has_qv;
+  qnb_qvals weight_qv;
+  const float* bias;                  /* FP32, OC / OUT entries, or NULL */
+  int32_t top_has_qv;                 /* quantized tops: Net::blob_qvals(top) */
+  qnb_qvals top_qv;
+} qnb_layer_desc;
+
+typedef struct {
+  int64_t max_batch;      /* batch the plan's buffers and CUDA graph are sized for */
+  int32_t use_cuda_graph; /* capture the whole forward once and replay it */
+  int32_t reserved;
+} qnb_plan_opts;
+
+typedef struct qnb_plan qnb_plan;
+
+/* Compiles the device plan: packs weights into tcgen05 operand tiles, computes every
+ * requant program and per-channel constant on the host with the reference's own
+ * arithmetic, chooses NHWC layouts with zero-point halos, fuses conv/IP+ReLU,
+ * pool+dequant+LRN+quant and dequant+softmax, and allocates one activation arena. */
+qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32_t n_blobs,
+                           const qnb_plan_opts* opts, qnb_plan** out);
+/* Net::forward for the single INPUT -> single sink chain: `input` is the FP32 (or
+ * declared INPUT dtype) NCHW batch, `output` receives the sink in the reference's
+ * layout and dtype.  *_on_host selects pinned/pageable host memory (copies inside the
+ * call, stream-ordered) or device memory. */
+qnb_status qnb_plan_forward(qnb_plan* plan, const void* input, int64_t batch, int32_t input_on_host,
+                            void* output, int32_t output_on_host, qnb_stream s);
+/* Sink blob of the plan: its qnb_dtype and reference shape (batch = max_batch). */
+qnb_status qnb_plan_output_info(const qnb_plan* plan, int32_t* dtype, int32_t* ndim,
+                                int64_t shape[4]);
+/* Device pointer of blob `blob`'s buffer and its layout (n, h, w, c_phys, halo h/w,
+ * extra columns), for inspection; NULL pointer when the blob was fused away. */
+qnb_status qnb_plan_blob_info(const qnb_plan* plan, int32_t blob, void** dev_ptr,
+                              int64_t layout[8]);
+/* Kernel launches per forward and device bytes held by the plan. */
+qnb_status qnb_plan_stats(const qnb_plan* plan, int64_t* kernels_per_forward,
+                          int64_t* arena_bytes, int64_t* weight_bytes);
+qnb_status qnb_plan_destroy(qnb_plan* plan);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -65,6 +65,40 @@ class ConvParams(C.Structure):
                                          "stride_w", "pad_h", "pad_w", "groups", "bias_term")]
 
 
+class LayerDesc(C.Structure):
+    """qnb_layer_desc (include/qnb.h)."""
+
+    _fields_ = [
+        ("kind", C.c_int32), ("mi_type", C.c_int32), ("d_type", C.c_int32), ("mo_type", C.c_int32),
+        ("bottom", C.c_int32), ("top", C.c_int32), ("input_ndim", C.c_int32),
+        ("input_shape", C.c_int64 * 4), ("conv", ConvParams),
+        ("pool_kernel", C.c_int64), ("pool_stride", C.c_int64),
+        ("lrn_local_size", C.c_int64), ("lrn_alpha", C.c_double), ("lrn_beta", C.c_double), ("lrn_k", C.c_double),
+        ("negative_slope", C.c_float), ("num_output", C.c_int64), ("bias_term", C.c_int32),
+        ("weight", C.c_void_p), ("weight_dtype", C.c_int32), ("weight_has_qv", C.c_int32),
+        ("weight_qv", QVals), ("bias", C.c_void_p), ("top_has_qv", C.c_int32), ("top_qv", QVals),
+    ]
+
+
+class PlanOpts(C.Structure):
+    _fields_ = [("max_batch", C.c_int64), ("use_cuda_graph", C.c_int32), ("reserved", C.c_int32)]
+
+
+_PLAN_SIGS = {
+    "qnb_plan_create": (C.c_int, [C.POINTER(LayerDesc), C.c_int32, C.c_int32, C.POINTER(PlanOpts),
+                                  C.POINTER(C.c_void_p)]),
+    "qnb_plan_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
+                                   C.c_void_p]),
+    "qnb_plan_output_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int64)]),
+    "qnb_plan_blob_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "qnb_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64)]),
+    "qnb_plan_destroy": (C.c_int, [C.c_void_p]),
+}
+
+
+
 _lib = None
 
 _P = C.c_void_p
@@ -106,6 +140,7 @@ _SIGS = {
     "qnb_gating_expf": (C.c_float, [C.c_float]),
     "qnb_moe_combine": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
 }
+_SIGS.update(_PLAN_SIGS)
 
 
 def lib() -> C.CDLL:

@@ -1,0 +1,904 @@
+// Plan compiler and executor: the device-resident replacement of Net::forward
+// (src/net.cpp:305-330, run_layer_typed src/net.cpp:391-508) for a finalized,
+// calibrated chain graph.
+//
+// Compilation (host, once):
+//   1. blob table: dtype / shape per blob exactly as infer_blobs (src/graph.cpp:247-318)
+//   2. lowering with fusion over single-consumer chains:
+//        INPUT -> QUANTIZER(fp->q|f16)       => pack_input (quantize + NCHW->NHWC)
+//        CONV|IP (-> RELU)                   => tcgen05 implicit GEMM, fused epilogue
+//        POOL (-> Q2F) -> LRN (-> F2Q)       => pool_lrn, one HBM pass
+//        Q2F -> SOFTMAX                      => softmax_rows with fused dequantize
+//        DROPOUT                             => alias (no kernel)
+//        anything else                       => generic NHWC kernels
+//   3. layouts: every blob is NHWC; a blob consumed by a convolution carries that
+//      convolution's padding as a halo pre-filled with the blob's zero point (0.0 for
+//      float), so the implicit GEMM never needs bounds checks and zero-point padding is
+//      exact (src/ops.cpp:236,252).
+//   4. one activation arena (no slot reuse: halos stay valid), weights packed into
+//      tcgen05 operand tiles, requant programs and per-channel constants computed with
+//      the reference's arithmetic.
+// Execution: the step list is captured once into a CUDA graph and replayed.
+#include <cuda_fp16.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "qnb_device.cuh"
+#include "qnb_internal.h"
+#include "qnb_plan_kernels.h"
+
+namespace qnb {
+
+ActLayout choose_input_layout(const IgemmGeometry& g, int dtype, int64_t n, int64_t c, int64_t h, int64_t w);
+Requant to_dev(const qnb_requant& r);
+ReluRequant to_dev_relu(const qnb_requant& r, int dtype);
+int default_shift_bits(int dtype);
+
+namespace {
+
+enum OpKind { OP_PACK, OP_IGEMM, OP_POOL, OP_POOL_LRN, OP_CONVERT, OP_SOFTMAX, OP_ALIAS };
+
+struct Blob {
+  bool defined = false;
+  int dtype = QNB_FP32;
+  int ndim = 4;
+  int64_t n = 0, c = 0, h = 1, w = 1;
+  std::vector<int> consumers;  // layer indices
+  bool has_qv = false;
+  qnb_qvals qv{};
+  // device side
+  int alias = -1;        // shares the buffer of another blob
+  bool external = false; // the user's NCHW input
+  bool needs_buffer = false;
+  bool layout_set = false;
+  ActLayout L;
+  size_t off = 0;
+};
+
+struct Op {
+  OpKind kind;
+  int in = -1, out = -1;
+  int layer = -1;       // main layer
+  int relu = -1;        // fused RELU layer (IGEMM)
+  int pool = -1, lrn = -1;  // POOL_LRN parts
+  int pack_op = PACK_COPY;
+  int conv_op = CVT_CONVERT;
+  int in_dtype = 0, out_dtype = 0;
+};
+
+enum Sym { SYM_NONE = 0, SYM_INPUT = 1, SYM_OUTPUT = 2 };
+
+struct Step {
+  OpKind kind;
+  int src_sym = SYM_NONE, dst_sym = SYM_NONE;
+  // one of:
+  IgemmArgs ig;
+  int mma_kind = 0;
+  int64_t groups = 1;
+  int64_t rows_per_img = 0;  // igemm: oh*ow
+  PackArgs pack;
+  PoolArgs pool;
+  PoolLrnArgs plrn;
+  ConvertArgs cvt;
+  const uint8_t* sm_src = nullptr;
+  DevLayout sm_S;
+  int sm_dtype = 0;
+  DevQ sm_q;
+  float* sm_out = nullptr;
+  int64_t sm_F = 0;
+  bool unpack = false;
+  const uint8_t* up_src = nullptr;
+  DevLayout up_S;
+  uint8_t* up_dst = nullptr;
+};
+
+template <typename T>
+__global__ void fill_kernel(T* p, int64_t n, T v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace
+}  // namespace qnb
+
+struct qnb_plan {
+  std::vector<qnb_layer_desc> layers;
+  std::vector<qnb::Blob> blobs;
+  std::vector<qnb::Op> ops;
+  std::vector<qnb::Step> steps;
+  int64_t max_batch = 0;
+  bool use_graph = true;
+  int input_blob = -1, sink_blob = -1;
+  int out_dtype = QNB_FP32, out_ndim = 2;
+  int64_t out_shape[4] = {0, 0, 0, 0};
+  int64_t out_bytes_per_sample = 0, in_bytes_per_sample = 0;
+  uint8_t* arena = nullptr;
+  size_t arena_bytes = 0;
+  std::vector<void*> weight_allocs;
+  size_t weight_bytes = 0;
+  void* in_staging = nullptr;
+  void* out_staging = nullptr;
+  // captured graph
+  cudaGraphExec_t exec = nullptr;
+  const void* g_in = nullptr;
+  void* g_out = nullptr;
+  int64_t g_batch = -1;
+  cudaStream_t capture_stream = nullptr;
+  int device = 0;
+};
+
+namespace qnb {
+namespace {
+
+qnb_status fill_buffer(void* p, int64_t bytes, int dtype, int64_t value, cudaStream_t s) {
+  if (bytes <= 0) return QNB_OK;
+  if (dtype == QNB_INT16Q) {
+    fill_kernel<uint16_t><<<1024, 256, 0, s>>>((uint16_t*)p, bytes / 2, (uint16_t)value);
+  } else {
+    QNB_CUDA(cudaMemsetAsync(p, dtype == QNB_INT8Q ? (int)value : 0, (size_t)bytes, s));
+  }
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
+ActLayout plain_layout(const Blob& b, int64_t batch) {
+  ActLayout L;
+  L.n = batch;
+  L.c = b.c;
+  L.h = b.h;
+  L.w = b.w;
+  L.dtype = b.dtype;
+  L.c_phys = b.c;
+  return L;
+}
+
+int mma_kind_of(int dtype) { return dtype == QNB_INT8Q ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32); }
+
+IgemmGeometry geometry_of(const qnb_layer_desc& l, const Blob& in, const Blob& out) {
+  IgemmGeometry g;
+  std::memset(&g, 0, sizeof(g));
+  g.kind = mma_kind_of(l.d_type);
+  if (l.kind == QNB_LAYER_CONV) {
+    g.groups = l.conv.groups;
+    g.cg = in.c / l.conv.groups;
+    g.og = l.conv.out_channels / l.conv.groups;
+    g.kh = l.conv.kernel_h;
+    g.kw = l.conv.kernel_w;
+    g.sh = l.conv.stride_h;
+    g.sw = l.conv.stride_w;
+    g.ph = l.conv.pad_h;
+    g.pw = l.conv.pad_w;
+    g.oh = out.h;
+    g.ow = out.w;
+    g.is_fc = false;
+  } else {
+    g.groups = 1;
+    g.cg = in.c * in.h * in.w;
+    g.og = l.num_output;
+    g.kh = g.kw = g.sh = g.sw = 1;
+    g.oh = g.ow = 1;
+    g.is_fc = true;
+    g.fc_c = in.c;
+    g.fc_h = in.h;
+    g.fc_w = in.w;
+  }
+  return g;
+}
+
+// Layout the consumer op needs for its input blob.
+ActLayout required_input_layout(const qnb_plan& P, const Op& op, const Blob& b) {
+  if (op.kind == OP_IGEMM) {
+    const qnb_layer_desc& l = P.layers[op.layer];
+    const Blob& out = P.blobs[op.out];
+    IgemmGeometry g = geometry_of(l, b, out);
+    if (l.kind == QNB_LAYER_CONV) return choose_input_layout(g, b.dtype, P.max_batch, b.c, b.h, b.w);
+    ActLayout L = plain_layout(b, P.max_batch);
+    const int64_t es = (int64_t)dtype_size(b.dtype);
+    while ((L.c_phys * L.h * L.w * es) % 16 != 0) ++L.c_phys;  // K row of 16-byte chunks
+    return L;
+  }
+  ActLayout L = plain_layout(b, P.max_batch);
+  if (op.kind == OP_POOL && b.dtype == QNB_INT8Q && b.c % 16 != 0 && b.c > 16) L.c_phys = round_up(b.c, 16);
+  return L;
+}
+
+int root_of(const qnb_plan& P, int b) {
+  while (P.blobs[b].alias >= 0) b = P.blobs[b].alias;
+  return b;
+}
+
+qnb_status build_blob_table(qnb_plan& P) {
+  for (size_t i = 0; i < P.layers.size(); ++i) {
+    const qnb_layer_desc& l = P.layers[i];
+    if (l.top < 0 || l.top >= (int)P.blobs.size()) return fail(QNB_E_ARG, "blob id out of range");
+    Blob& t = P.blobs[l.top];
+    if (t.defined) return fail(QNB_E_ARG, "blob produced twice");
+    t.defined = true;
+    t.dtype = l.mo_type;
+    if (l.kind == QNB_LAYER_INPUT) {
+      if (P.input_blob >= 0) return fail(QNB_E_UNSUPPORTED, "graphs with several INPUT layers");
+      P.input_blob = l.top;
+      t.ndim = l.input_ndim;
+      t.n = P.max_batch;
+      t.c = l.input_ndim > 1 ? l.input_shape[1] : 1;
+      t.h = l.input_ndim > 2 ? l.input_shape[2] : 1;
+      t.w = l.input_ndim > 3 ? l.input_shape[3] : 1;
+      t.external = true;
+      continue;
+    }
+    if (l.bottom < 0 || l.bottom >= (int)P.blobs.size() || !P.blobs[l.bottom].defined)
+      return fail(QNB_E_ARG, "undefined blob");
+    const Blob& b = P.blobs[l.bottom];
+    if (b.dtype != l.mi_type) return fail(QNB_E_DTYPE, "dtype mismatch at blob");
+    P.blobs[l.bottom].consumers.push_back((int)i);
+    t.n = b.n;
+    switch (l.kind) {
+      case QNB_LAYER_CONV: {
+        if (b.ndim != 4) return fail(QNB_E_SHAPE, "shape mismatch");
+        const auto& cp = l.conv;
+        if (cp.groups < 1 || b.c % cp.groups != 0 || cp.out_channels % cp.groups != 0)
+          return fail(QNB_E_GROUPS, "group divisibility violation");
+        t.ndim = 4;
+        t.c = cp.out_channels;
+        t.h = (b.h + 2 * cp.pad_h - cp.kernel_h) / cp.stride_h + 1;
+        t.w = (b.w + 2 * cp.pad_w - cp.kernel_w) / cp.stride_w + 1;
+        if (t.h < 1 || t.w < 1) return fail(QNB_E_EXTENT, "non-positive output extent");
+        break;
+      }
+      case QNB_LAYER_POOL: {
+        if (b.ndim != 4) return fail(QNB_E_SHAPE, "shape mismatch");
+        t.ndim = 4;
+        t.c = b.c;
+        t.h = (b.h - l.pool_kernel) / l.pool_stride + 1;
+        t.w = (b.w - l.pool_kernel) / l.pool_stride + 1;
+        if (t.h < 1 || t.w < 1) return fail(QNB_E_EXTENT, "non-positive output extent");
+        break;
+      }
+      case QNB_LAYER_INNER_PRODUCT:
+        t.ndim = 2;
+        t.c = l.num_output;
+        t.h = t.w = 1;
+        break;
+      case QNB_LAYER_MOE:
+        return fail(QNB_E_UNSUPPORTED, "MOE layers are compiled by qnb_moe_plan (not in this plan)");
+      default:
+        t.ndim = b.ndim;
+        t.c = b.c;
+        t.h = b.h;
+        t.w = b.w;
+    }
+    if (is_quant(t.dtype)) {
+      if (!l.top_has_qv) return fail(QNB_E_QVALS, "quantizer not finalized: blob " + std::to_string(l.top));
+      t.has_qv = true;
+      t.qv = l.top_qv;
+    }
+  }
+  int sinks = 0;
+  for (size_t b = 0; b < P.blobs.size(); ++b)
+    if (P.blobs[b].defined && P.blobs[b].consumers.empty()) {
+      P.sink_blob = (int)b;
+      ++sinks;
+    }
+  if (P.input_blob < 0) return fail(QNB_E_ARG, "missing input");
+  if (sinks != 1) return fail(QNB_E_UNSUPPORTED, "plans support exactly one sink");
+  for (const Blob& b : P.blobs)
+    if (b.defined && b.consumers.size() > 1) return fail(QNB_E_UNSUPPORTED, "plans support chain graphs only");
+  return QNB_OK;
+}
+
+int sole_consumer(const qnb_plan& P, int blob) {
+  const Blob& b = P.blobs[blob];
+  return b.consumers.size() == 1 ? b.consumers[0] : -1;
+}
+
+bool is_q2f(const qnb_layer_desc& l) {
+  return l.kind == QNB_LAYER_QUANTIZER && l.mo_type == QNB_FP32 && l.mi_type != QNB_FP32;
+}
+bool is_f2x(const qnb_layer_desc& l) {
+  return l.kind == QNB_LAYER_QUANTIZER && l.mi_type == QNB_FP32 && l.mo_type != QNB_FP32;
+}
+
+qnb_status lower(qnb_plan& P) {
+  std::vector<bool> done(P.layers.size(), false);
+  for (size_t i = 0; i < P.layers.size(); ++i) {
+    if (done[i]) continue;
+    const qnb_layer_desc& l = P.layers[i];
+    done[i] = true;
+    Op op;
+    op.layer = (int)i;
+    op.in = l.bottom;
+    op.out = l.top;
+    switch (l.kind) {
+      case QNB_LAYER_INPUT: {
+        const int j = sole_consumer(P, l.top);
+        if (j < 0) return fail(QNB_E_UNSUPPORTED, "input without consumer");
+        const qnb_layer_desc& q = P.layers[j];
+        op.kind = OP_PACK;
+        op.in = l.top;
+        if (q.kind == QNB_LAYER_QUANTIZER) {
+          done[j] = true;
+          op.out = q.top;
+          op.pack_op = is_quant(q.mo_type) ? PACK_QUANTIZE : (q.mo_type == l.mo_type ? PACK_COPY : PACK_CAST);
+        } else {
+          // the consumer reads the input itself: materialise a device-layout copy
+          const int v = (int)P.blobs.size();
+          Blob copy = P.blobs[l.top];
+          copy.external = false;
+          copy.consumers = {j};
+          P.blobs.push_back(copy);
+          P.layers[j].bottom = v;
+          op.out = v;
+          op.pack_op = PACK_COPY;
+        }
+        break;
+      }
+      case QNB_LAYER_CONV:
+      case QNB_LAYER_INNER_PRODUCT: {
+        op.kind = OP_IGEMM;
+        if (l.d_type == QNB_INT16Q) return fail(QNB_E_UNSUPPORTED, "INT16 contractions are not implemented yet");
+        const int j = sole_consumer(P, l.top);
+        if (j >= 0 && P.layers[j].kind == QNB_LAYER_RELU && P.layers[j].d_type == l.mo_type &&
+            P.layers[j].mo_type == l.mo_type) {
+          done[j] = true;
+          op.relu = j;
+          op.out = P.layers[j].top;
+        }
+        break;
+      }
+      case QNB_LAYER_POOL:
+      case QNB_LAYER_QUANTIZER:
+      case QNB_LAYER_LRN: {
+        // try pool? -> q2f? -> lrn -> f2x?
+        int cur = (int)i;
+        int pool = -1, lrn = -1, post = -1;
+        int in_dtype = l.mi_type;
+        if (l.kind == QNB_LAYER_POOL) {
+          pool = cur;
+          const int j = sole_consumer(P, P.layers[cur].top);
+          if (j >= 0 && (is_q2f(P.layers[j]) || P.layers[j].kind == QNB_LAYER_LRN)) cur = j;
+          else cur = -1;
+        }
+        if (cur >= 0 && is_q2f(P.layers[cur])) {
+          const int j = sole_consumer(P, P.layers[cur].top);
+          if (j >= 0 && P.layers[j].kind == QNB_LAYER_LRN) {
+            if (pool < 0) in_dtype = P.layers[cur].mi_type;
+            cur = j;
+          } else {
+            cur = -1;
+          }
+        }
+        if (cur >= 0 && P.layers[cur].kind == QNB_LAYER_LRN) {
+          lrn = cur;
+          const int j = sole_consumer(P, P.layers[cur].top);
+          if (j >= 0 && is_f2x(P.layers[j])) post = j;
+        }
+        if (lrn >= 0) {
+          int q2f = -1;
+          {
+            const int first = pool >= 0 ? sole_consumer(P, P.layers[pool].top) : (int)i;
+            if (first >= 0 && is_q2f(P.layers[first])) q2f = first;
+          }
+          for (int k : {pool, q2f, lrn, post})
+            if (k >= 0) done[k] = true;
+          op.kind = OP_POOL_LRN;
+          op.pool = pool;
+          op.lrn = lrn;
+          op.in = pool >= 0 ? P.layers[pool].bottom : l.bottom;
+          op.in_dtype = pool >= 0 ? P.layers[pool].mi_type : in_dtype;
+          op.out = post >= 0 ? P.layers[post].top : P.layers[lrn].top;
+          op.out_dtype = post >= 0 ? P.layers[post].mo_type : QNB_FP32;
+          break;
+        }
+        if (l.kind == QNB_LAYER_POOL) {
+          op.kind = OP_POOL;
+          break;
+        }
+        if (l.kind == QNB_LAYER_QUANTIZER) {
+          const int j = sole_consumer(P, l.top);
+          if (is_q2f(l) && j >= 0 && P.layers[j].kind == QNB_LAYER_SOFTMAX) {
+            done[j] = true;
+            op.kind = OP_SOFTMAX;
+            op.in_dtype = l.mi_type;
+            op.out = P.layers[j].top;
+            break;
+          }
+          op.kind = OP_CONVERT;
+          op.in_dtype = l.mi_type;
+          op.out_dtype = l.mo_type;
+          op.conv_op = (is_quant(l.mi_type) && is_quant(l.mo_type)) ? CVT_REQUANT : CVT_CONVERT;
+          break;
+        }
+        return fail(QNB_E_ARG, "unreachable lowering state");
+      }
+      case QNB_LAYER_RELU:
+        op.kind = OP_CONVERT;
+        op.in_dtype = l.mi_type;
+        op.out_dtype = l.mo_type;
+        op.conv_op = is_quant(l.d_type) ? CVT_RELU_Q : CVT_RELU_F;
+        break;
+      case QNB_LAYER_SOFTMAX:
+        op.kind = OP_SOFTMAX;
+        op.in_dtype = QNB_FP32;
+        break;
+      case QNB_LAYER_DROPOUT:
+        op.kind = OP_ALIAS;
+        P.blobs[l.top].alias = l.bottom;
+        break;
+      default:
+        return fail(QNB_E_UNSUPPORTED, "layer kind not supported by plans");
+    }
+    P.ops.push_back(op);
+  }
+  return QNB_OK;
+}
+
+qnb_status assign_layouts(qnb_plan& P) {
+  // Each op's input blob (through aliases) gets the layout the op requires.
+  for (const Op& op : P.ops) {
+    if (op.kind == OP_ALIAS || op.kind == OP_PACK) continue;
+    const int r = root_of(P, op.in);
+    Blob& b = P.blobs[r];
+    if (b.external) return fail(QNB_E_ARG, "internal: external blob consumed by a device op");
+    ActLayout L = required_input_layout(P, op, P.blobs[op.in]);
+    if (b.layout_set) {
+      if (L.hh != b.L.hh || L.hw != b.L.hw || L.c_phys != b.L.c_phys || L.wx != b.L.wx)
+        return fail(QNB_E_UNSUPPORTED, "conflicting layout requirements");
+    }
+    b.L = L;
+    b.layout_set = true;
+    b.needs_buffer = true;
+  }
+  for (const Op& op : P.ops) {
+    if (op.kind == OP_ALIAS) continue;
+    const int r = root_of(P, op.out);
+    Blob& b = P.blobs[r];
+    if (!b.layout_set) {
+      b.L = plain_layout(b, P.max_batch);
+      b.layout_set = true;
+    }
+    b.needs_buffer = true;
+  }
+  // softmax writes the user's output directly: no buffer for the sink then
+  return QNB_OK;
+}
+
+qnb_status dev_alloc(qnb_plan& P, void** p, size_t bytes) {
+  QNB_CUDA(cudaMalloc(p, bytes ? bytes : 16));
+  P.weight_allocs.push_back(*p);
+  P.weight_bytes += bytes;
+  return QNB_OK;
+}
+
+template <typename T>
+qnb_status upload(qnb_plan& P, const std::vector<T>& v, T** dst) {
+  void* p = nullptr;
+  QNB_TRY(dev_alloc(P, &p, v.size() * sizeof(T)));
+  QNB_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *dst = (T*)p;
+  return QNB_OK;
+}
+
+uint8_t* blob_ptr(qnb_plan& P, int b) { return P.arena + P.blobs[root_of(P, b)].off; }
+const ActLayout& blob_layout(qnb_plan& P, int b) { return P.blobs[root_of(P, b)].L; }
+
+qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
+  const qnb_layer_desc& l = P.layers[op.layer];
+  const Blob& in = P.blobs[op.in];
+  const Blob& conv_out = P.blobs[l.top];
+  const ActLayout& Lin = blob_layout(P, op.in);
+  const ActLayout& Lout = blob_layout(P, op.out);
+  IgemmGeometry g = geometry_of(l, in, conv_out);
+  const int dtype = l.d_type;
+  const bool quant = is_quant(dtype);
+  if (!l.weight) return fail(QNB_E_ARG, "missing parameter: weight");
+  if (quant && (l.weight_dtype != dtype || !l.weight_has_qv))
+    return fail(QNB_E_QVALS, "quantizer not finalized: weight of layer " + std::to_string(op.layer));
+  if (quant && !in.has_qv) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
+  IgemmPacked pk;
+  QNB_TRY(igemm_plan_k(g, Lin, &pk));
+  if (g.is_fc) pk.n_per_tile = 128;
+  QNB_TRY(igemm_pack_b(g, l.weight, l.weight_dtype, &pk));
+  IgemmArgs& a = st.ig;
+  std::memset(&a, 0, sizeof(a));
+  a.a = blob_ptr(P, op.in);
+  a.a_img = Lin.img();
+  a.a_row = Lin.row();
+  a.a_pix = Lin.pix();
+  a.a_group = g.cg * Lin.es();
+  a.a_origin = (Lin.hh - g.ph) * Lin.row() + (Lin.hw - g.pw) * Lin.pix();
+  a.stride_h = (int32_t)g.sh;
+  a.stride_w = (int32_t)g.sw;
+  a.oh = (int32_t)g.oh;
+  a.ow = (int32_t)g.ow;
+  a.m_total = P.max_batch * g.oh * g.ow;
+  a.num_kb = pk.num_kb;
+  a.n_rows = pk.n_rows;
+  a.n_tiles = pk.n_tiles;
+  a.n_real = (int32_t)g.og;
+  a.n_per_tile = pk.n_per_tile;
+  a.ones_col = pk.ones_col;
+  a.tmem_cols = pk.tmem_cols;
+  QNB_TRY(upload(P, pk.chunk_off, const_cast<int32_t**>(&a.chunk_off)));
+  QNB_TRY(upload(P, pk.b, const_cast<uint8_t**>(&a.b)));
+  const int64_t K = g.is_fc ? g.fc_c * g.fc_h * g.fc_w : g.cg * g.kh * g.kw;
+  const int64_t OC = g.groups * g.og;
+  if (quant) {
+    const qnb_qvals& qw = l.weight_qv;
+    const qnb_qvals& qx = in.qv;
+    const qnb_qvals& qa = g.is_fc ? qx : qw;  // src/ops.cpp:303-306 vs 428-431
+    const qnb_qvals& qb = g.is_fc ? qw : qx;
+    qnb_requant rq;
+    QNB_TRY(requant_from_ratio(qa.scale * qb.scale / conv_out.qv.scale, qa.zero, conv_out.qv,
+                               default_shift_bits(dtype), &rq));
+    a.rq = to_dev(rq);
+    a.zw = qw.zero;
+    const uint8_t* w = (const uint8_t*)l.weight;
+    std::vector<int64_t> cc((size_t)OC);
+    for (int64_t oc = 0; oc < OC; ++oc) {
+      int64_t wsum = 0;
+      for (int64_t k = 0; k < K; ++k) wsum += w[g.is_fc ? k * OC + oc : oc * K + k];
+      int64_t c = K * (int64_t)qx.zero * qw.zero - (int64_t)qx.zero * wsum;
+      if (l.bias_term && l.bias) c += bias_to_acc(l.bias[oc], qa.scale, qb.scale);
+      cc[(size_t)oc] = c;
+    }
+    QNB_TRY(upload(P, cc, const_cast<int64_t**>(&a.chan_const)));
+    a.epi = EPI_Q8;
+    if (op.relu >= 0) {
+      const Blob& rtop = P.blobs[P.layers[op.relu].top];
+      qnb_requant r2;
+      QNB_TRY(requant_from_ratio(conv_out.qv.scale / rtop.qv.scale, conv_out.qv.zero, rtop.qv,
+                                 default_shift_bits(dtype), &r2));
+      a.relu = to_dev_relu(r2, dtype);
+      a.has_relu = 1;
+    }
+  } else {
+    if (l.bias_term && l.bias) {
+      std::vector<float> b(l.bias, l.bias + OC);
+      QNB_TRY(upload(P, b, const_cast<float**>(&a.bias)));
+    }
+    a.epi = dtype == QNB_FP16 ? EPI_F16 : EPI_F32;
+    if (op.relu >= 0) {
+      a.has_relu = 1;
+      a.slope = P.layers[op.relu].negative_slope;
+    }
+  }
+  a.out = blob_ptr(P, op.out);
+  a.o_img = Lout.img();
+  a.o_row = Lout.row();
+  a.o_pix = Lout.pix();
+  a.o_origin = Lout.interior_offset();
+  a.o_es = (int32_t)Lout.es();
+  a.o_vec = (Lout.pix() % 16 == 0 && Lout.row() % 16 == 0 && Lout.interior_offset() % 16 == 0 &&
+             (g.og * a.o_es) % 16 == 0 && (pk.n_per_tile * a.o_es) % 16 == 0)
+                ? 1
+                : 0;
+  st.kind = OP_IGEMM;
+  st.mma_kind = g.kind;
+  st.groups = g.groups;
+  st.rows_per_img = g.oh * g.ow;
+  return QNB_OK;
+}
+
+qnb_status emit(qnb_plan& P) {
+  for (const Op& op : P.ops) {
+    if (op.kind == OP_ALIAS) continue;
+    Step st;
+    st.kind = op.kind;
+    const bool to_sink = root_of(P, op.out) == P.sink_blob;
+    switch (op.kind) {
+      case OP_PACK: {
+        const Blob& src = P.blobs[op.in];
+        const Blob& dst = P.blobs[op.out];
+        PackArgs& p = st.pack;
+        p.src = nullptr;
+        st.src_sym = SYM_INPUT;
+        p.src_dtype = src.dtype;
+        if (src.dtype != QNB_FP32 && src.dtype != QNB_FP16)
+          return fail(QNB_E_UNSUPPORTED, "quantized INPUT blobs");
+        p.N = P.max_batch;
+        p.C = src.c;
+        p.H = src.h;
+        p.W = src.w;
+        p.dst = blob_ptr(P, op.out);
+        p.L = dev_layout(blob_layout(P, op.out));
+        p.dst_dtype = dst.dtype;
+        p.op = op.pack_op;
+        p.q = dst.has_qv ? dev_q(dst.qv) : DevQ{1.0, 1.0, 0, 0, 0};
+        p.fill = dst.has_qv ? (double)dst.qv.zero : 0.0;
+        break;
+      }
+      case OP_IGEMM:
+        QNB_TRY(emit_igemm(P, op, st));
+        break;
+      case OP_POOL: {
+        const qnb_layer_desc& l = P.layers[op.layer];
+        st.pool.src = blob_ptr(P, op.in);
+        st.pool.S = dev_layout(blob_layout(P, op.in));
+        st.pool.dst = blob_ptr(P, op.out);
+        st.pool.D = dev_layout(blob_layout(P, op.out));
+        st.pool.dtype = l.mi_type;
+        st.pool.k = l.pool_kernel;
+        st.pool.s = l.pool_stride;
+        break;
+      }
+      case OP_POOL_LRN: {
+        const qnb_layer_desc& lr = P.layers[op.lrn];
+        PoolLrnArgs& a = st.plrn;
+        a.src = blob_ptr(P, op.in);
+        a.S = dev_layout(blob_layout(P, op.in));
+        a.dst = blob_ptr(P, op.out);
+        a.D = dev_layout(blob_layout(P, op.out));
+        a.in_dtype = op.in_dtype;
+        a.out_dtype = op.out_dtype;
+        const Blob& bi = P.blobs[op.in];
+        const Blob& bo = P.blobs[op.out];
+        a.in_q = bi.has_qv ? dev_q(bi.qv) : DevQ{1.0, 1.0, 0, 0, 0};
+        a.out_q = bo.has_qv ? dev_q(bo.qv) : DevQ{1.0, 1.0, 0, 0, 0};
+        if (op.pool >= 0) {
+          a.pool_k = P.layers[op.pool].pool_kernel;
+          a.pool_s = P.layers[op.pool].pool_stride;
+        } else {
+          a.pool_k = 0;
+          a.pool_s = 1;
+        }
+        if (bo.c > 512) return fail(QNB_E_UNSUPPORTED, "LRN over more than 512 channels");
+        a.half = (lr.lrn_local_size - 1) / 2;
+        a.a_n = lr.lrn_alpha / (double)lr.lrn_local_size;
+        a.beta = lr.lrn_beta;
+        a.k = lr.lrn_k;
+        break;
+      }
+      case OP_CONVERT: {
+        const qnb_layer_desc& l = P.layers[op.layer];
+        ConvertArgs& a = st.cvt;
+        std::memset(&a, 0, sizeof(a));
+        a.src = blob_ptr(P, op.in);
+        a.S = dev_layout(blob_layout(P, op.in));
+        a.dst = blob_ptr(P, op.out);
+        a.D = dev_layout(blob_layout(P, op.out));
+        a.op = op.conv_op;
+        a.in_dtype = op.in_dtype;
+        a.out_dtype = op.out_dtype;
+        const Blob& bi = P.blobs[op.in];
+        const Blob& bo = P.blobs[op.out];
+        a.in_q = bi.has_qv ? dev_q(bi.qv) : DevQ{1.0, 1.0, 0, 0, 0};
+        a.out_q = bo.has_qv ? dev_q(bo.qv) : DevQ{1.0, 1.0, 0, 0, 0};
+        if (op.conv_op == CVT_REQUANT || op.conv_op == CVT_RELU_Q) {
+          qnb_requant rq;
+          QNB_TRY(requant_from_ratio(bi.qv.scale / bo.qv.scale, bi.qv.zero, bo.qv,
+                                     default_shift_bits(op.conv_op == CVT_REQUANT ? l.mo_type : l.d_type), &rq));
+          a.rq = to_dev(rq);
+          a.in_zero = rq.in_zero;
+          a.relu = to_dev_relu(rq, l.d_type);
+        }
+        a.slope = l.negative_slope;
+        break;
+      }
+      case OP_SOFTMAX: {
+        const Blob& bi = P.blobs[op.in];
+        st.sm_src = blob_ptr(P, op.in);
+        st.sm_S = dev_layout(blob_layout(P, op.in));
+        st.sm_dtype = op.in_dtype;
+        st.sm_q = bi.has_qv ? dev_q(bi.qv) : DevQ{1.0, 1.0, 0, 0, 0};
+        st.sm_F = bi.c * bi.h * bi.w;
+        if (bi.h != 1 || bi.w != 1) return fail(QNB_E_UNSUPPORTED, "softmax over 4-D blobs");
+        if (!softmax_smem_ok(st.sm_F)) return fail(QNB_E_UNSUPPORTED, "softmax row too long");
+        if (!to_sink) return fail(QNB_E_UNSUPPORTED, "softmax must be the last layer");
+        st.dst_sym = SYM_OUTPUT;
+        break;
+      }
+      default:
+        break;
+    }
+    P.steps.push_back(st);
+    if (to_sink && op.kind != OP_SOFTMAX) {
+      Step up;
+      up.kind = OP_ALIAS;  // marker kind, unused
+      up.unpack = true;
+      up.up_src = blob_ptr(P, op.out);
+      up.up_S = dev_layout(blob_layout(P, op.out));
+      up.dst_sym = SYM_OUTPUT;
+      P.steps.push_back(up);
+    }
+  }
+  return QNB_OK;
+}
+
+Step with_batch(const Step& s0, int64_t b, const void* in, void* out) {
+  Step s = s0;
+  if (s.src_sym == SYM_INPUT) s.pack.src = (const uint8_t*)in;
+  if (s.dst_sym == SYM_OUTPUT) {
+    s.sm_out = (float*)out;
+    s.up_dst = (uint8_t*)out;
+  }
+  s.ig.m_total = b * s.rows_per_img;
+  s.pack.N = b;
+  s.pack.L.n = b;
+  s.pool.S.n = s.pool.D.n = b;
+  s.plrn.S.n = s.plrn.D.n = b;
+  s.cvt.S.n = s.cvt.D.n = b;
+  s.sm_S.n = b;
+  s.up_S.n = b;
+  return s;
+}
+
+qnb_status launch_steps(qnb_plan& P, int64_t b, const void* in, void* out, cudaStream_t s) {
+  for (const Step& s0 : P.steps) {
+    const Step st = with_batch(s0, b, in, out);
+    if (st.unpack) {
+      launch_unpack(st.up_src, st.up_S, st.up_dst, s);
+    } else {
+      switch (st.kind) {
+        case OP_PACK:
+          launch_pack_input(st.pack, s);
+          break;
+        case OP_IGEMM:
+          QNB_TRY(igemm_launch(st.mma_kind, st.ig, st.groups, s));
+          g_launches.fetch_sub(1);  // counted below with the others
+          break;
+        case OP_POOL:
+          launch_pool(st.pool, s);
+          break;
+        case OP_POOL_LRN:
+          launch_pool_lrn(st.plrn, s);
+          break;
+        case OP_CONVERT:
+          launch_convert(st.cvt, s);
+          break;
+        case OP_SOFTMAX:
+          launch_softmax_rows(st.sm_src, st.sm_S, st.sm_dtype, st.sm_q, st.sm_out, st.sm_F, b, s);
+          break;
+        default:
+          break;
+      }
+    }
+    QNB_CUDA(cudaGetLastError());
+  }
+  return QNB_OK;
+}
+
+}  // namespace
+}  // namespace qnb
+
+using namespace qnb;
+
+extern "C" {
+
+qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32_t n_blobs, const qnb_plan_opts* opts,
+                           qnb_plan** out) {
+  QNB_TRY(ensure_device());
+  if (!layers || n_layers <= 0 || !out) return fail(QNB_E_ARG, "empty graph");
+  auto P = std::make_unique<qnb_plan>();
+  P->layers.assign(layers, layers + n_layers);
+  P->blobs.resize((size_t)n_blobs);
+  P->max_batch = opts && opts->max_batch > 0 ? opts->max_batch : 1;
+  P->use_graph = opts ? opts->use_cuda_graph != 0 : true;
+  QNB_CUDA(cudaGetDevice(&P->device));
+  QNB_TRY(build_blob_table(*P));
+  QNB_TRY(lower(*P));
+  QNB_TRY(assign_layouts(*P));
+  // arena
+  size_t off = 0;
+  for (size_t b = 0; b < P->blobs.size(); ++b) {
+    Blob& bl = P->blobs[b];
+    if (!bl.needs_buffer || bl.alias >= 0 || bl.external) continue;
+    if ((int)b == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) continue;
+    bl.off = off;
+    off += round_up((int64_t)bl.L.bytes() + 1024, 256);
+  }
+  P->arena_bytes = off;
+  if (off) QNB_CUDA(cudaMalloc((void**)&P->arena, off));
+  for (size_t b = 0; b < P->blobs.size(); ++b) {
+    Blob& bl = P->blobs[b];
+    if (!bl.needs_buffer || bl.alias >= 0 || bl.external) continue;
+    if ((int)b == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) continue;
+    QNB_TRY(fill_buffer(P->arena + bl.off, bl.L.bytes() + 1024, bl.dtype, bl.has_qv ? bl.qv.zero : 0, 0));
+  }
+  QNB_TRY(emit(*P));
+  QNB_CUDA(cudaDeviceSynchronize());
+  // output description (reference layout)
+  const Blob& sk = P->blobs[P->sink_blob];
+  P->out_dtype = sk.dtype;
+  P->out_ndim = sk.ndim;
+  P->out_shape[0] = P->max_batch;
+  P->out_shape[1] = sk.c;
+  P->out_shape[2] = sk.h;
+  P->out_shape[3] = sk.w;
+  P->out_bytes_per_sample = sk.c * sk.h * sk.w * (int64_t)dtype_size(sk.dtype);
+  const Blob& ib = P->blobs[P->input_blob];
+  P->in_bytes_per_sample = ib.c * ib.h * ib.w * (int64_t)dtype_size(ib.dtype);
+  *out = P.release();
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32_t input_on_host, void* output,
+                            int32_t output_on_host, qnb_stream s_) {
+  if (!P) return fail(QNB_E_ARG, "null plan");
+  if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
+  cudaStream_t s = as_stream(s_);
+  const void* in_dev = input;
+  void* out_dev = output;
+  if (input_on_host) {
+    if (!P->in_staging) QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
+    QNB_CUDA(cudaMemcpyAsync(P->in_staging, input, (size_t)(P->in_bytes_per_sample * batch), cudaMemcpyHostToDevice, s));
+    in_dev = P->in_staging;
+  }
+  if (output_on_host) {
+    if (!P->out_staging) QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
+    out_dev = P->out_staging;
+  }
+  if (P->use_graph) {
+    if (!P->exec || P->g_in != in_dev || P->g_out != out_dev || P->g_batch != batch) {
+      if (P->exec) {
+        cudaGraphExecDestroy(P->exec);
+        P->exec = nullptr;
+      }
+      cudaGraph_t graph;
+      if (!P->capture_stream) QNB_CUDA(cudaStreamCreateWithFlags(&P->capture_stream, cudaStreamNonBlocking));
+      QNB_CUDA(cudaStreamBeginCapture(P->capture_stream, cudaStreamCaptureModeThreadLocal));
+      qnb_status st = launch_steps(*P, batch, in_dev, out_dev, P->capture_stream);
+      cudaError_t e = cudaStreamEndCapture(P->capture_stream, &graph);
+      if (st != QNB_OK) return st;
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      e = cudaGraphInstantiate(&P->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      P->g_in = in_dev;
+      P->g_out = out_dev;
+      P->g_batch = batch;
+    }
+    QNB_CUDA(cudaGraphLaunch(P->exec, s));
+  } else {
+    QNB_TRY(launch_steps(*P, batch, in_dev, out_dev, s));
+  }
+  count_launch((uint64_t)P->steps.size());
+  if (output_on_host)
+    QNB_CUDA(cudaMemcpyAsync(output, out_dev, (size_t)(P->out_bytes_per_sample * batch), cudaMemcpyDeviceToHost, s));
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_output_info(const qnb_plan* P, int32_t* dtype, int32_t* ndim, int64_t shape[4]) {
+  if (!P) return fail(QNB_E_ARG, "null plan");
+  *dtype = P->out_dtype;
+  *ndim = P->out_ndim;
+  for (int i = 0; i < 4; ++i) shape[i] = P->out_shape[i];
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_blob_info(const qnb_plan* P, int32_t blob, void** dev_ptr, int64_t layout[8]) {
+  if (!P || blob < 0 || blob >= (int)P->blobs.size()) return fail(QNB_E_ARG, "blob id out of range");
+  int r = blob;
+  while (P->blobs[r].alias >= 0) r = P->blobs[r].alias;
+  const Blob& b = P->blobs[r];
+  const bool has = b.needs_buffer && !b.external && !(r == P->sink_blob && P->ops.back().kind == OP_SOFTMAX);
+  *dev_ptr = has ? (void*)(P->arena + b.off) : nullptr;
+  const int64_t v[8] = {b.L.n, b.L.h, b.L.w, b.L.c_phys, b.L.hh, b.L.hw, b.L.wx, (int64_t)b.L.es()};
+  for (int i = 0; i < 8; ++i) layout[i] = v[i];
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_stats(const qnb_plan* P, int64_t* kernels, int64_t* arena, int64_t* weights) {
+  if (!P) return fail(QNB_E_ARG, "null plan");
+  if (kernels) *kernels = (int64_t)P->steps.size();
+  if (arena) *arena = (int64_t)P->arena_bytes;
+  if (weights) *weights = (int64_t)P->weight_bytes;
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_destroy(qnb_plan* P) {
+  if (!P) return QNB_OK;
+  if (P->exec) cudaGraphExecDestroy(P->exec);
+  if (P->capture_stream) cudaStreamDestroy(P->capture_stream);
+  if (P->arena) cudaFree(P->arena);
+  for (void* p : P->weight_allocs) cudaFree(p);
+  if (P->in_staging) cudaFree(P->in_staging);
+  if (P->out_staging) cudaFree(P->out_staging);
+  delete P;
+  return QNB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,425 @@
+// Memory-bound kernels of the compiled plan, all operating on device-native NHWC
+// activations (optional zero-point halo, padded channels):
+//
+//   pack_input     FP32 NCHW batch -> quantize / cast / copy -> NHWC (conv1's layout)
+//                  (src/quantizer.cpp:115-126 + the layout change, one HBM pass)
+//   pool           max-pool NHWC (src/ops.cpp:344-390), 16-byte vectors for u8
+//   pool_lrn       pool -> dequant/cast -> LRN (double) -> quantize/cast, one pass
+//                  (src/ops.cpp:344-390, 469-497; src/quantizer.cpp:103-139)
+//   convert        generic elementwise QUANTIZER / RELU between layouts
+//   softmax_rows   [dequant ->] softmax over rows (src/ops.cpp:445-467)
+//   unpack         NHWC -> NCHW for sinks
+#include <cuda_fp16.h>
+
+#include "qnb_device.cuh"
+#include "qnb_internal.h"
+#include "qnb_plan_kernels.h"
+
+namespace qnb {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint16_t f2h_bits(float x) {
+  const uint32_t b = __float_as_uint(x);
+  if ((b & 0x7F800000u) == 0x7F800000u && (b & 0x7FFFFFu) != 0) {
+    const uint16_t pl = (uint16_t)((b & 0x7FFFFFu) >> 13);
+    return (uint16_t)(((b >> 16) & 0x8000u) | 0x7C00u | (pl ? pl : 1u));
+  }
+  return __half_as_ushort(__float2half_rn(x));
+}
+__device__ __forceinline__ float h2f_bits(uint16_t h) {
+  if ((h & 0x7C00u) == 0x7C00u && (h & 0x3FFu) != 0)
+    return __uint_as_float(((uint32_t)(h & 0x8000u) << 16) | 0x7F800000u | ((uint32_t)(h & 0x3FFu) << 13));
+  return __half2float(__ushort_as_half(h));
+}
+
+// quantize_value (src/quantizer.cpp:103-109); exact division near rounding ties.
+__device__ __forceinline__ int64_t qz(float x, const DevQ& q) {
+  double y = __dmul_rn((double)x, q.inv);
+  const double frac = y - floor(y);
+  if (fabs(frac - 0.5) < 1e-9 * fmax(1.0, fabs(y)) || !(fabs(y) < 1e15)) y = __ddiv_rn((double)x, q.scale);
+  const double v = __dadd_rn(rint(y), (double)q.zero);
+  if (isnan(v)) return q.zero;
+  if (v <= (double)q.i_min) return q.i_min;
+  if (v >= (double)q.i_max) return q.i_max;
+  return (int64_t)v;
+}
+__device__ __forceinline__ float dq(int64_t v, const DevQ& q) {
+  return __double2float_rn(__dmul_rn((double)(v - q.zero), q.scale));
+}
+
+// Loads element c of a pixel as float (dequantizing integers with q).
+__device__ __forceinline__ float load_as_float(const uint8_t* p, int dtype, const DevQ& q) {
+  switch (dtype) {
+    case QNB_FP32:
+      return *reinterpret_cast<const float*>(p);
+    case QNB_FP16:
+      return h2f_bits(*reinterpret_cast<const uint16_t*>(p));
+    case QNB_INT8Q:
+      return dq(*p, q);
+    default:
+      return dq(*reinterpret_cast<const uint16_t*>(p), q);
+  }
+}
+__device__ __forceinline__ int64_t load_raw_int(const uint8_t* p, int dtype) {
+  return dtype == QNB_INT8Q ? (int64_t)*p : (int64_t) * reinterpret_cast<const uint16_t*>(p);
+}
+// Stores a float into dtype (quantizing with q for integer types).
+__device__ __forceinline__ void store_from_float(uint8_t* p, int dtype, float v, const DevQ& q) {
+  switch (dtype) {
+    case QNB_FP32:
+      *reinterpret_cast<float*>(p) = v;
+      break;
+    case QNB_FP16:
+      *reinterpret_cast<uint16_t*>(p) = f2h_bits(v);
+      break;
+    case QNB_INT8Q:
+      *p = (uint8_t)qz(v, q);
+      break;
+    default:
+      *reinterpret_cast<uint16_t*>(p) = (uint16_t)qz(v, q);
+  }
+}
+
+__device__ __forceinline__ uint8_t* at(uint8_t* base, const DevLayout& L, int64_t n, int64_t y, int64_t x) {
+  return base + n * L.img + y * L.row + x * L.pix + L.origin;
+}
+__device__ __forceinline__ const uint8_t* at(const uint8_t* base, const DevLayout& L, int64_t n, int64_t y,
+                                             int64_t x) {
+  return base + n * L.img + y * L.row + x * L.pix + L.origin;
+}
+
+// ------------------------------------------------------------- pack_input
+// One thread per interior pixel: reads C channel planes (coalesced along x),
+// writes the pixel's c_phys elements (padding channels get `fill`).
+__global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype, int64_t N, int64_t C, int64_t H,
+                                  int64_t W, uint8_t* __restrict__ dst, DevLayout L, int dst_dtype, int op, DevQ q,
+                                  double fill) {
+  const int64_t total = N * H * W;
+  const int64_t plane = H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % W, y = (i / W) % H, n = i / plane;
+    uint8_t* o = at(dst, L, n, y, x);
+    const uint8_t* s = src + ((n * C) * plane + y * W + x) * (int64_t)(src_dtype == QNB_FP32 ? 4 : 2);
+    if (dst_dtype == QNB_INT8Q && L.c_phys <= 16 && (L.c_phys & 3) == 0) {
+      uint32_t words[4] = {0, 0, 0, 0};
+      for (int c = 0; c < L.c_phys; ++c) {
+        uint32_t v = (uint32_t)(int64_t)fill;
+        if (c < C) {
+          const float f = src_dtype == QNB_FP32 ? reinterpret_cast<const float*>(s)[c * plane]
+                                                : h2f_bits(reinterpret_cast<const uint16_t*>(s)[c * plane]);
+          v = (uint32_t)qz(f, q);
+        }
+        words[c >> 2] |= (v & 0xFFu) << (8 * (c & 3));
+      }
+      for (int w4 = 0; w4 < (L.c_phys >> 2); ++w4) reinterpret_cast<uint32_t*>(o)[w4] = words[w4];
+      continue;
+    }
+    for (int64_t c = 0; c < L.c_phys; ++c) {
+      uint8_t* oc = o + c * L.es;
+      if (c >= C) {
+        if (dst_dtype == QNB_INT8Q) *oc = (uint8_t)(int64_t)fill;
+        else if (dst_dtype == QNB_INT16Q) *reinterpret_cast<uint16_t*>(oc) = (uint16_t)(int64_t)fill;
+        else if (dst_dtype == QNB_FP16) *reinterpret_cast<uint16_t*>(oc) = 0;
+        else *reinterpret_cast<float*>(oc) = 0.0f;
+        continue;
+      }
+      const float f = src_dtype == QNB_FP32 ? reinterpret_cast<const float*>(s)[c * plane]
+                                            : h2f_bits(reinterpret_cast<const uint16_t*>(s)[c * plane]);
+      if (op == PACK_COPY && dst_dtype == QNB_FP16 && src_dtype == QNB_FP16)
+        *reinterpret_cast<uint16_t*>(oc) = reinterpret_cast<const uint16_t*>(s)[c * plane];
+      else
+        store_from_float(oc, dst_dtype, f, q);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pool
+// Max over k x k windows (no padding).  Integer types compare raw values; float
+// types keep the first element unless a later one is strictly greater.
+__global__ void pool_u8_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst, DevLayout D,
+                               int64_t k, int64_t st) {
+  const int64_t chunks = S.c_phys / 16;
+  const int64_t total = D.n * D.h * D.w * chunks;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ch = i % chunks, pix = i / chunks;
+    const int64_t ox = pix % D.w, oy = (pix / D.w) % D.h, n = pix / (D.w * D.h);
+    uint4 m = make_uint4(0, 0, 0, 0);
+    for (int64_t ky = 0; ky < k; ++ky) {
+      const int64_t iy = oy * st + ky;
+      if (iy >= S.h) continue;
+      for (int64_t kx = 0; kx < k; ++kx) {
+        const int64_t ix = ox * st + kx;
+        if (ix >= S.w) continue;
+        const uint4 v = *reinterpret_cast<const uint4*>(at(src, S, n, iy, ix) + ch * 16);
+        m.x = __vmaxu4(m.x, v.x);
+        m.y = __vmaxu4(m.y, v.y);
+        m.z = __vmaxu4(m.z, v.z);
+        m.w = __vmaxu4(m.w, v.w);
+      }
+    }
+    *reinterpret_cast<uint4*>(at(dst, D, n, oy, ox) + ch * 16) = m;
+  }
+}
+
+__global__ void pool_generic_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst,
+                                    DevLayout D, int dtype, int64_t k, int64_t st) {
+  const int64_t total = D.n * D.h * D.w * D.c;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % D.c, pix = i / D.c;
+    const int64_t ox = pix % D.w, oy = (pix / D.w) % D.h, n = pix / (D.w * D.h);
+    int64_t bq = 0;
+    float bf = 0.0f;
+    uint16_t bh = 0;
+    bool first = true;
+    for (int64_t ky = 0; ky < k; ++ky)
+      for (int64_t kx = 0; kx < k; ++kx) {
+        const int64_t iy = oy * st + ky, ix = ox * st + kx;
+        if (iy >= S.h || ix >= S.w) continue;
+        const uint8_t* p = at(src, S, n, iy, ix) + c * S.es;
+        if (dtype == QNB_INT8Q || dtype == QNB_INT16Q) {
+          const int64_t v = load_raw_int(p, dtype);
+          if (first || v > bq) bq = v;
+        } else if (dtype == QNB_FP32) {
+          const float v = *reinterpret_cast<const float*>(p);
+          if (first || v > bf) bf = v;
+        } else {
+          const uint16_t hv = *reinterpret_cast<const uint16_t*>(p);
+          const float v = h2f_bits(hv);
+          if (first || v > bf) {
+            bf = v;
+            bh = hv;
+          }
+        }
+        first = false;
+      }
+    uint8_t* o = at(dst, D, n, oy, ox) + c * D.es;
+    if (dtype == QNB_INT8Q) *o = (uint8_t)bq;
+    else if (dtype == QNB_INT16Q) *reinterpret_cast<uint16_t*>(o) = (uint16_t)bq;
+    else if (dtype == QNB_FP32) *reinterpret_cast<float*>(o) = bf;
+    else *reinterpret_cast<uint16_t*>(o) = bh;  // max is an input element: keep its bits
+  }
+}
+
+// --------------------------------------------------------------- pool_lrn
+// One warp per output pixel.  Stage 1: (optional) pool each channel and convert it
+// to FP32 exactly as the reference's QUANTIZER / cast would; stage 2: across-channel
+// LRN in double with the reference's summation order, then the output conversion.
+// For integer outputs a float fast path decides the integer unless the value lies
+// within a conservative error bound of a rounding boundary, in which case the exact
+// double computation (pow) runs; the result is bit-identical either way.
+constexpr int kLrnMaxC = 512;
+constexpr int kLrnWarps = 4;
+
+__global__ void __launch_bounds__(32 * kLrnWarps) pool_lrn_kernel(PoolLrnArgs a) {
+  __shared__ float sx[kLrnWarps][kLrnMaxC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = a.D.n * a.D.h * a.D.w;
+  const int64_t C = a.D.c;
+  for (int64_t pix = (int64_t)blockIdx.x * kLrnWarps + warp; pix < total; pix += (int64_t)gridDim.x * kLrnWarps) {
+    const int64_t ox = pix % a.D.w, oy = (pix / a.D.w) % a.D.h, n = pix / (a.D.w * a.D.h);
+    for (int64_t c = lane; c < C; c += 32) {
+      float v;
+      if (a.pool_k > 0) {
+        int64_t bq = 0;
+        float bf = 0.0f;
+        bool first = true;
+        for (int64_t ky = 0; ky < a.pool_k; ++ky)
+          for (int64_t kx = 0; kx < a.pool_k; ++kx) {
+            const int64_t iy = oy * a.pool_s + ky, ix = ox * a.pool_s + kx;
+            if (iy >= a.S.h || ix >= a.S.w) continue;
+            const uint8_t* p = at(a.src, a.S, n, iy, ix) + c * a.S.es;
+            if (a.in_dtype == QNB_INT8Q || a.in_dtype == QNB_INT16Q) {
+              const int64_t q = load_raw_int(p, a.in_dtype);
+              if (first || q > bq) bq = q;
+            } else {
+              const float f = load_as_float(p, a.in_dtype, a.in_q);
+              if (first || f > bf) bf = f;
+            }
+            first = false;
+          }
+        v = (a.in_dtype == QNB_INT8Q || a.in_dtype == QNB_INT16Q) ? dq(bq, a.in_q) : bf;
+      } else {
+        v = load_as_float(at(a.src, a.S, n, oy, ox) + c * a.S.es, a.in_dtype, a.in_q);
+      }
+      sx[warp][c] = v;
+    }
+    __syncwarp();
+    uint8_t* obase = at(a.dst, a.D, n, oy, ox);
+    for (int64_t c = lane; c < C; c += 32) {
+      const int64_t c0 = c - a.half < 0 ? 0 : c - a.half;
+      const int64_t c1 = c + a.half > C - 1 ? C - 1 : c + a.half;
+      const float x = sx[warp][c];
+      bool done = false;
+      if (a.out_dtype == QNB_INT8Q || a.out_dtype == QNB_INT16Q) {
+        // float estimate of t = lrn(x) / scale
+        float sf = 0.0f;
+        for (int64_t cc = c0; cc <= c1; ++cc) sf = __fadd_rn(sf, __fmul_rn(sx[warp][cc], sx[warp][cc]));
+        const float base = __fadd_rn((float)a.k, __fmul_rn((float)a.a_n, sf));
+        const float den = exp2f(__fmul_rn((float)a.beta, __log2f(base)));
+        const float t = __fdiv_rn(__fdiv_rn(x, den), (float)a.out_q.scale);
+        const float fl = floorf(t);
+        const float margin = 4e-5f * fabsf(t) + 1e-5f;
+        if (isfinite(t) && fabsf(t - fl - 0.5f) > margin && fabsf(t) < 1e6f && base > 0.0f) {
+          double v = (double)rintf(t) + (double)a.out_q.zero;
+          int64_t q = v <= (double)a.out_q.i_min ? a.out_q.i_min : (v >= (double)a.out_q.i_max ? a.out_q.i_max : (int64_t)v);
+          if (a.out_dtype == QNB_INT8Q) obase[c] = (uint8_t)q;
+          else reinterpret_cast<uint16_t*>(obase)[c] = (uint16_t)q;
+          done = true;
+        }
+      }
+      if (!done) {
+        double sum = 0.0;
+        for (int64_t cc = c0; cc <= c1; ++cc) {
+          const double v = (double)sx[warp][cc];
+          sum = __dadd_rn(sum, __dmul_rn(v, v));
+        }
+        const double base = __dadd_rn(a.k, __dmul_rn(a.a_n, sum));
+        const float y = __double2float_rn(__ddiv_rn((double)x, pow(base, a.beta)));
+        store_from_float(obase + c * a.D.es, a.out_dtype, y, a.out_q);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- convert
+// Generic elementwise op between layouts (interior, real channels only).
+__global__ void convert_kernel(ConvertArgs a) {
+  const int64_t total = a.D.n * a.D.h * a.D.w * a.D.c;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % a.D.c, pix = i / a.D.c;
+    const int64_t x = pix % a.D.w, y = (pix / a.D.w) % a.D.h, n = pix / (a.D.w * a.D.h);
+    const uint8_t* s = at(a.src, a.S, n, y, x) + c * a.S.es;
+    uint8_t* d = at(a.dst, a.D, n, y, x) + c * a.D.es;
+    switch (a.op) {
+      case CVT_REQUANT: {
+        const int64_t q = requant_clamp(load_raw_int(s, a.in_dtype) - a.in_zero, a.rq);
+        if (a.out_dtype == QNB_INT8Q) *d = (uint8_t)q;
+        else *reinterpret_cast<uint16_t*>(d) = (uint16_t)q;
+        break;
+      }
+      case CVT_RELU_Q: {
+        const int64_t q = relu_requant(load_raw_int(s, a.in_dtype), a.relu);
+        if (a.out_dtype == QNB_INT8Q) *d = (uint8_t)q;
+        else *reinterpret_cast<uint16_t*>(d) = (uint16_t)q;
+        break;
+      }
+      case CVT_RELU_F: {
+        const float v = load_as_float(s, a.in_dtype, a.in_q);
+        float r;
+        if (v > 0.0f) r = v;
+        else if (isnan(v)) r = __uint_as_float(__float_as_uint(v) | 0x400000u);
+        else {
+          r = __fmul_rn(v, a.slope);
+          if (isnan(r)) r = __uint_as_float(0xFFC00000u);
+        }
+        store_from_float(d, a.out_dtype, r, a.out_q);
+        break;
+      }
+      default: {  // CVT_CONVERT: dequantize / quantize / cast / copy
+        if ((a.in_dtype == QNB_FP16 && a.out_dtype == QNB_FP16) ||
+            ((a.in_dtype == QNB_INT8Q || a.in_dtype == QNB_INT16Q) && a.in_dtype == a.out_dtype)) {
+          if (a.D.es == 1) *d = *s;
+          else *reinterpret_cast<uint16_t*>(d) = *reinterpret_cast<const uint16_t*>(s);
+        } else {
+          store_from_float(d, a.out_dtype, load_as_float(s, a.in_dtype, a.in_q), a.out_q);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ softmax_rows
+// One block per row: [dequantize ->] float max, double exp sum in the reference's
+// order (one thread), float quotient (src/ops.cpp:445-467).
+__global__ void softmax_rows_kernel(const uint8_t* __restrict__ src, DevLayout S, int in_dtype, DevQ q,
+                                    float* __restrict__ out, int64_t F) {
+  extern __shared__ double ex[];
+  float* xv = reinterpret_cast<float*>(ex + F);
+  __shared__ float smax;
+  __shared__ double ssum;
+  const int64_t n = blockIdx.x;
+  const uint8_t* row = at(src, S, n, 0, 0);
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) xv[f] = load_as_float(row + f * S.es, in_dtype, q);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = xv[0];
+    for (int64_t f = 1; f < F; ++f) m = m < xv[f] ? xv[f] : m;
+    smax = m;
+  }
+  __syncthreads();
+  const double m = smax;
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) ex[f] = exp(__dsub_rn((double)xv[f], m));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int64_t f = 0; f < F; ++f) s = __dadd_rn(s, ex[f]);
+    ssum = s;
+  }
+  __syncthreads();
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) out[n * F + f] = __double2float_rn(__ddiv_rn(ex[f], ssum));
+}
+
+// ------------------------------------------------------------------ unpack
+__global__ void unpack_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst) {
+  const int64_t total = S.n * S.c * S.h * S.w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i % S.w, y = (i / S.w) % S.h, c = (i / (S.w * S.h)) % S.c, n = i / (S.w * S.h * S.c);
+    const uint8_t* s = at(src, S, n, y, x) + c * S.es;
+    uint8_t* d = dst + i * S.es;
+    for (int b = 0; b < S.es; ++b) d[b] = s[b];
+  }
+}
+
+// ------------------------------------------------------------ launchers
+static unsigned blocks_for(int64_t n, int threads) {
+  int64_t b = ceil_div(n, threads);
+  if (b < 1) b = 1;
+  if (b > 148 * 64) b = 148 * 64;
+  return (unsigned)b;
+}
+
+void launch_pack_input(const PackArgs& p, cudaStream_t s) {
+  pack_input_kernel<<<blocks_for(p.N * p.H * p.W, 256), 256, 0, s>>>(p.src, p.src_dtype, p.N, p.C, p.H, p.W, p.dst,
+                                                                      p.L, p.dst_dtype, p.op, p.q, p.fill);
+}
+
+void launch_pool(const PoolArgs& p, cudaStream_t s) {
+  if (p.dtype == QNB_INT8Q && p.S.c_phys % 16 == 0 && p.D.c_phys == p.S.c_phys && p.S.c == p.S.c_phys &&
+      p.S.pix % 16 == 0 && p.D.pix % 16 == 0 && p.S.origin % 16 == 0 && p.D.origin % 16 == 0 && p.S.row % 16 == 0 &&
+      p.D.row % 16 == 0) {
+    pool_u8_kernel<<<blocks_for(p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16), 256), 256, 0, s>>>(p.src, p.S, p.dst, p.D,
+                                                                                            p.k, p.s);
+  } else {
+    pool_generic_kernel<<<blocks_for(p.D.n * p.D.h * p.D.w * p.D.c, 256), 256, 0, s>>>(p.src, p.S, p.dst, p.D,
+                                                                                      p.dtype, p.k, p.s);
+  }
+}
+
+void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
+  const int64_t pixels = a.D.n * a.D.h * a.D.w;
+  pool_lrn_kernel<<<blocks_for(ceil_div(pixels, kLrnWarps), 1), 32 * kLrnWarps, 0, s>>>(a);
+}
+
+void launch_convert(const ConvertArgs& a, cudaStream_t s) {
+  convert_kernel<<<blocks_for(a.D.n * a.D.h * a.D.w * a.D.c, 256), 256, 0, s>>>(a);
+}
+
+bool softmax_smem_ok(int64_t F) { return F * 12 <= 200 * 1024; }
+
+void launch_softmax_rows(const uint8_t* src, const DevLayout& S, int in_dtype, const DevQ& q, float* out, int64_t F,
+                         int64_t rows, cudaStream_t s) {
+  const size_t sm = (size_t)F * 12;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(softmax_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  softmax_rows_kernel<<<(unsigned)rows, 256, sm, s>>>(src, S, in_dtype, q, out, F);
+}
+
+void launch_unpack(const uint8_t* src, const DevLayout& S, uint8_t* dst, cudaStream_t s) {
+  unpack_kernel<<<blocks_for(S.n * S.c * S.h * S.w, 256), 256, 0, s>>>(src, S, dst);
+}
+
+}  // namespace qnb

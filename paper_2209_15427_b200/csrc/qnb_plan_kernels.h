@@ -1,0 +1,100 @@
+// Argument blocks of the plan's memory-bound kernels (host <-> device POD).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qnb_internal.h"
+
+namespace qnb {
+
+// NHWC activation view: element (n, y, x, c) lives at
+// base + n*img + y*row + x*pix + origin + c*es.
+struct DevLayout {
+  int64_t n, h, w, c, c_phys;
+  int64_t img, row, pix, origin;
+  int32_t es;
+};
+
+inline DevLayout dev_layout(const ActLayout& L) {
+  DevLayout d;
+  d.n = L.n;
+  d.h = L.h;
+  d.w = L.w;
+  d.c = L.c;
+  d.c_phys = L.c_phys;
+  d.img = L.img();
+  d.row = L.row();
+  d.pix = L.pix();
+  d.origin = L.interior_offset();
+  d.es = (int32_t)L.es();
+  return d;
+}
+
+// Quantizer values as the kernels use them.
+struct DevQ {
+  double scale, inv;
+  int64_t zero, i_min, i_max;
+};
+inline DevQ dev_q(const qnb_qvals& q) { return DevQ{q.scale, 1.0 / q.scale, q.zero, q.i_min, q.i_max}; }
+
+enum PackOp : int { PACK_QUANTIZE = 0, PACK_CAST = 1, PACK_COPY = 2 };
+
+struct PackArgs {
+  const uint8_t* src;  // NCHW
+  int src_dtype;
+  int64_t N, C, H, W;
+  uint8_t* dst;
+  DevLayout L;
+  int dst_dtype, op;
+  DevQ q;
+  double fill;
+};
+
+struct PoolArgs {
+  const uint8_t* src;
+  DevLayout S;
+  uint8_t* dst;
+  DevLayout D;
+  int dtype;
+  int64_t k, s;
+};
+
+struct PoolLrnArgs {
+  const uint8_t* src;
+  DevLayout S;
+  uint8_t* dst;
+  DevLayout D;
+  int in_dtype, out_dtype;
+  DevQ in_q, out_q;
+  int64_t pool_k, pool_s;  // pool_k = 0: no pooling stage
+  int64_t half;
+  double a_n, beta, k;
+};
+
+enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3 };
+
+struct ConvertArgs {
+  const uint8_t* src;
+  DevLayout S;
+  uint8_t* dst;
+  DevLayout D;
+  int op, in_dtype, out_dtype;
+  DevQ in_q, out_q;
+  Requant rq;
+  int64_t in_zero;
+  ReluRequant relu;
+  float slope;
+};
+
+void launch_pack_input(const PackArgs& p, cudaStream_t s);
+void launch_pool(const PoolArgs& p, cudaStream_t s);
+void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s);
+void launch_convert(const ConvertArgs& a, cudaStream_t s);
+bool softmax_smem_ok(int64_t F);
+void launch_softmax_rows(const uint8_t* src, const DevLayout& S, int in_dtype, const DevQ& q, float* out, int64_t F,
+                         int64_t rows, cudaStream_t s);
+void launch_unpack(const uint8_t* src, const DevLayout& S, uint8_t* dst, cudaStream_t s);
+
+}  // namespace qnb

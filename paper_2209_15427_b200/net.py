@@ -1,0 +1,258 @@
+"""Host-side mirror of qnet::Net (include/qnet/net.hpp:44-92) whose forward runs the
+compiled B200 plan (qnb_plan_* in include/qnb.h).
+
+    net = Net(override_precision(alexnet(), "int8"))
+    for name, arr in params.items(): net.set_param(name, arr)
+    for key, (lo, hi) in ranges.items(): net.set_range(key, lo, hi)
+    net.finalize_quantizers()                  # src/net.cpp:211-248
+    net.set_quant_mode(QUANTIZED)              # src/net.cpp:250-275
+    out = net.forward({"data": images})        # src/net.cpp:305-330 -> {"prob": ...}
+
+Parameters, calibration ranges, finalization and the error messages follow the
+reference.  Weight quantization during finalize runs on the GPU (qnb_quantize).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from . import graph as G
+from . import ops
+from ._lib import QnbError, QVals, check
+
+PASSIVE, OBSERVE, PSEUDO, QUANTIZED = 0, 1, 2, 3
+
+
+from ._lib import LayerDesc, PlanOpts  # noqa: E402
+
+
+def _plan_lib():
+    return L.lib()
+
+
+NP_OF = {0: np.float32, 1: np.uint16, 2: np.uint8, 3: np.uint16}
+
+
+class Plan:
+    """A compiled device plan (qnb_plan) for one calibrated chain graph."""
+
+    def __init__(self, descs, n_blobs, keep_alive, max_batch, use_cuda_graph=True, blob_ids=None):
+        self._keep = keep_alive
+        self.max_batch = max_batch
+        self.blob_ids = blob_ids or {}
+        arr = (LayerDesc * len(descs))(*descs)
+        opts = PlanOpts(max_batch, 1 if use_cuda_graph else 0, 0)
+        self.h = C.c_void_p()
+        lib = _plan_lib()
+        check(lib.qnb_plan_create(arr, len(descs), n_blobs, C.byref(opts), C.byref(self.h)))
+        dt, nd = C.c_int32(), C.c_int32()
+        shape = (C.c_int64 * 4)()
+        check(lib.qnb_plan_output_info(self.h, C.byref(dt), C.byref(nd), shape))
+        self.out_dtype, self.out_ndim = dt.value, nd.value
+        self.out_shape = tuple(shape[: nd.value])
+        self._keep = None  # host parameter copies are no longer needed
+
+    def stats(self):
+        k, a, w = C.c_int64(), C.c_int64(), C.c_int64()
+        check(_plan_lib().qnb_plan_stats(self.h, C.byref(k), C.byref(a), C.byref(w)))
+        return {"kernels_per_forward": k.value, "arena_bytes": a.value, "weight_bytes": w.value}
+
+    def forward_host(self, x: np.ndarray) -> np.ndarray:
+        """Host buffers in and out (copies inside the call)."""
+        x = np.ascontiguousarray(x)
+        b = x.shape[0]
+        out = np.empty((b,) + self.out_shape[1:], NP_OF[self.out_dtype])
+        check(_plan_lib().qnb_plan_forward(self.h, x.ctypes.data_as(C.c_void_p), b, 1,
+                                           out.ctypes.data_as(C.c_void_p), 1, None))
+        check(L.lib().qnb_stream_sync(None))
+        return out
+
+    def forward_device(self, in_ptr: int, out_ptr: int, batch: int, stream: int = 0,
+                       in_host: bool = False, out_host: bool = False) -> None:
+        """Raw pointers (device by default), stream-ordered, no synchronisation."""
+        check(_plan_lib().qnb_plan_forward(self.h, C.c_void_p(in_ptr), batch, 1 if in_host else 0,
+                                           C.c_void_p(out_ptr), 1 if out_host else 0, C.c_void_p(stream)))
+
+    def blob(self, name: str, shape=None):
+        """Reads a materialised blob's interior back (NHWC -> reference NCHW)."""
+        ptr = C.c_void_p()
+        lay = (C.c_int64 * 8)()
+        check(_plan_lib().qnb_plan_blob_info(self.h, self.blob_ids[name], C.byref(ptr), lay))
+        if not ptr.value:
+            return None
+        n, h, w, cp, hh, hw, wx, es = list(lay)
+        raw = np.empty(n * (h + 2 * hh) * (w + 2 * hw + wx) * cp * es, np.uint8)
+        check(L.lib().qnb_memcpy_d2h(raw.ctypes.data_as(C.c_void_p), ptr, raw.nbytes, None))
+        check(L.lib().qnb_stream_sync(None))
+        return raw, (n, h, w, cp, hh, hw, wx, es)
+
+    def __del__(self):
+        try:
+            if self.h:
+                _plan_lib().qnb_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Net:
+    """qnet::Net surface backed by the B200 plan."""
+
+    def __init__(self, graph: dict):
+        self.graph = G.normalized(graph)
+        self.blobs = G.infer_blobs(self.graph)
+        self.aliases = G.range_aliases(self.graph)
+        if any(l["kind"] == "moe" for l in self.graph["layers"]):
+            raise QnbError(10, "MOE graphs run through paper_2209_15427_b200.moe.MoeNet")
+        self.params = {}       # name -> (array, dtype code, qv or None)
+        self.ranges = {}       # range key -> (lo, hi)
+        self.blob_qv = {}
+        self.mode = PASSIVE
+        self._plans = {}
+
+    # ---- parameters / ranges (src/net.cpp:140-209)
+    def set_param(self, name, arr, dtype=0, qv=None):
+        self.params[name] = (np.ascontiguousarray(arr), dtype, qv)
+        self._plans.clear()
+
+    def param(self, name):
+        return self.params.get(name)
+
+    def set_range(self, key, lo, hi):
+        self.ranges[G.range_key(self.aliases, key)] = (float(lo), float(hi))
+        self._plans.clear()
+
+    def range(self, key):
+        return self.ranges.get(G.range_key(self.aliases, key))
+
+    def finalize_quantizers(self):
+        """src/net.cpp:211-248."""
+        for l in self.graph["layers"]:
+            if l["kind"] not in ("conv", "inner_product") or l["compute_data_type"] not in G.QUANT:
+                continue
+            dt = G.DTYPE_CODE[l["compute_data_type"]]
+            wkey = l["name"] + ".weight"
+            if wkey not in self.params or self.params[wkey][1] != 0:
+                continue
+            w = self.params[wkey][0]
+            if wkey in self.ranges:
+                lo, hi = self.ranges[wkey]
+            else:
+                lo, hi = float(w.min()), float(w.max())
+            qv = ops.estimate_from_observation(lo, hi, dt)
+            self.params[wkey] = (ops.quantize(w, qv, dt), dt, qv)
+        for b, info in self.blobs.items():
+            if info["dtype"] not in G.QUANT:
+                continue
+            r = self.ranges.get(G.range_key(self.aliases, b))
+            if r is not None:
+                self.blob_qv[b] = ops.estimate_from_observation(r[0], r[1], G.DTYPE_CODE[info["dtype"]])
+        self._plans.clear()
+
+    def set_quant_mode(self, mode):
+        """src/net.cpp:250-275 (OBSERVE and PSEUDO are host-calibration modes, not the B200 path)."""
+        if mode in (QUANTIZED, PSEUDO):
+            for b, info in self.blobs.items():
+                if info["dtype"] in G.QUANT and b not in self.blob_qv:
+                    raise QnbError(5, "quantizer not finalized: " + G.range_key(self.aliases, b))
+            for l in self.graph["layers"]:
+                if l["kind"] in ("conv", "inner_product") and l["compute_data_type"] in G.QUANT:
+                    p = self.params.get(l["name"] + ".weight")
+                    if p is not None and p[1] != G.DTYPE_CODE[l["compute_data_type"]]:
+                        raise QnbError(5, "quantizer not finalized: " + l["name"] + ".weight")
+        self.mode = mode
+
+    def blob_qvals(self, blob):
+        return self.blob_qv.get(blob)
+
+    # ---- compilation
+    def layer_descs(self):
+        ids = {}
+        for l in self.graph["layers"]:
+            for b in l.get("bottom", []) + l["top"]:
+                ids.setdefault(b, len(ids))
+        descs, keep = [], []
+        for l in self.graph["layers"]:
+            d = LayerDesc()
+            d.kind = G.KIND_CODE[l["kind"]]
+            d.mi_type = G.DTYPE_CODE[l["bottom_data_type"]]
+            d.d_type = G.DTYPE_CODE[l["compute_data_type"]]
+            d.mo_type = G.DTYPE_CODE[l["top_data_type"]]
+            d.bottom = ids[l["bottom"][0]] if l.get("bottom") else -1
+            d.top = ids[l["top"][0]]
+            k = l["kind"]
+            if k == "input":
+                d.input_ndim = len(l["input_shape"])
+                for i, v in enumerate(l["input_shape"]):
+                    d.input_shape[i] = v
+            if k == "conv":
+                c = l["conv"]
+                d.conv = L.ConvParams(c["out_channels"], c.get("kernel_h", 1), c.get("kernel_w", 1),
+                                      c.get("stride_h", 1), c.get("stride_w", 1), c.get("pad_h", 0),
+                                      c.get("pad_w", 0), c.get("groups", 1), 1 if c.get("bias_term", True) else 0)
+                d.bias_term = d.conv.bias_term
+            if k == "pool":
+                d.pool_kernel, d.pool_stride = l["pool"]["kernel"], l["pool"]["stride"]
+            if k == "lrn":
+                p = l.get("lrn", {})
+                d.lrn_local_size = p.get("local_size", 5)
+                d.lrn_alpha, d.lrn_beta, d.lrn_k = p.get("alpha", 1e-4), p.get("beta", 0.75), p.get("k", 1.0)
+            if k == "relu":
+                d.negative_slope = l.get("negative_slope", 0.0)
+            if k == "inner_product":
+                d.num_output = l["num_output"]
+                d.bias_term = 1 if l.get("bias_term", True) else 0
+            if k in ("conv", "inner_product"):
+                w = self.params.get(l["name"] + ".weight")
+                if w is None:
+                    raise QnbError(1, "missing parameter: " + l["name"] + ".weight")
+                arr, dt, qv = w
+                if dt == 0 and l["compute_data_type"] == G.FP16:
+                    pass  # fp32 weights feed the f16 MMA after rounding in the packer
+                keep.append(arr)
+                d.weight = arr.ctypes.data
+                d.weight_dtype = dt
+                if qv is not None:
+                    d.weight_has_qv = 1
+                    d.weight_qv = QVals(*qv.as_tuple()) if hasattr(qv, "as_tuple") else qv
+                if d.bias_term:
+                    b = self.params.get(l["name"] + ".bias")
+                    if b is None:
+                        raise QnbError(1, "missing parameter: " + l["name"] + ".bias")
+                    barr = np.ascontiguousarray(b[0], dtype=np.float32)
+                    keep.append(barr)
+                    d.bias = barr.ctypes.data
+            top = l["top"][0]
+            if l["top_data_type"] in G.QUANT:
+                qv = self.blob_qv.get(top)
+                if qv is None:
+                    raise QnbError(5, "quantizer not finalized: " + G.range_key(self.aliases, top))
+                d.top_has_qv = 1
+                d.top_qv = QVals(*qv.as_tuple())
+            descs.append(d)
+        return descs, len(ids), keep, ids
+
+    def compile(self, max_batch: int, use_cuda_graph: bool = True) -> Plan:
+        descs, n_blobs, keep, ids = self.layer_descs()
+        return Plan(descs, n_blobs, keep, max_batch, use_cuda_graph, ids)
+
+    def plan(self, batch: int) -> Plan:
+        if batch not in self._plans:
+            self._plans[batch] = self.compile(batch)
+        return self._plans[batch]
+
+    def forward(self, inputs: dict) -> dict:
+        """src/net.cpp:305-330: returns {sink: tensor} in the reference layout."""
+        if self.mode == QUANTIZED or all(
+                self.blobs[b]["dtype"] in G.FLOAT for b in self.blobs):
+            pass
+        name = G.input_name(self.graph)
+        if name not in inputs:
+            raise QnbError(1, "missing input: " + name)
+        x = np.ascontiguousarray(inputs[name])
+        want = next(l for l in self.graph["layers"] if l["kind"] == "input")["input_shape"]
+        if x.ndim != len(want) or list(x.shape[1:]) != list(want[1:]):
+            raise QnbError(2, "shape mismatch")
+        out = self.plan(x.shape[0]).forward_host(x)
+        return {G.sinks(self.graph)[-1]: out}

@@ -1,0 +1,110 @@
+"""Whole-network parity on the B200: the compiled AlexNet INT8 plan against the
+UNMODIFIED reference Net (oracle/_ref) on identical seeded weights, calibration and
+images.  Integer blobs must be bit-identical at every checkpoint; the FP32 softmax
+output may differ by 1 ulp (double exp in libm vs CUDA)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ffi
+from paper_2209_15427_b200 import graph as G
+from paper_2209_15427_b200 import graphs
+from paper_2209_15427_b200.net import QUANTIZED, Net
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+DT = {"fp32": 0, "fp16": 1, "int8": 2, "int16": 3}
+
+
+def load_calib(model, precision):
+    with open(os.path.join(HERE, "golden", f"{model}_{precision}_calib.json")) as f:
+        return json.load(f)["ranges"]
+
+
+def nhwc_interior_to_nchw(raw, lay, np_dtype):
+    n, h, w, cp, hh, hw, wx, es = lay
+    a = raw.view(np_dtype).reshape(n, h + 2 * hh, w + 2 * hw + wx, cp)
+    return a[:, hh:hh + h, hw:hw + w, :]
+
+
+def ref_net(ref, g, precision, params, ranges):
+    net = ref.net(json.dumps(g), DT[precision])
+    for k, v in params.items():
+        net.set_param(k, v)
+    for k, (lo, hi) in ranges.items():
+        net.set_range(k, lo, hi)
+    net.finalize()
+    net.set_mode(3)
+    return net
+
+
+@pytest.fixture(scope="module")
+def setup():
+    if not ffi.have_reference():
+        pytest.skip("needs oracle/_ref")
+    ref = ffi.Reference()
+    g = graphs.alexnet(1)
+    shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
+    params = graphs.synth_params(g, shapes)
+    ranges = load_calib("alexnet", "int8")
+    ours = Net(G.override_precision(g, "int8"))
+    for k, v in params.items():
+        ours.set_param(k, v)
+    for k, (lo, hi) in ranges.items():
+        ours.set_range(k, lo, hi)
+    ours.finalize_quantizers()
+    ours.set_quant_mode(QUANTIZED)
+    return ref, g, params, ranges, ours
+
+
+def test_finalize_matches_reference(setup):
+    ref, g, params, ranges, ours = setup
+    rn = ref_net(ref, g, "int8", params, ranges)
+    for l in ours.graph["layers"]:
+        if l["kind"] in ("conv", "inner_product"):
+            w_ref, qv_ref = rn.param(l["name"] + ".weight")
+            w_ours, dt, qv = ours.param(l["name"] + ".weight")
+            assert qv.as_tuple() == qv_ref.as_tuple()
+            assert np.array_equal(w_ours, w_ref), l["name"]
+    for b in ours.blobs:
+        q = ours.blob_qvals(b)
+        if q is not None:
+            assert q.as_tuple() == rn.blob_qvals(b).as_tuple(), b
+
+
+def test_alexnet_int8_bit_exact(setup):
+    ref, g, params, ranges, ours = setup
+    batch = 2
+    x = graphs.synth_images(batch, (3, 227, 227), offset=0)
+    out = ours.forward({"data": x})["prob"]
+    plan = ours.plan(batch)
+    st = plan.stats()
+    assert st["kernels_per_forward"] <= 16
+    # checkpoints: reference prefix nets give the reference's blob at that point
+    names = [l["name"] for l in g["layers"]]
+    for ck in ("relu1", "norm1", "relu2", "relu5", "pool5", "relu7", "fc8"):
+        prefix = {"name": "alexnet_prefix", "layers": g["layers"][: names.index(ck) + 1]}
+        pr = {k: v for k, v in params.items() if k.split(".")[0] in names[: names.index(ck) + 1]}
+        rn = ref_net(ref, prefix, "int8", pr, ranges)
+        res = rn.forward("data", x)
+        (arr, dt, qv), = [v for k, v in res.items()]
+        blob = ck if ck != "norm1" else "norm1__int8"
+        got = plan.blob(blob)
+        assert got is not None, blob
+        raw, lay = got
+        mine = nhwc_interior_to_nchw(raw, lay, np.uint8)
+        theirs = arr.reshape(batch, lay[3] if arr.ndim == 2 else arr.shape[1], *(arr.shape[2:] or (1, 1)))
+        if arr.ndim == 4:
+            theirs = np.transpose(arr, (0, 2, 3, 1))
+        else:
+            theirs = arr.reshape(batch, 1, 1, -1)
+        mine = mine[..., : theirs.shape[-1]]
+        mism = int((mine != theirs).sum())
+        assert mism == 0, f"{ck}: {mism} of {theirs.size} differ"
+    rn = ref_net(ref, g, "int8", params, ranges)
+    res = rn.forward("data", x)
+    prob_ref = res["prob"][0]
+    d = np.abs(out.view(np.int32).astype(np.int64) - prob_ref.view(np.int32).astype(np.int64))
+    assert d.max() <= 1, d.max()
