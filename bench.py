@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""AlexNet INT8 batch-256 inference on B200 through the compiled qnb plan
+(BASELINE.json metric: AlexNet INT8/FP16 images/sec at 1/2/4/8 B200; conv TOPS vs
+int8 tensor peak).
+
+    python bench.py [--gpus N --steps K --warmup W]            # this framework
+    python bench.py --impl reference [--steps K --warmup W]     # the reference's CPU path
+    torchrun --nproc-per-node N bench.py --gpus N ...          # weak scaling, 256 img/GPU
+
+A step is one forward of one batch of synthetic 227x227 images (seeded U(0,255)),
+seeded random-init weights, calibration fixture tests/golden/alexnet_int8_calib.json.
+The input batch (158 MB FP32) is larger than the 126 MB L2, so no explicit flush is
+needed between steps.  One JSON line is printed by rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "AlexNet INT8 images/sec (batch 256 per GPU, 227x227)"
+DT = {"fp32": 0, "fp16": 1, "int8": 2, "int16": 3}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="qnb", choices=["qnb", "reference"])
+    ap.add_argument("--model", default="alexnet")
+    ap.add_argument("--precision", default="int8")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--cpu-threads", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-reps", type=int, default=3)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(use_cuda: bool):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if use_cuda else "gloo")
+    return ws, rank, local
+
+
+def barrier(ws, device=None):
+    if ws > 1:
+        import torch.distributed as dist
+        if device is not None:
+            dist.barrier(device_ids=[device])
+        else:
+            dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clocks and throttle reasons."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop_flag = [], set(), False
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop_flag:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_flag = True
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ model setup
+def model_setup(model: str, precision: str):
+    from paper_2209_15427_b200 import graph as G
+    from paper_2209_15427_b200 import graphs
+    g = graphs.MODELS[model](1)
+    shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
+    params = graphs.synth_params(g, shapes)
+    with open(os.path.join(ROOT, "tests", "golden", f"{model}_{precision}_calib.json")) as f:
+        ranges = json.load(f)["ranges"]
+    return g, shapes, params, ranges
+
+
+def reference_nets(g, precision, params, ranges, n):
+    """n independent reference Nets (one per host thread), built in parallel."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import ffi
+    ref = ffi.Reference()
+
+    def one(_):
+        net = ref.net(json.dumps(g), DT[precision])
+        for k, v in params.items():
+            net.set_param(k, v)
+        for k, (lo, hi) in ranges.items():
+            net.set_range(k, lo, hi)
+        net.finalize()
+        net.set_mode(3 if precision in ("int8", "int16") else 0)
+        return net
+
+    with ThreadPoolExecutor(max_workers=min(n, 16)) as ex:
+        return list(ex.map(one, range(n)))
+
+
+def cpu_forward_rate(nets, x, out_bytes):
+    from oracle import ffi
+    t0 = time.perf_counter()
+    ffi.forward_mt(nets, "data", x, "prob", out_bytes)
+    return x.shape[0] / (time.perf_counter() - t0)
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(a):
+    ws, rank, local = dist_setup(use_cuda=False)
+    if rank != 0:
+        return
+    from oracle import ffi
+    if not ffi.have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    g, shapes, params, ranges = model_setup(a.model, a.precision)
+    T = os.cpu_count() or 1
+    T = min(T, 64)
+    nets = reference_nets(g, a.precision, params, ranges, T)
+    from paper_2209_15427_b200 import graphs
+    x = graphs.synth_images(T, shapes["data"][1:], offset=0)
+    for _ in range(a.warmup):
+        cpu_forward_rate(nets, x, 4000)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        cpu_forward_rate(nets, x, 4000)
+    dt = time.perf_counter() - t0
+    v = T * a.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic U(0,255) images, seeded random-init weights",
+            "config": {"workload": f"{a.model} {a.precision} forward, 227x227, bounded sample of {T} images "
+                                   f"per step (reference Net::forward, QUANTIZED mode)", "global_batch": T,
+                       "parallelism": f"{T} host threads, one Net each"},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": T, "kind": "reference",
+                             "sample": f"{T} images per step x {a.steps} steps"},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_qnb(a):
+    import torch
+    ws, rank, local = dist_setup(use_cuda=True)
+    torch.cuda.set_device(local)
+    from paper_2209_15427_b200 import graph as G
+    from paper_2209_15427_b200 import graphs
+    from paper_2209_15427_b200._lib import check, lib
+    from paper_2209_15427_b200.net import QUANTIZED, Net
+
+    check(lib().qnb_device_check(local))
+    g, shapes, params, ranges = model_setup(a.model, a.precision)
+    net = Net(G.override_precision(g, a.precision) if a.precision != "fp32" else g)
+    for k, v in params.items():
+        net.set_param(k, v)
+    for k, (lo, hi) in ranges.items():
+        net.set_range(k, lo, hi)
+    net.finalize_quantizers()
+    net.set_quant_mode(QUANTIZED)
+    B = a.batch
+    plan = net.compile(B)
+    kernels = plan.stats()["kernels_per_forward"]
+    x_host = graphs.synth_images(B, shapes["data"][1:], offset=rank * B)
+    x_dev = torch.from_numpy(x_host).cuda()
+    out_dev = torch.empty((B, 1000), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step():
+        plan.forward_device(x_dev.data_ptr(), out_dev.data_ptr(), B, sp)
+
+    for _ in range(max(a.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launches0 = lib().qnb_kernel_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(ws, local)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws, local)
+    launches = lib().qnb_kernel_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms, ws, local)
+    value = ws * B * a.steps / (ms_max / 1e3)
+
+    # end to end through the C-ABI with pinned host buffers (H2D input + D2H result per step)
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    o_pin = torch.empty((B, 1000), dtype=torch.float32).pin_memory()
+
+    def step_e2e():
+        plan.forward_device(x_pin.data_ptr(), o_pin.data_ptr(), B, sp, in_host=True, out_host=True)
+
+    for _ in range(2):
+        step_e2e()
+    torch.cuda.synchronize()
+    barrier(ws, local)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step_e2e()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws, local)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws, local)
+    e2e_value = ws * B * a.steps / (e2e_ms / 1e3)
+
+    # per-step profile (events between steps, eager) -> roofline of the dominant kernel
+    ms_steps = plan.profile(x_dev.data_ptr(), out_dev.data_ptr(), B, a.profile_reps, sp)
+    steps_info = plan.steps()
+    names = [l["name"] for l in net.graph["layers"]]
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+        peak_src = "measured"
+    except Exception:
+        peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+        peak_src = "fallback"
+    int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 = 2x dense bf16 on B200
+    hbm_peak = peaks["hbm_gbs"]
+    per_layer = []
+    conv_ops = conv_ms = 0.0
+    for (li, kind, ops_, by), t in zip(steps_info, ms_steps):
+        per_layer.append({"layer": names[li] if 0 <= li < len(names) else str(li), "kernel": kind,
+                          "ms": round(t, 4),
+                          "tops": round(ops_ / (t * 1e-3) / 1e12, 1) if ops_ else None,
+                          "gbs": round(by / (t * 1e-3) / 1e9, 1)})
+        if kind == "igemm" and names[li].startswith("conv"):
+            conv_ops += ops_
+            conv_ms += t
+    dom = int(np.argmax(ms_steps))
+    li, kind, ops_, by = steps_info[dom]
+    t = ms_steps[dom]
+    if kind == "igemm":
+        roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",
+                "kernel": f"igemm {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
+    else:
+        roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "kernel": f"{kind} {names[li]}", "algorithmic_bytes": by, "launch_ms": t}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["peak_source"] = (f"{peak_src}: 2 x bf16_tflops {peaks['bf16_tflops']} (dense int8 = 2x bf16)"
+                           if kind == "igemm" else f"{peak_src}: hbm_gbs")
+    conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+        try:
+            from oracle import ffi
+            if ffi.have_reference():
+                T = min(a.cpu_threads, os.cpu_count() or 1)
+                nets = reference_nets(g, a.precision, params, ranges, T)
+                xs = x_host[:T]
+                v = cpu_forward_rate(nets, xs, 4000)
+                cpu = {"value": v, "unit": "images/s", "cores": T, "kind": "reference",
+                       "sample": f"{T} images of the same batch, one reference Net::forward thread each"}
+                del nets
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u8 (s32 accumulate)",
+                "data": "synthetic U(0,255) images, seeded random-init weights",
+                "config": {"workload": f"{a.model} {a.precision} forward, batch {B} per GPU, 227x227 (BASELINE "
+                                       f"configs[1])", "model": a.model, "global_batch": B * ws,
+                           "parallelism": f"dp{ws} (independent replicas, no collective)",
+                           "l2": "input batch 158 MB > 126 MB L2 (no flush needed)"},
+                "e2e": {"value": e2e_value, "unit": "images/s",
+                        "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(B * 1000 * 4)},
+                "gpu_launches": int(launches), "kernels_per_forward": kernels,
+                "roofline": roof, "conv_tops": conv_tops, "conv_frac_of_int8_peak":
+                    (conv_tops / int8_peak if conv_tops else None),
+                "cpu_baseline": cpu, "clocks": clk.summary(), "per_layer": per_layer}
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_qnb(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -95,6 +95,10 @@ _PLAN_SIGS = {
     "qnb_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                  C.POINTER(C.c_int64)]),
     "qnb_plan_destroy": (C.c_int, [C.c_void_p]),
+    "qnb_plan_step_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "qnb_plan_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,
+                                   C.POINTER(C.c_float)]),
 }
 
 

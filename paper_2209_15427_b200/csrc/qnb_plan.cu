@@ -75,6 +75,8 @@ enum Sym { SYM_NONE = 0, SYM_INPUT = 1, SYM_OUTPUT = 2 };
 struct Step {
   OpKind kind;
   int src_sym = SYM_NONE, dst_sym = SYM_NONE;
+  int layer = -1;            // main reference layer of this step
+  double ops = 0, bytes = 0;  // algorithmic work at max_batch (2 per MAC; bytes in + out)
   // one of:
   IgemmArgs ig;
   int mma_kind = 0;
@@ -588,7 +590,24 @@ qnb_status emit(qnb_plan& P) {
     if (op.kind == OP_ALIAS) continue;
     Step st;
     st.kind = op.kind;
+    st.layer = op.layer;
     const bool to_sink = root_of(P, op.out) == P.sink_blob;
+    {
+      const Blob& bi = P.blobs[op.in];
+      const Blob& bo = P.blobs[op.out];
+      const double in_b = (double)P.max_batch * bi.c * bi.h * bi.w * dtype_size(bi.dtype);
+      const double out_b = (double)P.max_batch * bo.c * bo.h * bo.w * dtype_size(bo.dtype);
+      st.bytes = in_b + out_b;
+      if (op.kind == OP_IGEMM) {
+        const qnb_layer_desc& l = P.layers[op.layer];
+        const double K = l.kind == QNB_LAYER_CONV
+                             ? (double)(bi.c / l.conv.groups) * l.conv.kernel_h * l.conv.kernel_w
+                             : (double)bi.c * bi.h * bi.w;
+        const double M = (double)P.max_batch * bo.h * bo.w;
+        st.ops = 2.0 * M * bo.c * K;
+        st.bytes += (double)bo.c * K * dtype_size(l.d_type);
+      }
+    }
     switch (op.kind) {
       case OP_PACK: {
         const Blob& src = P.blobs[op.in];
@@ -702,6 +721,9 @@ qnb_status emit(qnb_plan& P) {
       up.up_src = blob_ptr(P, op.out);
       up.up_S = dev_layout(blob_layout(P, op.out));
       up.dst_sym = SYM_OUTPUT;
+      up.layer = op.layer;
+      up.bytes = 2.0 * (double)P.max_batch * P.blobs[op.out].c * P.blobs[op.out].h * P.blobs[op.out].w *
+                 dtype_size(P.blobs[op.out].dtype);
       P.steps.push_back(up);
     }
   }
@@ -726,8 +748,8 @@ Step with_batch(const Step& s0, int64_t b, const void* in, void* out) {
   return s;
 }
 
-qnb_status launch_steps(qnb_plan& P, int64_t b, const void* in, void* out, cudaStream_t s) {
-  for (const Step& s0 : P.steps) {
+qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cudaStream_t s) {
+  {
     const Step st = with_batch(s0, b, in, out);
     if (st.unpack) {
       launch_unpack(st.up_src, st.up_S, st.up_dst, s);
@@ -759,6 +781,24 @@ qnb_status launch_steps(qnb_plan& P, int64_t b, const void* in, void* out, cudaS
     QNB_CUDA(cudaGetLastError());
   }
   return QNB_OK;
+}
+
+qnb_status launch_steps(qnb_plan& P, int64_t b, const void* in, void* out, cudaStream_t s) {
+  for (const Step& st : P.steps) QNB_TRY(launch_one(st, b, in, out, s));
+  return QNB_OK;
+}
+
+int step_kind_code(const Step& st) {
+  if (st.unpack) return 6;
+  switch (st.kind) {
+    case OP_PACK: return 0;
+    case OP_IGEMM: return 1;
+    case OP_POOL: return 2;
+    case OP_POOL_LRN: return 3;
+    case OP_CONVERT: return 4;
+    case OP_SOFTMAX: return 5;
+    default: return 7;
+  }
 }
 
 }  // namespace
@@ -886,6 +926,45 @@ qnb_status qnb_plan_stats(const qnb_plan* P, int64_t* kernels, int64_t* arena, i
   if (kernels) *kernels = (int64_t)P->steps.size();
   if (arena) *arena = (int64_t)P->arena_bytes;
   if (weights) *weights = (int64_t)P->weight_bytes;
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_step_info(const qnb_plan* P, int32_t step, int32_t* layer, int32_t* kind, double* ops,
+                              double* bytes) {
+  if (!P || step < 0 || step >= (int)P->steps.size()) return fail(QNB_E_ARG, "step out of range");
+  const Step& st = P->steps[(size_t)step];
+  if (layer) *layer = st.layer;
+  if (kind) *kind = step_kind_code(st);
+  if (ops) *ops = st.ops;
+  if (bytes) *bytes = st.bytes;
+  return QNB_OK;
+}
+
+qnb_status qnb_plan_profile(qnb_plan* P, const void* input, int64_t batch, void* output, int32_t reps,
+                            qnb_stream s_, float* ms_per_step) {
+  if (!P) return fail(QNB_E_ARG, "null plan");
+  if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
+  cudaStream_t s = as_stream(s_);
+  const size_t n = P->steps.size();
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) QNB_CUDA(cudaEventCreate(&e));
+  std::vector<double> acc(n, 0.0);
+  for (int r = 0; r < reps; ++r) {
+    QNB_CUDA(cudaEventRecord(ev[0], s));
+    for (size_t i = 0; i < n; ++i) {
+      QNB_TRY(launch_one(P->steps[i], batch, input, output, s));
+      QNB_CUDA(cudaEventRecord(ev[i + 1], s));
+    }
+    count_launch(n);
+    QNB_CUDA(cudaEventSynchronize(ev[n]));
+    for (size_t i = 0; i < n; ++i) {
+      float ms = 0;
+      QNB_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      acc[i] += ms;
+    }
+  }
+  for (size_t i = 0; i < n; ++i) ms_per_step[i] = (float)(acc[i] / (reps > 0 ? reps : 1));
+  for (auto& e : ev) cudaEventDestroy(e);
   return QNB_OK;
 }
 

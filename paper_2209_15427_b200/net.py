@@ -59,6 +59,28 @@ class Plan:
         check(_plan_lib().qnb_plan_stats(self.h, C.byref(k), C.byref(a), C.byref(w)))
         return {"kernels_per_forward": k.value, "arena_bytes": a.value, "weight_bytes": w.value}
 
+    STEP_KINDS = {0: "pack_input", 1: "igemm", 2: "pool", 3: "pool_lrn", 4: "convert", 5: "softmax",
+                  6: "unpack"}
+
+    def steps(self):
+        """[(layer index, kind name, ops, bytes)] per step at max_batch."""
+        n = self.stats()["kernels_per_forward"]
+        out = []
+        for i in range(n):
+            lay, kind, ops_, by = C.c_int32(), C.c_int32(), C.c_double(), C.c_double()
+            check(_plan_lib().qnb_plan_step_info(self.h, i, C.byref(lay), C.byref(kind), C.byref(ops_),
+                                                 C.byref(by)))
+            out.append((lay.value, self.STEP_KINDS.get(kind.value, "?"), ops_.value, by.value))
+        return out
+
+    def profile(self, in_ptr: int, out_ptr: int, batch: int, reps: int = 3, stream: int = 0):
+        """Mean ms per step (eager launches, CUDA events between steps)."""
+        n = self.stats()["kernels_per_forward"]
+        ms = (C.c_float * n)()
+        check(_plan_lib().qnb_plan_profile(self.h, C.c_void_p(in_ptr), batch, C.c_void_p(out_ptr), reps,
+                                           C.c_void_p(stream), ms))
+        return list(ms)
+
     def forward_host(self, x: np.ndarray) -> np.ndarray:
         """Host buffers in and out (copies inside the call)."""
         x = np.ascontiguousarray(x)
