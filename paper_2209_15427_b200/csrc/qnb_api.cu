@@ -233,6 +233,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     QNB_TRY(tmp.alloc((void**)&d_cc, cc.size() * 8));
     QNB_CUDA(cudaMemcpyAsync(d_cc, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice, s));
     a.chan_const = d_cc;
+    a.fast_rq = igemm_fast_requant_ok(cc, K, zw, a.rq) ? 1 : 0;
     a.epi = EPI_Q8;
   } else {
     a.bias = bias_dev;

@@ -30,40 +30,88 @@
 
 namespace qnb {
 
-constexpr int kStages = 4;
 constexpr int kBM = 128;
 constexpr int kStageA = kBM * 128;
-constexpr int kThreads = 160;  // warps 0-3: A producers + epilogue; warp 4: MMA
+constexpr int kMaxStages = 8;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (5 + kEpiWarps) * 32;  // 4 producer warps, 1 MMA warp, 8 epilogue warps
 
+__host__ __device__ inline int igemm_stages(int n_rows) {
+  const int per = kStageA + n_rows * 128;
+  const int s = (200 * 1024) / per;
+  return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
+}
 __host__ __device__ inline size_t igemm_smem_bytes(int n_rows) {
-  return 1024 + (size_t)kStages * (kStageA + (size_t)n_rows * 128) + (2 * kStages + 2) * 8;
+  return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16;
 }
 
+struct TileCoord {
+  int64_t mt;
+  int nt, g;
+};
+// Tile order: m fastest, so the CTAs resident at any moment share one B tile in L2.
+__device__ __forceinline__ TileCoord tile_of(int64_t t, int64_t m_tiles, int n_tiles) {
+  TileCoord c;
+  c.mt = t % m_tiles;
+  const int64_t r = t / m_tiles;
+  c.nt = (int)(r % n_tiles);
+  c.g = (int)(r / n_tiles);
+  return c;
+}
+
+// requant_clamp when the host proved |acc| < 2^31 and 1 <= s <= 62: the 128-bit
+// product of the reference collapses to one 32x32->64 multiply; round half to even
+// at bit s exactly as src/quantizer.cpp:205-211.
+__device__ __forceinline__ int64_t requant_fast(int32_t acc, const Requant& rq) {
+  const int64_t pr = (int64_t)acc * rq.mult;
+  const int64_t half = 1LL << (rq.s - 1);
+  int64_t q = (pr + half) >> rq.s;
+  if ((pr & ((half << 1) - 1)) == half) q &= ~1LL;
+  const int64_t v = q + rq.out_zero;
+  return v < rq.out_min ? rq.out_min : (v > rq.out_max ? rq.out_max : v);
+}
+
+// Persistent, warp-specialised implicit GEMM.  One CTA per SM loops over output
+// tiles (128 pixels x n_rows channels of one group):
+//   warps 0-3  A producers: thread t gathers row t of the tile with cp.async (16 B
+//              chunks from the chunk table) into a S-stage 128B-swizzled ring; thread 0
+//              also streams the pre-swizzled B stage with one bulk copy.
+//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer; two TMEM
+//              accumulators so tile i+1's MMAs overlap tile i's epilogue.
+//   warps 5-12 epilogue: tcgen05.ld -> exact requant (+ReLU) -> NHWC stores.  Two
+//              warps per TMEM lane quarter split the 16-column blocks.
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constant__ IgemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int S = igemm_stages(p.n_rows);
   const int b_stage = p.n_rows * 128;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kStageA;
-  uint64_t* full = (uint64_t*)(sB + (size_t)kStages * b_stage);
-  uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;
-  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  uint8_t* sB = smem + (size_t)S * kStageA;
+  uint64_t* full = (uint64_t*)(sB + (size_t)S * b_stage);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* acc_full = empty + kMaxStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x, nt = blockIdx.y, g = blockIdx.z;
+  const int64_t m_tiles = (p.m_total + kBM - 1) / kBM;
+  const int64_t total = m_tiles * p.n_tiles * p.groups;
+  const int64_t pix_per_img = (int64_t)p.oh * p.ow;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 129);  // 128 cp.async arrivals + 1 expect_tx arrival
       mbar_init(&empty[i], 1);
     }
-    mbar_init(done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kEpiWarps);
+    }
     fence_barrier_init();
   }
   if (warp == 4) {
-    tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
+    tmem_alloc(tmem_slot, (uint32_t)(2 * p.tmem_cols));
     tmem_relinquish();
   }
   tc_fence_before();
@@ -72,151 +120,187 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    // ------------------------------------------------------------ producer
+    // ---------------------------------------------------------------- producers
     const int t = threadIdx.x;
-    const int64_t pix_per_img = (int64_t)p.oh * p.ow;
-    int64_t row = (int64_t)mt * kBM + t;
-    const bool valid = row < p.m_total;
-    const uint8_t* base = p.a;
-    if (valid) {
-      const int64_t img = row / pix_per_img;
-      const int64_t rem = row - img * pix_per_img;
-      const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-      base = p.a + img * p.a_img + oy * p.stride_h * p.a_row + ox * p.stride_w * p.a_pix +
-             (int64_t)g * p.a_group + p.a_origin;
-    }
-    const uint8_t* btile = p.b + (int64_t)(g * p.n_tiles + nt) * p.num_kb * b_stage;
-    uint8_t* arow = sA + t * 128;
     const int sw = t & 7;
-    for (int kb = 0; kb < p.num_kb; ++kb) {
-      const int s = kb % kStages;
-      if (kb >= kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-      if (t == 0) {
-        mbar_arrive_expect_tx(&full[s], (uint32_t)b_stage);
-        bulk_g2s(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage,
-                 &full[s]);
-      }
+    uint32_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const TileCoord c = tile_of(tile, m_tiles, p.n_tiles);
+      const int64_t row = c.mt * kBM + t;
+      const bool valid = row < p.m_total;
+      const uint8_t* base = p.a;
       if (valid) {
-        const int32_t* co = p.chunk_off + kb * 8;
-        uint8_t* dst = arow + s * kStageA;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) cp_async_16(dst + ((j ^ sw) << 4), base + __ldg(co + j));
+        const int64_t img = row / pix_per_img;
+        const int64_t rem = row - img * pix_per_img;
+        const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
+        base = p.a + img * p.a_img + oy * p.stride_h * p.a_row + ox * p.stride_w * p.a_pix +
+               (int64_t)c.g * p.a_group + p.a_origin;
       }
-      cp_async_arrive_noinc(&full[s]);
-    }
-
-    // ------------------------------------------------------------ epilogue
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16);
-    row = (int64_t)mt * kBM + 32 * warp + lane;
-    const bool ok = row < p.m_total;
-    uint8_t* obase = p.out;
-    if (ok) {
-      const int64_t img = row / pix_per_img;
-      const int64_t rem = row - img * pix_per_img;
-      const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-      obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
-    }
-    int64_t rowsum = 0;
-    if (p.ones_col >= 0) {
-      uint32_t v;
-      tmem_ld1(trow + (uint32_t)p.ones_col, v);
-      tmem_ld_wait();
-      rowsum = (int64_t)(int32_t)v;
-    }
-    const int n0 = nt * p.n_per_tile;
-    const int n_here = min(p.n_per_tile, p.n_real - n0);
-    const int ch0 = g * p.n_real + n0;  // global output channel of column 0
-    for (int cb = 0; cb < n_here; cb += 16) {
-      uint32_t r[16];
-      tmem_ld16(trow + (uint32_t)cb, r);
-      tmem_ld_wait();
-      if (!ok) continue;
-      const int cnt = min(16, n_here - cb);
-      uint8_t* dst = obase + (int64_t)(ch0 + cb) * p.o_es;
-      if (p.epi == EPI_Q8) {
-        uint32_t packed[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i < cnt) {
-            int64_t acc = (int64_t)(int32_t)r[i] + __ldg(p.chan_const + ch0 + cb + i) - p.zw * rowsum;
-            int64_t q = requant_clamp(acc, p.rq);
-            if (p.has_relu) q = relu_requant(q, p.relu);
-            packed[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
-          }
+      const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
+      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const int s = (int)(it % S);
+        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        if (t == 0) {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)b_stage);
+          bulk_g2s(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s]);
         }
-        if (cnt == 16 && p.o_vec) {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        } else {
-          for (int i = 0; i < cnt; ++i) dst[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
+        if (valid) {
+          const int32_t* co = p.chunk_off + kb * 8;
+          uint8_t* dst = sA + (size_t)s * kStageA + t * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) cp_async_16(dst + ((j ^ sw) << 4), base + __ldg(co + j));
         }
-      } else {
-        float y[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float v = __uint_as_float(r[i]);
-          if (p.bias != nullptr && i < cnt) v = __fadd_rn(v, __ldg(p.bias + ch0 + cb + i));
-          y[i] = v;
-        }
-        if (p.epi == EPI_F16) {
-          __half h[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            __half hv = __float2half_rn(y[i]);
-            if (p.has_relu) {
-              const float x = __half2float(hv);
-              hv = __float2half_rn(x > 0.0f ? x : __fmul_rn(x, p.slope));
-            }
-            h[i] = hv;
-          }
-          if (cnt == 16 && p.o_vec) {
-            const uint4* src = reinterpret_cast<const uint4*>(h);
-            reinterpret_cast<uint4*>(dst)[0] = src[0];
-            reinterpret_cast<uint4*>(dst)[1] = src[1];
-          } else {
-            for (int i = 0; i < cnt; ++i) reinterpret_cast<__half*>(dst)[i] = h[i];
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (p.has_relu) y[i] = y[i] > 0.0f ? y[i] : __fmul_rn(y[i], p.slope);
-          }
-          if (cnt == 16 && p.o_vec) {
-            const uint4* src = reinterpret_cast<const uint4*>(y);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(dst)[q] = src[q];
-          } else {
-            for (int i = 0; i < cnt; ++i) reinterpret_cast<float*>(dst)[i] = y[i];
-          }
-        }
+        cp_async_arrive_noinc(&full[s]);
       }
     }
-  } else {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = make_idesc<KIND>(p.n_rows);
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+      uint32_t it = 0, j = 0;
+      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++j) {
+        const uint32_t buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint64_t ad = smem_desc_sw128(sA + (size_t)s * kStageA);
-        const uint64_t bd = smem_desc_sw128(sB + (size_t)s * b_stage);
+        const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = (int)(it % S);
+          mbar_wait(&full[s], (it / S) & 1);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_sw128(sA + (size_t)s * kStageA);
+          const uint64_t bd = smem_desc_sw128(sB + (size_t)s * b_stage);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) umma<KIND>(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-        tc_commit(&empty[s]);
+          for (int k = 0; k < 4; ++k) umma<KIND>(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&acc_full[buf]);
       }
-      tc_commit(done);
     }
     __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int quarter = warp & 3;           // TMEM lanes 32*quarter .. +31
+    const int half = (warp - 5) >> 2;       // which 16-column blocks of the tile
+    uint32_t j = 0;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++j) {
+      const TileCoord c = tile_of(tile, m_tiles, p.n_tiles);
+      const uint32_t buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t trow = tmem + buf * (uint32_t)p.tmem_cols + ((uint32_t)(32 * quarter) << 16);
+      const int64_t row = c.mt * kBM + 32 * quarter + lane;
+      const bool ok = row < p.m_total;
+      uint8_t* obase = p.out;
+      if (ok) {
+        const int64_t img = row / pix_per_img;
+        const int64_t rem = row - img * pix_per_img;
+        const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
+        obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+      }
+      int64_t rowsum = 0;
+      if (p.ones_col >= 0) {
+        uint32_t v;
+        tmem_ld1(trow + (uint32_t)p.ones_col, v);
+        tmem_ld_wait();
+        rowsum = (int64_t)(int32_t)v;
+      }
+      const int32_t rowterm32 = (int32_t)(-p.zw * rowsum);
+      const int n0 = c.nt * p.n_per_tile;
+      const int n_here = min(p.n_per_tile, p.n_real - n0);
+      const int ch0 = c.g * p.n_real + n0;
+      for (int cb = half * 16; cb < n_here; cb += 32) {
+        uint32_t r[16];
+        tmem_ld16(trow + (uint32_t)cb, r);
+        tmem_ld_wait();
+        if (!ok) continue;
+        const int cnt = min(16, n_here - cb);
+        uint8_t* dst = obase + (int64_t)(ch0 + cb) * p.o_es;
+        if (p.epi == EPI_Q8) {
+          uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i < cnt) {
+              const int64_t cc = __ldg(p.chan_const + ch0 + cb + i);
+              int64_t q;
+              if (p.fast_rq)
+                q = requant_fast((int32_t)r[i] + (int32_t)cc + rowterm32, p.rq);
+              else
+                q = requant_clamp((int64_t)(int32_t)r[i] + cc - p.zw * rowsum, p.rq);
+              if (p.has_relu) q = relu_requant(q, p.relu);
+              packed[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
+            }
+          }
+          if (cnt == 16 && p.o_vec) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          } else {
+            for (int i = 0; i < cnt; ++i) dst[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
+          }
+        } else {
+          float y[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float v = __uint_as_float(r[i]);
+            if (p.bias != nullptr && i < cnt) v = __fadd_rn(v, __ldg(p.bias + ch0 + cb + i));
+            y[i] = v;
+          }
+          if (p.epi == EPI_F16) {
+            __align__(16) __half h[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __half hv = __float2half_rn(y[i]);
+              if (p.has_relu) {
+                const float x = __half2float(hv);
+                hv = __float2half_rn(x > 0.0f ? x : __fmul_rn(x, p.slope));
+              }
+              h[i] = hv;
+            }
+            if (cnt == 16 && p.o_vec) {
+              const uint4* src = reinterpret_cast<const uint4*>(h);
+              reinterpret_cast<uint4*>(dst)[0] = src[0];
+              reinterpret_cast<uint4*>(dst)[1] = src[1];
+            } else {
+              for (int i = 0; i < cnt; ++i) reinterpret_cast<__half*>(dst)[i] = h[i];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (p.has_relu) y[i] = y[i] > 0.0f ? y[i] : __fmul_rn(y[i], p.slope);
+            if (cnt == 16 && p.o_vec) {
+              const uint4* src = reinterpret_cast<const uint4*>(y);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(dst)[q] = src[q];
+            } else {
+              for (int i = 0; i < cnt; ++i) reinterpret_cast<float*>(dst)[i] = y[i];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    tmem_dealloc(tmem, (uint32_t)p.tmem_cols);
+    tmem_dealloc(tmem, (uint32_t)(2 * p.tmem_cols));
   }
+}
+
+bool igemm_fast_requant_ok(const std::vector<int64_t>& chan_const, int64_t K, int64_t zw, const Requant& rq) {
+  if (rq.s < 1 || rq.s > 62) return false;
+  const int64_t lim = (int64_t(1) << 31) - 1;
+  if (K < 0 || K > 33025) return false;
+  const int64_t dot_max = K * 255 * 255, row_max = K * 255;
+  for (int64_t c : chan_const) {
+    const int64_t lo = c - zw * row_max;  // dot >= 0, rowsum <= 255*K
+    const int64_t hi = c + dot_max;       // rowsum >= 0
+    if (lo < -lim || hi > lim || c < -lim || c > lim) return false;
+  }
+  if (zw * row_max > lim) return false;
+  return rq.mult < (int64_t(1) << 31);
 }
 
 // ---------------------------------------------------------------- host side
@@ -354,16 +438,30 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
   return QNB_OK;
 }
 
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int KIND>
-static qnb_status launch_kind(const IgemmArgs& a, int64_t groups, cudaStream_t s) {
+static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t s) {
   static bool attr_set = false;
-  const size_t smem = igemm_smem_bytes(256);
   if (!attr_set) {
-    QNB_CUDA(cudaFuncSetAttribute(igemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    size_t mx = 0;
+    for (int r = 16; r <= 256; r += 16) mx = std::max(mx, igemm_smem_bytes(r));
+    QNB_CUDA(cudaFuncSetAttribute(igemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
     attr_set = true;
   }
-  dim3 grid((unsigned)ceil_div(a.m_total, kBM), (unsigned)a.n_tiles, (unsigned)groups);
+  IgemmArgs a = a0;
+  a.groups = (int32_t)groups;
+  const int64_t tiles = ceil_div(a.m_total, kBM) * a.n_tiles * groups;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
   igemm_kernel<KIND><<<grid, kThreads, igemm_smem_bytes(a.n_rows), s>>>(a);
   count_launch();
   QNB_CUDA(cudaGetLastError());

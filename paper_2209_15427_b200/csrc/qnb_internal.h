@@ -91,6 +91,7 @@ struct IgemmArgs {
   // B operand: packed, pre-swizzled [G][n_tiles][num_kb][n_rows][128 B]
   const uint8_t* b;
   int32_t n_rows, n_tiles, n_real, n_per_tile, ones_col, tmem_cols;
+  int32_t groups;             // set by igemm_launch
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)
@@ -103,7 +104,15 @@ struct IgemmArgs {
   uint8_t* out;
   int64_t o_img, o_row, o_pix, o_origin;  // byte strides / origin
   int32_t o_es, o_vec;                     // element bytes; 16-byte stores allowed
+  // 1: the host proved every accumulator (dot + chan_const - zw*rowsum) fits int32 and
+  // 1 <= s <= 62, so the requant runs as one 32x32->64 multiply + 64-bit round;
+  // 0: exact 128-bit path (src/quantizer.cpp:201-212 verbatim).
+  int32_t fast_rq;
 };
+
+// Host proof for IgemmArgs::fast_rq: bounds of the int64 accumulator over all
+// inputs (u8 x u8 dot in [0, 255*255*K], rowsum in [0, 255*K]).
+bool igemm_fast_requant_ok(const std::vector<int64_t>& chan_const, int64_t K, int64_t zw, const Requant& rq);
 
 // Host description of one contraction (conv or inner product) to compile.
 struct IgemmGeometry {

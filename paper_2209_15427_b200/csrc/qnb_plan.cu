@@ -548,6 +548,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
       cc[(size_t)oc] = c;
     }
     QNB_TRY(upload(P, cc, const_cast<int64_t**>(&a.chan_const)));
+    a.fast_rq = igemm_fast_requant_ok(cc, K, qw.zero, a.rq) ? 1 : 0;
     a.epi = EPI_Q8;
     if (op.relu >= 0) {
       const Blob& rtop = P.blobs[P.layers[op.relu].top];
