@@ -234,6 +234,14 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     QNB_CUDA(cudaMemcpyAsync(d_cc, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice, s));
     a.chan_const = d_cc;
     a.fast_rq = igemm_fast_requant_ok(cc, K, zw, a.rq) ? 1 : 0;
+    if (a.fast_rq) {
+      std::vector<int32_t> cc32(cc.begin(), cc.end());
+      int32_t* d32 = nullptr;
+      QNB_TRY(tmp.alloc((void**)&d32, cc32.size() * 4));
+      QNB_CUDA(cudaMemcpyAsync(d32, cc32.data(), cc32.size() * 4, cudaMemcpyHostToDevice, s));
+      QNB_CUDA(cudaStreamSynchronize(s));
+      a.chan_const32 = d32;
+    }
     a.epi = EPI_Q8;
   } else {
     a.bias = bias_dev;

@@ -71,6 +71,157 @@ __device__ __forceinline__ int64_t requant_fast(int32_t acc, const Requant& rq) 
   return v < rq.out_min ? rq.out_min : (v > rq.out_max ? rq.out_max : v);
 }
 
+// ---------------------------------------------------------------- epilogue
+// Per-element tails, specialised per layer so the per-element code is branch-free.
+struct Q8Consts {
+  int64_t mult, half, mask;
+  int32_t s, oz, omin, omax;
+  int32_t rz, rsb, rsh, rzo, rmin, rmax;
+  int64_t rmult;
+};
+
+// requant_clamp (fast form, see requant_fast) followed by the truncating INT8 ReLU
+// requant (src/ops.cpp:156-181) with 32-bit Acctype wrap-around.
+template <bool RELU>
+__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k) {
+  const int64_t pr = (int64_t)acc * k.mult;
+  const int64_t t = pr + k.half;
+  int64_t q = t >> k.s;
+  if ((t & k.mask) == 0) q &= ~1LL;  // exact tie -> even
+  int32_t v = (int32_t)q + k.oz;
+  v = v < k.omin ? k.omin : (v > k.omax ? k.omax : v);
+  if constexpr (RELU) {
+    int32_t d = v - k.rz;
+    d = d > 0 ? d : 0;
+    int32_t reg = (int32_t)(uint32_t)(uint64_t)(((int64_t)d * k.rmult) >> k.rsb);
+    reg = k.rsh >= 0 ? (reg >> k.rsh) : (int32_t)((uint32_t)reg << (-k.rsh));
+    int32_t o = (int32_t)((uint32_t)reg + (uint32_t)k.rzo);
+    v = o < k.rmin ? k.rmin : (o > k.rmax ? k.rmax : o);
+  }
+  return (uint32_t)v;
+}
+
+template <int MODE>
+__device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
+                                               uint64_t* acc_empty, int64_t m_tiles, int64_t total, int warp,
+                                               int lane) {
+  const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
+  const int half = (warp - 5) >> 2;  // which 16-column blocks of the tile
+  const int64_t pix_per_img = (int64_t)p.oh * p.ow;
+  Q8Consts k;
+  k.mult = p.rq.mult;
+  k.s = p.rq.s;
+  k.half = (MODE == EPIM_Q8_FAST || MODE == EPIM_Q8_FAST_RELU) ? (1LL << (p.rq.s - 1)) : 0;
+  k.mask = (k.half << 1) - 1;
+  k.oz = (int32_t)p.rq.out_zero;
+  k.omin = (int32_t)p.rq.out_min;
+  k.omax = (int32_t)p.rq.out_max;
+  k.rz = (int32_t)p.relu.in_zero;
+  k.rmult = p.relu.mult;
+  k.rsb = p.relu.shift_bits;
+  k.rsh = p.relu.shift;
+  k.rzo = (int32_t)p.relu.out_zero;
+  k.rmin = (int32_t)p.relu.out_min;
+  k.rmax = (int32_t)p.relu.out_max;
+  const int n_tiles = p.n_tiles, n_real = p.n_real, npt = p.n_per_tile, tcols = p.tmem_cols;
+  const int ones_col = p.ones_col, o_es = p.o_es, o_vec = p.o_vec, has_relu = p.has_relu;
+  const int64_t zw = p.zw;
+  const float slope = p.slope;
+  uint32_t j = 0;
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++j) {
+    const TileCoord c = tile_of(tile, m_tiles, n_tiles);
+    const uint32_t buf = j & 1;
+    mbar_wait(&acc_full[buf], (j >> 1) & 1);
+    tc_fence_after();
+    const uint32_t trow = tmem + buf * (uint32_t)tcols + ((uint32_t)(32 * quarter) << 16);
+    const int64_t row = c.mt * kBM + 32 * quarter + lane;
+    const bool ok = row < p.m_total;
+    uint8_t* obase = p.out;
+    if (ok) {
+      const int64_t img = row / pix_per_img;
+      const int64_t rem = row - img * pix_per_img;
+      const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
+      obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+    }
+    int64_t rowsum = 0;
+    if (ones_col >= 0) {
+      uint32_t v;
+      tmem_ld1(trow + (uint32_t)ones_col, v);
+      tmem_ld_wait();
+      rowsum = (int64_t)(int32_t)v;
+    }
+    const int32_t rowterm32 = (int32_t)(-zw * rowsum);
+    const int n0 = c.nt * npt;
+    const int n_here = min(npt, n_real - n0);
+    const int ch0 = c.g * n_real + n0;
+    for (int cb = half * 16; cb < n_here; cb += 32) {
+      uint32_t r[16];
+      tmem_ld16(trow + (uint32_t)cb, r);
+      tmem_ld_wait();
+      if (!ok) continue;
+      const int cnt = min(16, n_here - cb);
+      uint8_t* dst = obase + (int64_t)(ch0 + cb) * o_es;
+      if constexpr (MODE == EPIM_Q8_FAST || MODE == EPIM_Q8_FAST_RELU) {
+        constexpr bool RELU = MODE == EPIM_Q8_FAST_RELU;
+        if (cnt == 16) {
+          const int4* cc4 = reinterpret_cast<const int4*>(p.chan_const32 + ch0 + cb);
+          uint32_t w[4];
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            const int4 cc = __ldg(cc4 + qd);
+            const uint32_t b0 = q8_fast<RELU>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k);
+            const uint32_t b1 = q8_fast<RELU>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k);
+            const uint32_t b2 = q8_fast<RELU>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k);
+            const uint32_t b3 = q8_fast<RELU>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k);
+            w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+          }
+          if (o_vec) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dst[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < cnt)
+              dst[i] = (uint8_t)q8_fast<RELU>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k);
+        }
+      } else if constexpr (MODE == EPIM_Q8_EXACT) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i >= cnt) continue;
+          int64_t q = requant_clamp((int64_t)(int32_t)r[i] + __ldg(p.chan_const + ch0 + cb + i) - zw * rowsum, p.rq);
+          if (has_relu) q = relu_requant(q, p.relu);
+          dst[i] = (uint8_t)q;
+        }
+      } else {
+        const float* bias = p.bias;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i >= cnt) continue;
+          float v = __uint_as_float(r[i]);
+          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + ch0 + cb + i));
+          if constexpr (MODE == EPIM_F16) {
+            __half hv = __float2half_rn(v);
+            if (has_relu) {
+              const float x = __half2float(hv);
+              hv = __float2half_rn(x > 0.0f ? x : __fmul_rn(x, slope));
+            }
+            reinterpret_cast<__half*>(dst)[i] = hv;
+          } else {
+            if (has_relu) v = v > 0.0f ? v : __fmul_rn(v, slope);
+            reinterpret_cast<float*>(dst)[i] = v;
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&acc_empty[buf]);
+  }
+}
+
 // Persistent, warp-specialised implicit GEMM.  One CTA per SM loops over output
 // tiles (128 pixels x n_rows channels of one group):
 //   warps 0-3  A producers: thread t gathers row t of the tile with cp.async (16 B
@@ -179,105 +330,21 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int quarter = warp & 3;           // TMEM lanes 32*quarter .. +31
-    const int half = (warp - 5) >> 2;       // which 16-column blocks of the tile
-    uint32_t j = 0;
-    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++j) {
-      const TileCoord c = tile_of(tile, m_tiles, p.n_tiles);
-      const uint32_t buf = j & 1;
-      mbar_wait(&acc_full[buf], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t trow = tmem + buf * (uint32_t)p.tmem_cols + ((uint32_t)(32 * quarter) << 16);
-      const int64_t row = c.mt * kBM + 32 * quarter + lane;
-      const bool ok = row < p.m_total;
-      uint8_t* obase = p.out;
-      if (ok) {
-        const int64_t img = row / pix_per_img;
-        const int64_t rem = row - img * pix_per_img;
-        const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-        obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
-      }
-      int64_t rowsum = 0;
-      if (p.ones_col >= 0) {
-        uint32_t v;
-        tmem_ld1(trow + (uint32_t)p.ones_col, v);
-        tmem_ld_wait();
-        rowsum = (int64_t)(int32_t)v;
-      }
-      const int32_t rowterm32 = (int32_t)(-p.zw * rowsum);
-      const int n0 = c.nt * p.n_per_tile;
-      const int n_here = min(p.n_per_tile, p.n_real - n0);
-      const int ch0 = c.g * p.n_real + n0;
-      for (int cb = half * 16; cb < n_here; cb += 32) {
-        uint32_t r[16];
-        tmem_ld16(trow + (uint32_t)cb, r);
-        tmem_ld_wait();
-        if (!ok) continue;
-        const int cnt = min(16, n_here - cb);
-        uint8_t* dst = obase + (int64_t)(ch0 + cb) * p.o_es;
-        if (p.epi == EPI_Q8) {
-          uint32_t packed[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i < cnt) {
-              const int64_t cc = __ldg(p.chan_const + ch0 + cb + i);
-              int64_t q;
-              if (p.fast_rq)
-                q = requant_fast((int32_t)r[i] + (int32_t)cc + rowterm32, p.rq);
-              else
-                q = requant_clamp((int64_t)(int32_t)r[i] + cc - p.zw * rowsum, p.rq);
-              if (p.has_relu) q = relu_requant(q, p.relu);
-              packed[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
-            }
-          }
-          if (cnt == 16 && p.o_vec) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-          } else {
-            for (int i = 0; i < cnt; ++i) dst[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
-          }
-        } else {
-          float y[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float v = __uint_as_float(r[i]);
-            if (p.bias != nullptr && i < cnt) v = __fadd_rn(v, __ldg(p.bias + ch0 + cb + i));
-            y[i] = v;
-          }
-          if (p.epi == EPI_F16) {
-            __align__(16) __half h[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              __half hv = __float2half_rn(y[i]);
-              if (p.has_relu) {
-                const float x = __half2float(hv);
-                hv = __float2half_rn(x > 0.0f ? x : __fmul_rn(x, p.slope));
-              }
-              h[i] = hv;
-            }
-            if (cnt == 16 && p.o_vec) {
-              const uint4* src = reinterpret_cast<const uint4*>(h);
-              reinterpret_cast<uint4*>(dst)[0] = src[0];
-              reinterpret_cast<uint4*>(dst)[1] = src[1];
-            } else {
-              for (int i = 0; i < cnt; ++i) reinterpret_cast<__half*>(dst)[i] = h[i];
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (p.has_relu) y[i] = y[i] > 0.0f ? y[i] : __fmul_rn(y[i], p.slope);
-            if (cnt == 16 && p.o_vec) {
-              const uint4* src = reinterpret_cast<const uint4*>(y);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(dst)[q] = src[q];
-            } else {
-              for (int i = 0; i < cnt; ++i) reinterpret_cast<float*>(dst)[i] = y[i];
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    switch (p.epi_mode) {
+      case EPIM_Q8_FAST_RELU:
+        epilogue_tiles<EPIM_Q8_FAST_RELU>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        break;
+      case EPIM_Q8_FAST:
+        epilogue_tiles<EPIM_Q8_FAST>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        break;
+      case EPIM_Q8_EXACT:
+        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        break;
+      case EPIM_F16:
+        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        break;
+      default:
+        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
     }
   }
 
@@ -460,6 +527,13 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   }
   IgemmArgs a = a0;
   a.groups = (int32_t)groups;
+  if (a.epi == EPI_Q8) {
+    const bool fast = a.fast_rq && a.chan_const32 != nullptr;
+    a.epi_mode = fast ? (a.has_relu ? (a.relu.acc32 ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
+                      : EPIM_Q8_EXACT;
+  } else {
+    a.epi_mode = a.epi == EPI_F16 ? EPIM_F16 : EPIM_F32;
+  }
   const int64_t tiles = ceil_div(a.m_total, kBM) * a.n_tiles * groups;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
   igemm_kernel<KIND><<<grid, kThreads, igemm_smem_bytes(a.n_rows), s>>>(a);

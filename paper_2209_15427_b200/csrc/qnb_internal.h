@@ -65,6 +65,8 @@ struct ActLayout {
 
 // ------------------------------------------------- implicit GEMM (tcgen05)
 enum EpiKind : int { EPI_Q8 = 0, EPI_F16 = 1, EPI_F32 = 2 };
+// Epilogue specialisation chosen on the host (igemm_launch).
+enum EpiMode : int { EPIM_Q8_FAST_RELU = 0, EPIM_Q8_FAST = 1, EPIM_Q8_EXACT = 2, EPIM_F16 = 3, EPIM_F32 = 4 };
 
 // Device copies of the reference's RequantParams, pre-digested:
 // s = shift_bits + shift (src/quantizer.cpp:202).
@@ -95,6 +97,8 @@ struct IgemmArgs {
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)
+  const int32_t* chan_const32;  // int32 copy when fast_rq
+  int32_t epi_mode;           // EpiMode, set by igemm_launch
   const float* bias;          // [G * n_real] or null (float)
   int64_t zw;                 // weight zero point, multiplies the ones-column sum
   Requant rq;

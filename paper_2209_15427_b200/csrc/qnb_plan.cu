@@ -549,6 +549,10 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     }
     QNB_TRY(upload(P, cc, const_cast<int64_t**>(&a.chan_const)));
     a.fast_rq = igemm_fast_requant_ok(cc, K, qw.zero, a.rq) ? 1 : 0;
+    if (a.fast_rq) {
+      std::vector<int32_t> cc32(cc.begin(), cc.end());
+      QNB_TRY(upload(P, cc32, const_cast<int32_t**>(&a.chan_const32)));
+    }
     a.epi = EPI_Q8;
     if (op.relu >= 0) {
       const Blob& rtop = P.blobs[P.layers[op.relu].top];

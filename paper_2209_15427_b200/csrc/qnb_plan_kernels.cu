@@ -43,6 +43,24 @@ __device__ __forceinline__ int64_t qz(float x, const DevQ& q) {
   if (v >= (double)q.i_max) return q.i_max;
   return (int64_t)v;
 }
+// Same result as qz(): the float product decides the integer whenever it lies more
+// than 4e-7 relative (3x its worst-case error) away from a rounding boundary; ties,
+// NaN and infinities take the exact double path.
+__device__ __forceinline__ int64_t qz_fast(float x, const DevQ& q, float invf) {
+  const float yf = __fmul_rn(x, invf);
+  const float ay = fabsf(yf);
+  if (ay < 4194304.0f) {
+    const float d = yf - floorf(yf);
+    if (fabsf(d - 0.5f) > __fmaf_rn(4e-7f, ay, 1e-6f)) {
+      const int32_t v = (int32_t)rintf(yf) + (int32_t)q.zero;
+      return v < q.i_min ? q.i_min : (v > q.i_max ? q.i_max : v);
+    }
+  } else if (ay <= 3.0e38f) {
+    return yf > 0.0f ? q.i_max : q.i_min;  // |x/scale| >= 2^22: saturated either way
+  }
+  return qz(x, q);
+}
+
 __device__ __forceinline__ float dq(int64_t v, const DevQ& q) {
   return __double2float_rn(__dmul_rn((double)(v - q.zero), q.scale));
 }
@@ -102,6 +120,7 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
   uint8_t* o = at(dst, L, n, y, x);
   const int ses = src_dtype == QNB_FP32 ? 4 : 2;
   const uint8_t* s = src + ((n * C) * plane + y * W + x) * ses;
+  const float invf = (float)q.inv;
   if (dst_dtype == QNB_INT8Q && L.c_phys <= 16 && (L.c_phys & 3) == 0) {
     uint32_t words[4] = {0, 0, 0, 0};
 #pragma unroll 4
@@ -110,7 +129,7 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
       if (c < C) {
         const float f = src_dtype == QNB_FP32 ? reinterpret_cast<const float*>(s)[c * plane]
                                               : h2f_bits(reinterpret_cast<const uint16_t*>(s)[c * plane]);
-        v = (uint32_t)qz(f, q);
+        v = (uint32_t)qz_fast(f, q, invf);
       }
       words[c >> 2] |= (v & 0xFFu) << (8 * (c & 3));
     }
@@ -211,14 +230,19 @@ __global__ void pool_generic_kernel(const uint8_t* __restrict__ src, DevLayout S
 // float evaluation (relative error < 1.1e-6) decides the integer
 // unless the value lies within 3e-6 relative of a rounding boundary; only then does
 // the exact double pow path run, so the result is bit-identical either way.
-constexpr int kLrnMaxC = 512;
-constexpr int kLrnPix = 8;
 constexpr int kLrnThreads = 256;
+__host__ __device__ inline int lrn_pixels(int64_t C) {
+  int64_t p = 16384 / (C > 0 ? C : 1);
+  return (int)(p < 8 ? 8 : (p > 256 ? 256 : p));
+}
 
 __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
-  __shared__ float sx[kLrnPix][kLrnMaxC];
+  extern __shared__ float lrn_smem[];
   __shared__ float lut[256];
   const int64_t C = a.D.c;
+  const int kLrnPix = lrn_pixels(C);
+  float* sxb = lrn_smem;  // [kLrnPix][C]
+#define sx(pi, c) sxb[(int64_t)(pi) * C + (c)]
   const bool q8 = a.in_dtype == QNB_INT8Q;
   if (q8)
     for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dq(v, a.in_q);
@@ -253,7 +277,7 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
       }
       const uint32_t w4[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
-      for (int b = 0; b < 16; ++b) sx[pi][ch * 16 + b] = lut[(w4[b >> 2] >> (8 * (b & 3))) & 0xFFu];
+      for (int b = 0; b < 16; ++b) sx(pi, ch * 16 + b) = lut[(w4[b >> 2] >> (8 * (b & 3))) & 0xFFu];
     }
   } else {
     for (int item = threadIdx.x; item < np * C; item += blockDim.x) {
@@ -284,13 +308,13 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
       } else {
         v = load_as_float(at(a.src, a.S, n, oy, ox) + c * a.S.es, a.in_dtype, a.in_q);
       }
-      sx[pi][c] = v;
+      sx(pi, c) = v;
     }
   }
   __syncthreads();
   // ---- stage 2
   const bool qout = a.out_dtype == QNB_INT8Q || a.out_dtype == QNB_INT16Q;
-  const float fa_n = (float)a.a_n, fbeta = (float)a.beta, fk = (float)a.k, fscale = (float)a.out_q.scale;
+  const float fa_n = (float)a.a_n, fbeta = (float)a.beta, fk = (float)a.k, finv = (float)(1.0 / a.out_q.scale);
   for (int item = threadIdx.x; item < np * C; item += blockDim.x) {
     const int pi = item / (int)C;
     const int64_t c = item % C;
@@ -298,14 +322,14 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
     const int64_t oy = pp / a.D.w, ox = pp % a.D.w;
     const int64_t c0 = c - a.half < 0 ? 0 : c - a.half;
     const int64_t c1 = c + a.half > C - 1 ? C - 1 : c + a.half;
-    const float x = sx[pi][c];
+    const float x = sx(pi, c);
     uint8_t* o = at(a.dst, a.D, n, oy, ox) + c * a.D.es;
     if (qout) {
       float sf = 0.0f;
-      for (int64_t cc = c0; cc <= c1; ++cc) sf = __fadd_rn(sf, __fmul_rn(sx[pi][cc], sx[pi][cc]));
+      for (int64_t cc = c0; cc <= c1; ++cc) sf = __fadd_rn(sf, __fmul_rn(sx(pi, cc), sx(pi, cc)));
       const float base = __fadd_rn(fk, __fmul_rn(fa_n, sf));
-      const float den = exp2f(__fmul_rn(fbeta, log2f(base)));
-      const float t = __fdiv_rn(__fdiv_rn(x, den), fscale);
+      const float rden = exp2f(-__fmul_rn(fbeta, log2f(base)));
+      const float t = __fmul_rn(__fmul_rn(x, rden), finv);
       const float fl = floorf(t);
       const float margin = 3e-6f * fabsf(t) + 1e-6f;
       if (isfinite(t) && fabsf(t) < 1e6f && base > 0.0f && fabsf(t - fl - 0.5f) > margin) {
@@ -319,13 +343,14 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
     }
     double sum = 0.0;
     for (int64_t cc = c0; cc <= c1; ++cc) {
-      const double v = (double)sx[pi][cc];
+      const double v = (double)sx(pi, cc);
       sum = __dadd_rn(sum, __dmul_rn(v, v));
     }
     const double base = __dadd_rn(a.k, __dmul_rn(a.a_n, sum));
     const float y = __double2float_rn(__ddiv_rn((double)x, pow(base, a.beta)));
     store_from_float(o, a.out_dtype, y, a.out_q);
   }
+#undef sx
 }
 
 // ---------------------------------------------------------------- convert
@@ -445,8 +470,14 @@ void launch_pool(const PoolArgs& p, cudaStream_t s) {
 }
 
 void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
-  const int64_t blocks = a.D.n * ceil_div(a.D.h * a.D.w, kLrnPix);
-  pool_lrn_kernel<<<(unsigned)blocks, kLrnThreads, 0, s>>>(a);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pool_lrn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    attr = true;
+  }
+  const int pix = lrn_pixels(a.D.c);
+  const int64_t blocks = a.D.n * ceil_div(a.D.h * a.D.w, pix);
+  pool_lrn_kernel<<<(unsigned)blocks, kLrnThreads, (size_t)pix * a.D.c * 4, s>>>(a);
 }
 
 void launch_convert(const ConvertArgs& a, cudaStream_t s) {
