@@ -82,6 +82,21 @@ int64_t bias_to_acc(float b, double scale_a, double scale_b) {
 
 int default_shift_bits(int dtype) { return dtype == QNB_INT8Q ? 31 : 15; }
 
+// src/ops.cpp:156-181
+int64_t relu_requant_host(int64_t q, const qnb_requant& r, int dtype) {
+  const bool acc32 = dtype == QNB_INT8Q;
+  auto wrap = [acc32](int64_t v) { return acc32 ? (int64_t)(int32_t)(uint32_t)v : v; };
+  int64_t d = q - r.in_zero;
+  d = d > 0 ? d : 0;
+  int64_t reg = wrap((d * r.mult) >> r.shift_bits);
+  if (r.shift >= 0)
+    reg = wrap(reg >> r.shift);
+  else
+    reg = wrap((int64_t)((uint64_t)reg << (unsigned)(-r.shift)));
+  const int64_t v = wrap(reg + r.out_zero);
+  return v < r.out_min ? r.out_min : (v > r.out_max ? r.out_max : v);
+}
+
 qnb_status launch_nchw_to_nhwc(const void* in, int dtype, int64_t N, int64_t C, int64_t H, int64_t W,
                                const ActLayout& L, double fill, void* out, cudaStream_t s);
 qnb_status launch_nhwc_to_nchw(const void* in, int dtype, const ActLayout& L, void* out, cudaStream_t s);

@@ -42,7 +42,7 @@ __host__ __device__ inline int igemm_stages(int n_rows) {
   return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
 }
 __host__ __device__ inline size_t igemm_smem_bytes(int n_rows) {
-  return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16;
+  return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16 + 256;
 }
 
 struct TileCoord {
@@ -83,28 +83,26 @@ struct Q8Consts {
 // requant_clamp (fast form, see requant_fast) followed by the truncating INT8 ReLU
 // requant (src/ops.cpp:156-181) with 32-bit Acctype wrap-around.
 template <bool RELU>
-__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k) {
+__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const uint8_t* lut) {
   const int64_t pr = (int64_t)acc * k.mult;
   const int64_t t = pr + k.half;
   int64_t q = t >> k.s;
   if ((t & k.mask) == 0) q &= ~1LL;  // exact tie -> even
   int32_t v = (int32_t)q + k.oz;
   v = v < k.omin ? k.omin : (v > k.omax ? k.omax : v);
-  if constexpr (RELU) {
-    int32_t d = v - k.rz;
-    d = d > 0 ? d : 0;
-    int32_t reg = (int32_t)(uint32_t)(uint64_t)(((int64_t)d * k.rmult) >> k.rsb);
-    reg = k.rsh >= 0 ? (reg >> k.rsh) : (int32_t)((uint32_t)reg << (-k.rsh));
-    int32_t o = (int32_t)((uint32_t)reg + (uint32_t)k.rzo);
-    v = o < k.rmin ? k.rmin : (o > k.rmax ? k.rmax : o);
-  }
+  if constexpr (RELU) return lut[v];  // relu_quant of the 256 possible inputs, tabulated on the host
   return (uint32_t)v;
 }
 
 template <int MODE>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
                                                uint64_t* acc_empty, int64_t m_tiles, int64_t total, int warp,
-                                               int lane) {
+                                               int lane, uint8_t* lut) {
+  if constexpr (MODE == EPIM_Q8_FAST_RELU) {
+    const int et = threadIdx.x - 5 * 32;  // 0 .. 255 across the epilogue warps
+    lut[et] = p.relu_lut[et];
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  }
   const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
   const int half = (warp - 5) >> 2;  // which 16-column blocks of the tile
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
@@ -169,10 +167,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int qd = 0; qd < 4; ++qd) {
             const int4 cc = __ldg(cc4 + qd);
-            const uint32_t b0 = q8_fast<RELU>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k);
-            const uint32_t b1 = q8_fast<RELU>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k);
-            const uint32_t b2 = q8_fast<RELU>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k);
-            const uint32_t b3 = q8_fast<RELU>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k);
+            const uint32_t b0 = q8_fast<RELU>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut);
+            const uint32_t b1 = q8_fast<RELU>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut);
+            const uint32_t b2 = q8_fast<RELU>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut);
+            const uint32_t b3 = q8_fast<RELU>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut);
             w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           if (o_vec) {
@@ -185,7 +183,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (i < cnt)
-              dst[i] = (uint8_t)q8_fast<RELU>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k);
+              dst[i] = (uint8_t)q8_fast<RELU>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut);
         }
       } else if constexpr (MODE == EPIM_Q8_EXACT) {
 #pragma unroll
@@ -244,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   uint64_t* acc_full = empty + kMaxStages;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+  uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m_tiles = (p.m_total + kBM - 1) / kBM;
@@ -332,19 +331,19 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     // ---------------------------------------------------------------- epilogue
     switch (p.epi_mode) {
       case EPIM_Q8_FAST_RELU:
-        epilogue_tiles<EPIM_Q8_FAST_RELU>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        epilogue_tiles<EPIM_Q8_FAST_RELU>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
         break;
       case EPIM_Q8_FAST:
-        epilogue_tiles<EPIM_Q8_FAST>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        epilogue_tiles<EPIM_Q8_FAST>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
         break;
       case EPIM_Q8_EXACT:
-        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
         break;
       case EPIM_F16:
-        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
         break;
       default:
-        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane);
+        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
     }
   }
 
@@ -529,7 +528,7 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   a.groups = (int32_t)groups;
   if (a.epi == EPI_Q8) {
     const bool fast = a.fast_rq && a.chan_const32 != nullptr;
-    a.epi_mode = fast ? (a.has_relu ? (a.relu.acc32 ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
+    a.epi_mode = fast ? (a.has_relu ? ((a.relu.acc32 && a.relu_lut) ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
                       : EPIM_Q8_EXACT;
   } else {
     a.epi_mode = a.epi == EPI_F16 ? EPIM_F16 : EPIM_F32;

@@ -43,6 +43,8 @@ double round_half_even(double x);
 qnb_status requant_from_ratio(double r, int64_t in_zero, const qnb_qvals& out, int sb,
                               qnb_requant* rq);
 int64_t bias_to_acc(float b, double scale_a, double scale_b);
+// Host copy of the truncating ReLU requant (src/ops.cpp:156-181).
+int64_t relu_requant_host(int64_t q, const qnb_requant& r, int dtype);
 
 // ------------------------------------------------- device activation layout
 // NHWC activation with a border ("halo") of hh rows / hw columns on each side,
@@ -104,6 +106,7 @@ struct IgemmArgs {
   Requant rq;
   ReluRequant relu;
   int32_t has_relu;
+  const uint8_t* relu_lut;    // [256] relu_quant of every INT8 conv output (fast path)
   float slope;
   uint8_t* out;
   int64_t o_img, o_row, o_pix, o_origin;  // byte strides / origin

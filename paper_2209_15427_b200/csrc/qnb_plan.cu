@@ -561,6 +561,9 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
                                  default_shift_bits(dtype), &r2));
       a.relu = to_dev_relu(r2, dtype);
       a.has_relu = 1;
+      std::vector<uint8_t> lut(256);
+      for (int q = 0; q < 256; ++q) lut[(size_t)q] = (uint8_t)relu_requant_host(q, r2, dtype);
+      QNB_TRY(upload(P, lut, const_cast<uint8_t**>(&a.relu_lut)));
     }
   } else {
     if (l.bias_term && l.bias) {

@@ -154,6 +154,39 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
   }
 }
 
+// FP32 NCHW with <= 4 channels -> u8 NHWC4 (AlexNet/VGG RGB input): each thread
+// issues all loads of kRows rows x 4 planes before converting, so enough bytes are in
+// flight to run the 158 MB read at HBM rate.
+constexpr int kPackRows = 8;
+__global__ void __launch_bounds__(256) pack_rgb_u8_kernel(const float* __restrict__ src, int C, int H, int W,
+                                                          uint8_t* __restrict__ dst, DevLayout L, DevQ q,
+                                                          uint32_t fill) {
+  const int y0 = blockIdx.x * kPackRows;
+  const int64_t n = blockIdx.y;
+  const int64_t plane = (int64_t)H * W;
+  const float invf = (float)q.inv;
+  const float* img = src + n * C * plane;
+  for (int x = threadIdx.x; x < W; x += blockDim.x) {
+    float v[kPackRows][4];
+#pragma unroll
+    for (int r = 0; r < kPackRows; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        v[r][c] = (c < C && y0 + r < H) ? __ldg(img + c * plane + (int64_t)(y0 + r) * W + x) : 0.0f;
+#pragma unroll
+    for (int r = 0; r < kPackRows; ++r) {
+      if (y0 + r >= H) break;
+      uint32_t w = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t b = c < C ? (uint32_t)qz_fast(v[r][c], q, invf) : fill;
+        w |= (b & 0xFFu) << (8 * c);
+      }
+      *reinterpret_cast<uint32_t*>(at(dst, L, n, y0 + r, x)) = w;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ pool
 // Max over k x k windows (no padding).  Integer types compare raw values; float
 // types keep the first element unless a later one is strictly greater.
@@ -353,6 +386,92 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
 #undef sx
 }
 
+// INT8 -> INT8 specialisation of pool_lrn (the AlexNet norm layers): the PK x PK
+// window of 16-byte channel vectors is loaded in one unrolled batch (enough bytes in
+// flight to cover HBM latency), pooled with __vmaxu4, dequantised through the LUT;
+// stage 2 produces 4 channels per thread with one 32-bit store.
+template <int PK>
+__global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a) {
+  extern __shared__ float lrn_smem[];
+  __shared__ float lut[256];
+  const int C = (int)a.D.c;
+  const int P = lrn_pixels(C);
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dq(v, a.in_q);
+  const int pix_per_img = (int)(a.D.h * a.D.w);
+  const int tiles_per_img = (pix_per_img + P - 1) / P;
+  const int64_t n = blockIdx.x / tiles_per_img;
+  const int p0 = (blockIdx.x % tiles_per_img) * P;
+  const int np = min(P, pix_per_img - p0);
+  const int Dw = (int)a.D.w;
+  __syncthreads();
+  const int chunks = C >> 4;
+  for (int item = threadIdx.x; item < np * chunks; item += blockDim.x) {
+    const int pi = item / chunks, ch = item - pi * chunks;
+    const int pp = p0 + pi;
+    const int oy = pp / Dw, ox = pp - oy * Dw;
+    uint4 v[PK > 0 ? PK * PK : 1];
+    if constexpr (PK > 0) {
+#pragma unroll
+      for (int ky = 0; ky < PK; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < PK; ++kx)
+          v[ky * PK + kx] =
+              __ldg(reinterpret_cast<const uint4*>(at(a.src, a.S, n, oy * a.pool_s + ky, ox * a.pool_s + kx) + ch * 16));
+#pragma unroll
+      for (int i = 1; i < PK * PK; ++i) {
+        v[0].x = __vmaxu4(v[0].x, v[i].x);
+        v[0].y = __vmaxu4(v[0].y, v[i].y);
+        v[0].z = __vmaxu4(v[0].z, v[i].z);
+        v[0].w = __vmaxu4(v[0].w, v[i].w);
+      }
+    } else {
+      v[0] = __ldg(reinterpret_cast<const uint4*>(at(a.src, a.S, n, oy, ox) + ch * 16));
+    }
+    const uint32_t w4[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
+    float* row = lrn_smem + pi * C + ch * 16;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) row[b] = lut[(w4[b >> 2] >> (8 * (b & 3))) & 0xFFu];
+  }
+  __syncthreads();
+  const float fa_n = (float)a.a_n, fbeta = (float)a.beta, fk = (float)a.k, finv = (float)(1.0 / a.out_q.scale);
+  const int half = (int)a.half;
+  const int quads = C >> 2;
+  for (int item = threadIdx.x; item < np * quads; item += blockDim.x) {
+    const int pi = item / quads, c4 = (item - pi * quads) * 4;
+    const int pp = p0 + pi;
+    const int oy = pp / Dw, ox = pp - oy * Dw;
+    const float* row = lrn_smem + pi * C;
+    uint32_t packed = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c4 + u;
+      const int c0 = max(0, c - half), c1 = min(C - 1, c + half);
+      const float x = row[c];
+      float sf = 0.0f;
+      for (int cc = c0; cc <= c1; ++cc) sf = __fadd_rn(sf, __fmul_rn(row[cc], row[cc]));
+      const float base = __fadd_rn(fk, __fmul_rn(fa_n, sf));
+      const float rden = exp2f(-__fmul_rn(fbeta, log2f(base)));
+      const float t = __fmul_rn(__fmul_rn(x, rden), finv);
+      const float fl = floorf(t);
+      uint32_t q;
+      if (isfinite(t) && fabsf(t) < 1e6f && fabsf(t - fl - 0.5f) > __fmaf_rn(3e-6f, fabsf(t), 1e-6f)) {
+        const int32_t v = (int32_t)rintf(t) + (int32_t)a.out_q.zero;
+        q = (uint32_t)(v < a.out_q.i_min ? a.out_q.i_min : (v > a.out_q.i_max ? a.out_q.i_max : v));
+      } else {
+        double sum = 0.0;
+        for (int cc = c0; cc <= c1; ++cc) {
+          const double d = (double)row[cc];
+          sum = __dadd_rn(sum, __dmul_rn(d, d));
+        }
+        const double b = __dadd_rn(a.k, __dmul_rn(a.a_n, sum));
+        q = (uint32_t)qz(__double2float_rn(__ddiv_rn((double)x, pow(b, a.beta))), a.out_q);
+      }
+      packed |= (q & 0xFFu) << (8 * u);
+    }
+    *reinterpret_cast<uint32_t*>(at(a.dst, a.D, n, oy, ox) + c4) = packed;
+  }
+}
+
 // ---------------------------------------------------------------- convert
 // Generic elementwise op between layouts (interior, real channels only).
 __global__ void convert_kernel(ConvertArgs a) {
@@ -451,6 +570,13 @@ static unsigned blocks_for(int64_t n, int threads) {
 }
 
 void launch_pack_input(const PackArgs& p, cudaStream_t s) {
+  if (p.src_dtype == QNB_FP32 && p.dst_dtype == QNB_INT8Q && p.op == PACK_QUANTIZE && p.L.c_phys == 4 &&
+      p.C <= 4 && p.L.pix % 4 == 0 && p.L.origin % 4 == 0 && p.L.row % 4 == 0 && p.L.img % 4 == 0) {
+    dim3 grid((unsigned)ceil_div(p.H, kPackRows), (unsigned)p.N);
+    pack_rgb_u8_kernel<<<grid, 256, 0, s>>>((const float*)p.src, (int)p.C, (int)p.H, (int)p.W, p.dst, p.L, p.q,
+                                            (uint32_t)(int64_t)p.fill);
+    return;
+  }
   const int threads = p.W >= 256 ? 256 : (int)round_up(p.W, 32);
   dim3 grid((unsigned)ceil_div(p.W, threads), (unsigned)p.H, (unsigned)p.N);
   pack_input_kernel<<<grid, threads, 0, s>>>(p.src, p.src_dtype, p.N, p.C, p.H, p.W, p.dst, p.L, p.dst_dtype, p.op,
@@ -477,7 +603,36 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
   }
   const int pix = lrn_pixels(a.D.c);
   const int64_t blocks = a.D.n * ceil_div(a.D.h * a.D.w, pix);
-  pool_lrn_kernel<<<(unsigned)blocks, kLrnThreads, (size_t)pix * a.D.c * 4, s>>>(a);
+  const size_t sm = (size_t)pix * a.D.c * 4;
+  const bool q8 = a.in_dtype == QNB_INT8Q && a.out_dtype == QNB_INT8Q && a.D.c % 16 == 0 && a.S.c == a.D.c &&
+                  a.S.c_phys % 16 == 0 && a.S.pix % 16 == 0 && a.S.row % 16 == 0 && a.S.img % 16 == 0 &&
+                  a.S.origin % 16 == 0 && a.D.pix % 4 == 0 && a.D.row % 4 == 0 && a.D.img % 4 == 0 &&
+                  a.D.origin % 4 == 0;
+  // windows never leave the input: (out-1)*s + k <= in for floor-mode pooling
+  if (q8 && a.pool_k == 3) {
+    static bool at3 = false;
+    if (!at3) {
+      cudaFuncSetAttribute(pool_lrn_q8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      at3 = true;
+    }
+    pool_lrn_q8_kernel<3><<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
+  } else if (q8 && a.pool_k == 2) {
+    static bool at2 = false;
+    if (!at2) {
+      cudaFuncSetAttribute(pool_lrn_q8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      at2 = true;
+    }
+    pool_lrn_q8_kernel<2><<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
+  } else if (q8 && a.pool_k == 0) {
+    static bool at0 = false;
+    if (!at0) {
+      cudaFuncSetAttribute(pool_lrn_q8_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      at0 = true;
+    }
+    pool_lrn_q8_kernel<0><<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
+  } else {
+    pool_lrn_kernel<<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
+  }
 }
 
 void launch_convert(const ConvertArgs& a, cudaStream_t s) {
