@@ -46,6 +46,8 @@ __device__ __forceinline__ int64_t qz(float x, const DevQ& q) {
 // Same result as qz(): the float product decides the integer whenever it lies more
 // than 4e-7 relative (3x its worst-case error) away from a rounding boundary; ties,
 // NaN and infinities take the exact double path.
+__device__ __noinline__ int64_t qz_slow(float x, DevQ q) { return qz(x, q); }
+
 __device__ __forceinline__ int64_t qz_fast(float x, const DevQ& q, float invf) {
   const float yf = __fmul_rn(x, invf);
   const float ay = fabsf(yf);
@@ -58,7 +60,7 @@ __device__ __forceinline__ int64_t qz_fast(float x, const DevQ& q, float invf) {
   } else if (ay <= 3.0e38f) {
     return yf > 0.0f ? q.i_max : q.i_min;  // |x/scale| >= 2^22: saturated either way
   }
-  return qz(x, q);
+  return qz_slow(x, q);
 }
 
 __device__ __forceinline__ float dq(int64_t v, const DevQ& q) {
@@ -386,6 +388,18 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
 #undef sx
 }
 
+// Exact reference LRN value (double sum in channel order, libm-style pow) quantized.
+__device__ __noinline__ int64_t lrn_exact_q(const float* row, int c0, int c1, float x, double k, double a_n,
+                                            double beta, DevQ q) {
+  double sum = 0.0;
+  for (int cc = c0; cc <= c1; ++cc) {
+    const double d = (double)row[cc];
+    sum = __dadd_rn(sum, __dmul_rn(d, d));
+  }
+  const double b = __dadd_rn(k, __dmul_rn(a_n, sum));
+  return qz(__double2float_rn(__ddiv_rn((double)x, pow(b, beta))), q);
+}
+
 // INT8 -> INT8 specialisation of pool_lrn (the AlexNet norm layers): the PK x PK
 // window of 16-byte channel vectors is loaded in one unrolled batch (enough bytes in
 // flight to cover HBM latency), pooled with __vmaxu4, dequantised through the LUT;
@@ -458,13 +472,7 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
         const int32_t v = (int32_t)rintf(t) + (int32_t)a.out_q.zero;
         q = (uint32_t)(v < a.out_q.i_min ? a.out_q.i_min : (v > a.out_q.i_max ? a.out_q.i_max : v));
       } else {
-        double sum = 0.0;
-        for (int cc = c0; cc <= c1; ++cc) {
-          const double d = (double)row[cc];
-          sum = __dadd_rn(sum, __dmul_rn(d, d));
-        }
-        const double b = __dadd_rn(a.k, __dmul_rn(a.a_n, sum));
-        q = (uint32_t)qz(__double2float_rn(__ddiv_rn((double)x, pow(b, a.beta))), a.out_q);
+        q = (uint32_t)lrn_exact_q(row, c0, c1, x, a.k, a.a_n, a.beta, a.out_q);
       }
       packed |= (q & 0xFFu) << (8 * u);
     }
