@@ -96,8 +96,8 @@ __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, cons
 
 template <int MODE>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
-                                               uint64_t* acc_empty, int64_t m_tiles, int64_t total, int warp,
-                                               int lane, uint8_t* lut) {
+                                               uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
+                                               int64_t ncl, int cs, int rank, int warp, int lane, uint8_t* lut) {
   if constexpr (MODE == EPIM_Q8_FAST_RELU) {
     const int et = threadIdx.x - 5 * 32;  // 0 .. 255 across the epilogue warps
     lut[et] = p.relu_lut[et];
@@ -126,13 +126,14 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
   const int64_t zw = p.zw;
   const float slope = p.slope;
   uint32_t j = 0;
-  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++j) {
-    const TileCoord c = tile_of(tile, m_tiles, n_tiles);
+  for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
+    const TileCoord c = tile_of(ct, m_groups, n_tiles);
+    const int64_t mt = c.mt * cs + rank;
     const uint32_t buf = j & 1;
     mbar_wait(&acc_full[buf], (j >> 1) & 1);
     tc_fence_after();
     const uint32_t trow = tmem + buf * (uint32_t)tcols + ((uint32_t)(32 * quarter) << 16);
-    const int64_t row = c.mt * kBM + 32 * quarter + lane;
+    const int64_t row = mt * kBM + 32 * quarter + lane;
     const bool ok = row < p.m_total;
     uint8_t* obase = p.out;
     if (ok) {
@@ -245,14 +246,21 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Cluster of `cs` CTAs sharing each B stage (multicast): cluster-tile ct covers the
+  // m-tiles [mg*cs, mg*cs+cs) of one (group, n-tile); this CTA takes m-tile mg*cs+rank.
+  const int cs = p.cluster;
+  const int rank = cs > 1 ? (int)cluster_ctarank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << cs) - 1u);
+  const int64_t cid = blockIdx.x / cs, ncl = gridDim.x / cs;
   const int64_t m_tiles = (p.m_total + kBM - 1) / kBM;
-  const int64_t total = m_tiles * p.n_tiles * p.groups;
+  const int64_t m_groups = (m_tiles + cs - 1) / cs;
+  const int64_t total = m_groups * p.n_tiles * p.groups;
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 129);  // 128 cp.async arrivals + 1 expect_tx arrival
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], (uint32_t)cs);  // one MMA commit per CTA of the cluster
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -266,25 +274,34 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
+  if (cs > 1) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
     // ---------------------------------------------------------------- producers
+    // Coalesced gather: lane l copies chunk (l & 7) of rows w*32 + (l >> 3) + 4*i,
+    // i = 0..7, so the 8 lanes of a row fetch its 128 contiguous K bytes together.
     const int t = threadIdx.x;
-    const int sw = t & 7;
+    const int jc = lane & 7, rr = lane >> 3;
     uint32_t it = 0;
-    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const TileCoord c = tile_of(tile, m_tiles, p.n_tiles);
-      const int64_t row = c.mt * kBM + t;
-      const bool valid = row < p.m_total;
-      const uint8_t* base = p.a;
-      if (valid) {
-        const int64_t img = row / pix_per_img;
-        const int64_t rem = row - img * pix_per_img;
-        const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-        base = p.a + img * p.a_img + oy * p.stride_h * p.a_row + ox * p.stride_w * p.a_pix +
-               (int64_t)c.g * p.a_group + p.a_origin;
+    for (int64_t ct = cid; ct < total; ct += ncl) {
+      const TileCoord c = tile_of(ct, m_groups, p.n_tiles);
+      const int64_t mt = c.mt * cs + rank;
+      const uint8_t* base[8];
+      uint32_t valid = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t row = mt * kBM + warp * 32 + rr + 4 * i;
+        base[i] = p.a;
+        if (row < p.m_total) {
+          const int64_t img = row / pix_per_img;
+          const int64_t rem = row - img * pix_per_img;
+          const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
+          base[i] = p.a + img * p.a_img + oy * p.stride_h * p.a_row + ox * p.stride_w * p.a_pix +
+                    (int64_t)c.g * p.a_group + p.a_origin;
+          valid |= 1u << i;
+        }
       }
       const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
       for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
@@ -292,13 +309,18 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
         if (t == 0) {
           mbar_arrive_expect_tx(&full[s], (uint32_t)b_stage);
-          bulk_g2s(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s]);
+          if (cs == 1)
+            bulk_g2s(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s]);
+          else if (rank == 0)
+            bulk_g2s_multicast(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s],
+                               cmask);
         }
-        if (valid) {
-          const int32_t* co = p.chunk_off + kb * 8;
-          uint8_t* dst = sA + (size_t)s * kStageA + t * 128;
+        const int32_t off = __ldg(p.chunk_off + kb * 8 + jc);
+        uint8_t* dst = sA + (size_t)s * kStageA;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) cp_async_16(dst + ((j ^ sw) << 4), base + __ldg(co + j));
+        for (int i = 0; i < 8; ++i) {
+          const int row = warp * 32 + rr + 4 * i;
+          if (valid & (1u << i)) cp_async_16(dst + row * 128 + ((jc ^ (row & 7)) << 4), base[i] + off);
         }
         cp_async_arrive_noinc(&full[s]);
       }
@@ -308,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     if (lane == 0) {
       const uint32_t idesc = make_idesc<KIND>(p.n_rows);
       uint32_t it = 0, j = 0;
-      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++j) {
+      for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
         const uint32_t buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -321,7 +343,10 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
           const uint64_t bd = smem_desc_sw128(sB + (size_t)s * b_stage);
 #pragma unroll
           for (int k = 0; k < 4; ++k) umma<KIND>(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          tc_commit(&empty[s]);
+          if (cs == 1)
+            tc_commit(&empty[s]);
+          else
+            tc_commit_multicast(&empty[s], cmask);
         }
         tc_commit(&acc_full[buf]);
       }
@@ -331,24 +356,25 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     // ---------------------------------------------------------------- epilogue
     switch (p.epi_mode) {
       case EPIM_Q8_FAST_RELU:
-        epilogue_tiles<EPIM_Q8_FAST_RELU>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
+        epilogue_tiles<EPIM_Q8_FAST_RELU>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       case EPIM_Q8_FAST:
-        epilogue_tiles<EPIM_Q8_FAST>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
+        epilogue_tiles<EPIM_Q8_FAST>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       case EPIM_Q8_EXACT:
-        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
+        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       case EPIM_F16:
-        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
+        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       default:
-        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_tiles, total, warp, lane, relu_lut);
+        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (cs > 1) cluster_sync_all();  // no CTA leaves while cluster peers may still signal it
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc(tmem, (uint32_t)(2 * p.tmem_cols));
@@ -533,9 +559,23 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   } else {
     a.epi_mode = a.epi == EPI_F16 ? EPIM_F16 : EPIM_F32;
   }
-  const int64_t tiles = ceil_div(a.m_total, kBM) * a.n_tiles * groups;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, num_sms());
-  igemm_kernel<KIND><<<grid, kThreads, igemm_smem_bytes(a.n_rows), s>>>(a);
+  const int64_t m_tiles = ceil_div(a.m_total, kBM);
+  a.cluster = (m_tiles >= 2 && a.cluster != 1) ? 2 : 1;
+  const int64_t ctiles = ceil_div(m_tiles, a.cluster) * a.n_tiles * groups;
+  const int64_t nclusters = std::min<int64_t>(ctiles, num_sms() / a.cluster);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nclusters * a.cluster));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = igemm_smem_bytes(a.n_rows);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)a.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_kernel<KIND>, a));
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;

@@ -96,6 +96,7 @@ struct IgemmArgs {
   const uint8_t* b;
   int32_t n_rows, n_tiles, n_real, n_per_tile, ones_col, tmem_cols;
   int32_t groups;             // set by igemm_launch
+  int32_t cluster;            // CTAs sharing each B stage (1 or 2); 1 forces no cluster
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)
