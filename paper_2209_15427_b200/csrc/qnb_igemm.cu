@@ -42,7 +42,8 @@ __host__ __device__ inline int igemm_stages(int n_rows) {
   return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
 }
 __host__ __device__ inline size_t igemm_smem_bytes(int n_rows) {
-  return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16 + 256;
+  return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16 + 256 +
+         2 * 128 * 8;
 }
 
 struct TileCoord {
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
   uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
+  int64_t* rowoff = (int64_t*)(relu_lut + 256);  // [2][128] per-tile row base offsets (-1: invalid)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Cluster of `cs` CTAs sharing each B stage (multicast): cluster-tile ct covers the
@@ -284,24 +286,30 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     // i = 0..7, so the 8 lanes of a row fetch its 128 contiguous K bytes together.
     const int t = threadIdx.x;
     const int jc = lane & 7, rr = lane >> 3;
-    uint32_t it = 0;
-    for (int64_t ct = cid; ct < total; ct += ncl) {
+    uint32_t it = 0, par = 0;
+    for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
       const TileCoord c = tile_of(ct, m_groups, p.n_tiles);
       const int64_t mt = c.mt * cs + rank;
+      {  // one row decomposition per thread, shared through smem
+        const int64_t row = mt * kBM + t;
+        int64_t off = -1;
+        if (row < p.m_total) {
+          const int64_t img = row / pix_per_img;
+          const int32_t rem = (int32_t)(row - img * pix_per_img);
+          const int32_t oy = rem / p.ow, ox = rem - oy * p.ow;
+          off = img * p.a_img + (int64_t)oy * p.stride_h * p.a_row + (int64_t)ox * p.stride_w * p.a_pix +
+                (int64_t)c.g * p.a_group + p.a_origin;
+        }
+        rowoff[par * 128 + t] = off;
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
       const uint8_t* base[8];
       uint32_t valid = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int64_t row = mt * kBM + warp * 32 + rr + 4 * i;
-        base[i] = p.a;
-        if (row < p.m_total) {
-          const int64_t img = row / pix_per_img;
-          const int64_t rem = row - img * pix_per_img;
-          const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-          base[i] = p.a + img * p.a_img + oy * p.stride_h * p.a_row + ox * p.stride_w * p.a_pix +
-                    (int64_t)c.g * p.a_group + p.a_origin;
-          valid |= 1u << i;
-        }
+        const int64_t off = rowoff[par * 128 + warp * 32 + rr + 4 * i];
+        base[i] = p.a + (off < 0 ? 0 : off);
+        valid |= (off >= 0 ? 1u : 0u) << i;
       }
       const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
       for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
