@@ -126,7 +126,9 @@ ActLayout choose_input_layout(const IgemmGeometry& g, int dtype, int64_t n, int6
     ActLayout R = L;
     R.c_phys = cp;
     while (R.row() % 16 != 0) ++R.wx;
-    if ((g.sw * R.pix()) % 16 == 0 && R.interior_offset() % 16 == 0) return R;
+    // window origins (a_origin + oy*sh*row + ox*sw*pix, a_origin = 0 as halo == pad)
+    // must be 16-byte aligned for the 16-byte run chunks
+    if ((g.sw * R.pix()) % 16 == 0) return R;
   }
   L.c_phys = round_up(c * es, 16) / es;
   return L;

@@ -128,7 +128,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
   const float slope = p.slope;
   uint32_t j = 0;
   for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
-    const TileCoord c = tile_of(ct, m_groups, n_tiles);
+    const TileCoord c0 = tile_of(ct, m_groups, n_tiles * p.ksplit);
+    const int ks = c0.nt % p.ksplit;
+    TileCoord c = c0;
+    c.nt = c0.nt / p.ksplit;
     const int64_t mt = c.mt * cs + rank;
     const uint32_t buf = j & 1;
     mbar_wait(&acc_full[buf], (j >> 1) & 1);
@@ -142,6 +145,22 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       const int64_t rem = row - img * pix_per_img;
       const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
       obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+    }
+    if constexpr (MODE == EPIM_RAW32) {
+      int32_t* wrow = p.ws + (((int64_t)ks * p.m_total + row) * n_tiles + c.nt) * p.n_rows;
+      for (int cb = half * 16; cb < p.n_rows; cb += 32) {
+        uint32_t r[16];
+        tmem_ld16(trow + (uint32_t)cb, r);
+        tmem_ld_wait();
+        if (!ok) continue;
+        uint4* w4 = reinterpret_cast<uint4*>(wrow + cb);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) w4[qd] = make_uint4(r[4 * qd], r[4 * qd + 1], r[4 * qd + 2], r[4 * qd + 3]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      continue;
     }
     int64_t rowsum = 0;
     if (ones_col >= 0) {
@@ -256,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   const int64_t cid = blockIdx.x / cs, ncl = gridDim.x / cs;
   const int64_t m_tiles = (p.m_total + kBM - 1) / kBM;
   const int64_t m_groups = (m_tiles + cs - 1) / cs;
-  const int64_t total = m_groups * p.n_tiles * p.groups;
+  const int64_t total = m_groups * p.n_tiles * p.ksplit * p.groups;
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
 
   if (threadIdx.x == 0) {
@@ -288,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     const int jc = lane & 7, rr = lane >> 3;
     uint32_t it = 0, par = 0;
     for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
-      const TileCoord c = tile_of(ct, m_groups, p.n_tiles);
+      const TileCoord c = tile_of(ct, m_groups, p.n_tiles * p.ksplit);
       const int64_t mt = c.mt * cs + rank;
       {  // one row decomposition per thread, shared through smem
         const int64_t row = mt * kBM + t;
@@ -311,8 +330,10 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         base[i] = p.a + (off < 0 ? 0 : off);
         valid |= (off >= 0 ? 1u : 0u) << i;
       }
-      const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
-      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+      const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
+      const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + ntile) * p.num_kb * b_stage;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const int s = (int)(it % S);
         mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
         if (t == 0) {
@@ -343,14 +364,16 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
-        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const int ks = (int)((ct / m_groups) % (p.n_tiles * p.ksplit)) % p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = (int)(it % S);
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
           const uint64_t ad = smem_desc_sw128(sA + (size_t)s * kStageA);
           const uint64_t bd = smem_desc_sw128(sB + (size_t)s * b_stage);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) umma<KIND>(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) umma<KIND>(dt, ad + 2 * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
           if (cs == 1)
             tc_commit(&empty[s]);
           else
@@ -374,6 +397,9 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         break;
       case EPIM_F16:
         epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+        break;
+      case EPIM_RAW32:
+        epilogue_tiles<EPIM_RAW32>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       default:
         epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
@@ -538,6 +564,42 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
   return QNB_OK;
 }
 
+// Split-K finalize: sums the ks partial accumulators of each (row, channel) in
+// integer arithmetic (exact, order-free) and applies the INT8 epilogue.
+__global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
+  const int64_t n_out = (int64_t)p.groups * p.n_real;  // groups == 1 for the FC layers this serves
+  const int64_t total = p.m_total * n_out;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / n_out;
+    const int o = (int)(i - row * n_out);
+    const int nt = o / p.n_per_tile, j = o - nt * p.n_per_tile;
+    int64_t dot = 0, rs = 0;
+    for (int ks = 0; ks < p.ksplit; ++ks) {
+      const int32_t* w = p.ws + (((int64_t)ks * p.m_total + row) * p.n_tiles + nt) * p.n_rows;
+      dot += w[j];
+      rs += w[p.ones_col];
+    }
+    const int64_t pix_per_img = (int64_t)p.oh * p.ow;
+    const int64_t img = row / pix_per_img;
+    const int64_t rem = row - img * pix_per_img;
+    const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
+    uint8_t* dst = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+    int64_t q = requant_clamp(dot + p.chan_const[o] - p.zw * rs, p.rq);
+    if (p.has_relu) q = p.relu_lut ? (int64_t)p.relu_lut[q] : relu_requant(q, p.relu);
+    dst[o] = (uint8_t)q;
+  }
+}
+
+qnb_status igemm_finalize(const IgemmArgs& a, cudaStream_t s) {
+  const int64_t total = a.m_total * a.n_real;
+  int64_t blocks = ceil_div(total, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  igemm_finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -560,7 +622,11 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   }
   IgemmArgs a = a0;
   a.groups = (int32_t)groups;
-  if (a.epi == EPI_Q8) {
+  if (a.ksplit < 1) a.ksplit = 1;
+  if (a.ksplit == 1) a.kb_per_split = a.num_kb;
+  if (a.ksplit > 1) {
+    a.epi_mode = EPIM_RAW32;
+  } else if (a.epi == EPI_Q8) {
     const bool fast = a.fast_rq && a.chan_const32 != nullptr;
     a.epi_mode = fast ? (a.has_relu ? ((a.relu.acc32 && a.relu_lut) ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
                       : EPIM_Q8_EXACT;
@@ -569,7 +635,7 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   }
   const int64_t m_tiles = ceil_div(a.m_total, kBM);
   a.cluster = (m_tiles >= 2 && a.cluster != 1) ? 2 : 1;
-  const int64_t ctiles = ceil_div(m_tiles, a.cluster) * a.n_tiles * groups;
+  const int64_t ctiles = ceil_div(m_tiles, a.cluster) * a.n_tiles * a.ksplit * groups;
   const int64_t nclusters = std::min<int64_t>(ctiles, num_sms() / a.cluster);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nclusters * a.cluster));

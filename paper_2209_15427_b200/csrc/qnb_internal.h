@@ -68,7 +68,8 @@ struct ActLayout {
 // ------------------------------------------------- implicit GEMM (tcgen05)
 enum EpiKind : int { EPI_Q8 = 0, EPI_F16 = 1, EPI_F32 = 2 };
 // Epilogue specialisation chosen on the host (igemm_launch).
-enum EpiMode : int { EPIM_Q8_FAST_RELU = 0, EPIM_Q8_FAST = 1, EPIM_Q8_EXACT = 2, EPIM_F16 = 3, EPIM_F32 = 4 };
+enum EpiMode : int { EPIM_Q8_FAST_RELU = 0, EPIM_Q8_FAST = 1, EPIM_Q8_EXACT = 2, EPIM_F16 = 3, EPIM_F32 = 4,
+                     EPIM_RAW32 = 5 };
 
 // Device copies of the reference's RequantParams, pre-digested:
 // s = shift_bits + shift (src/quantizer.cpp:202).
@@ -97,6 +98,11 @@ struct IgemmArgs {
   int32_t n_rows, n_tiles, n_real, n_per_tile, ones_col, tmem_cols;
   int32_t groups;             // set by igemm_launch
   int32_t cluster;            // CTAs sharing each B stage (1 or 2); 1 forces no cluster
+  // split-K: ksplit > 1 partitions the K stages; each split writes raw s32 accumulators
+  // (all n_rows columns, incl. the ones column) to ws[ks][row][n_tile][n_rows] and
+  // igemm_finalize applies the epilogue.
+  int32_t ksplit, kb_per_split;
+  int32_t* ws;
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)
@@ -151,5 +157,7 @@ qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked
 qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, IgemmPacked* pk);
 // Launches the tcgen05 kernel.
 qnb_status igemm_launch(int kind, const IgemmArgs& a, int64_t groups, cudaStream_t s);
+// Split-K reduction + INT8 epilogue (same arithmetic as the fused epilogue).
+qnb_status igemm_finalize(const IgemmArgs& a, cudaStream_t s);
 
 }  // namespace qnb

@@ -21,6 +21,7 @@
 // Execution: the step list is captured once into a CUDA graph and replayed.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -129,6 +130,7 @@ struct qnb_plan {
   const void* g_in = nullptr;
   void* g_out = nullptr;
   int64_t g_batch = -1;
+  int64_t launches_per_forward = 0;
   cudaStream_t capture_stream = nullptr;
   int device = 0;
 };
@@ -502,7 +504,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   if (quant && !in.has_qv) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
   IgemmPacked pk;
   QNB_TRY(igemm_plan_k(g, Lin, &pk));
-  if (g.is_fc) pk.n_per_tile = 128;
+  if (g.is_fc && !quant) pk.n_per_tile = 128;
   QNB_TRY(igemm_pack_b(g, l.weight, l.weight_dtype, &pk));
   IgemmArgs& a = st.ig;
   std::memset(&a, 0, sizeof(a));
@@ -574,6 +576,22 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     if (op.relu >= 0) {
       a.has_relu = 1;
       a.slope = P.layers[op.relu].negative_slope;
+    }
+  }
+  // Inner products at small batch have few (m, n) tiles: split K so every SM streams
+  // a share of the weights; partial s32 sums are reduced exactly by igemm_finalize.
+  if (g.is_fc && quant) {
+    const int64_t m_tiles = ceil_div(P.max_batch, 128);
+    const int64_t ctiles = ceil_div(m_tiles, 2) * pk.n_tiles;
+    int64_t ks = (74 + ctiles - 1) / ctiles;
+    ks = std::max<int64_t>(1, std::min<int64_t>(ks, pk.num_kb / 2));
+    if (ks > 1) {
+      a.ksplit = (int32_t)ks;
+      a.kb_per_split = (int32_t)ceil_div(pk.num_kb, ks);
+      a.ksplit = (int32_t)ceil_div(pk.num_kb, a.kb_per_split);
+      void* ws = nullptr;
+      QNB_TRY(dev_alloc(P, &ws, (size_t)a.ksplit * P.max_batch * pk.n_tiles * pk.n_rows * 4));
+      a.ws = (int32_t*)ws;
     }
   }
   a.out = blob_ptr(P, op.out);
@@ -769,6 +787,10 @@ qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cuda
         case OP_IGEMM:
           QNB_TRY(igemm_launch(st.mma_kind, st.ig, st.groups, s));
           g_launches.fetch_sub(1);  // counted below with the others
+          if (st.ig.ksplit > 1) {
+            QNB_TRY(igemm_finalize(st.ig, s));
+            g_launches.fetch_sub(1);
+          }
           break;
         case OP_POOL:
           launch_pool(st.pool, s);
@@ -847,6 +869,9 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
     QNB_TRY(fill_buffer(P->arena + bl.off, bl.L.bytes() + 1024, bl.dtype, bl.has_qv ? bl.qv.zero : 0, 0));
   }
   QNB_TRY(emit(*P));
+  P->launches_per_forward = (int64_t)P->steps.size();
+  for (const Step& st : P->steps)
+    if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1) ++P->launches_per_forward;
   QNB_CUDA(cudaDeviceSynchronize());
   // output description (reference layout)
   const Blob& sk = P->blobs[P->sink_blob];
@@ -903,7 +928,7 @@ qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32
   } else {
     QNB_TRY(launch_steps(*P, batch, in_dev, out_dev, s));
   }
-  count_launch((uint64_t)P->steps.size());
+  count_launch((uint64_t)P->launches_per_forward);
   if (output_on_host)
     QNB_CUDA(cudaMemcpyAsync(output, out_dev, (size_t)(P->out_bytes_per_sample * batch), cudaMemcpyDeviceToHost, s));
   return QNB_OK;
@@ -931,7 +956,7 @@ qnb_status qnb_plan_blob_info(const qnb_plan* P, int32_t blob, void** dev_ptr, i
 
 qnb_status qnb_plan_stats(const qnb_plan* P, int64_t* kernels, int64_t* arena, int64_t* weights) {
   if (!P) return fail(QNB_E_ARG, "null plan");
-  if (kernels) *kernels = (int64_t)P->steps.size();
+  if (kernels) *kernels = (int64_t)P->steps.size();  // steps (a split-K GEMM step launches 2 kernels)
   if (arena) *arena = (int64_t)P->arena_bytes;
   if (weights) *weights = (int64_t)P->weight_bytes;
   return QNB_OK;

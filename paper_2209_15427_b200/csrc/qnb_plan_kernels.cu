@@ -578,28 +578,47 @@ __global__ void softmax_rows_kernel(const uint8_t* __restrict__ src, DevLayout S
                                     float* __restrict__ out, int64_t F) {
   extern __shared__ double ex[];
   float* xv = reinterpret_cast<float*>(ex + F);
+  __shared__ float wmax[32];
   __shared__ float smax;
   __shared__ double ssum;
   const int64_t n = blockIdx.x;
   const uint8_t* row = at(src, S, n, 0, 0);
-  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) xv[f] = load_as_float(row + f * S.es, in_dtype, q);
+  float m = -INFINITY;
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
+    const float v = load_as_float(row + f * S.es, in_dtype, q);
+    xv[f] = v;
+    m = fmaxf(m, v);  // NaN-ignoring; std::max order semantics restored below
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float m = xv[0];
-    for (int64_t f = 1; f < F; ++f) m = m < xv[f] ? xv[f] : m;
-    smax = m;
+    float mm = wmax[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, wmax[w]);
+    // float maxv = x[0]; maxv = std::max(maxv, x[f]): NaN only if x[0] is NaN
+    smax = isnan(xv[0]) ? xv[0] : mm;
   }
   __syncthreads();
-  const double m = smax;
-  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) ex[f] = exp(__dsub_rn((double)xv[f], m));
+  const double md = smax;
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) ex[f] = exp(__dsub_rn((double)xv[f], md));
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // the reference's sequential double sum, loads batched for ILP
     double s = 0.0;
-    for (int64_t f = 0; f < F; ++f) s = __dadd_rn(s, ex[f]);
+    int64_t f = 0;
+    for (; f + 8 <= F; f += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ex[f + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+    }
+    for (; f < F; ++f) s = __dadd_rn(s, ex[f]);
     ssum = s;
   }
   __syncthreads();
-  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) out[n * F + f] = __double2float_rn(__ddiv_rn(ex[f], ssum));
+  const double sum = ssum;
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) out[n * F + f] = __double2float_rn(__ddiv_rn(ex[f], sum));
 }
 
 // ------------------------------------------------------------------ unpack

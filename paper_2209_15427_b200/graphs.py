@@ -73,9 +73,10 @@ def alexnet(batch: int = 1) -> dict:
     return {"name": "alexnet", "layers": L}
 
 
-def vgg16(batch: int = 1) -> dict:
-    """VGG-16 (configuration D), 3x224x224 input."""
-    L = [_input("data", [batch, 3, 224, 224])]
+def vgg16(batch: int = 1, res: int = 224) -> dict:
+    """VGG-16 (configuration D), 3 x res x res input (224 for the benchmark; the
+    parity tests use res=32, which keeps every layer kind and shape rule)."""
+    L = [_input("data", [batch, 3, res, res])]
     cur = "data"
     cfg = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
     blk, idx = 1, 1
@@ -177,7 +178,8 @@ def alexnet_moe(batch: int = 1, dtype: str = "int8", n_experts: int = 16, top_k:
     return {"name": "alexnet_moe", "layers": L}
 
 
-MODELS = {"alexnet": alexnet, "vgg16": vgg16, "lenet5": lenet5}
+MODELS = {"alexnet": alexnet, "vgg16": vgg16, "lenet5": lenet5,
+          "vgg16_32": lambda batch=1: vgg16(batch, res=32)}
 
 
 def to_json(g: dict) -> str:

@@ -1,0 +1,93 @@
+"""FP16 / FP32 AlexNet plans against the reference Net (tolerance: max-abs error
+<= 1e-2 x the reference's output range, BASELINE.json north_star), plus VGG-16 and
+LeNet-5 INT8 plans (bit-exact) at small resolution."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ffi
+from paper_2209_15427_b200 import graph as G
+from paper_2209_15427_b200 import graphs
+from paper_2209_15427_b200.net import QUANTIZED, Net
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+DT = {"fp32": 0, "fp16": 1, "int8": 2, "int16": 3}
+
+
+def ref_net(ref, g, precision, params, ranges=None):
+    net = ref.net(json.dumps(g), DT[precision] if precision != "fp32" else -1)
+    for k, v in params.items():
+        net.set_param(k, v)
+    if ranges:
+        for k, (lo, hi) in ranges.items():
+            net.set_range(k, lo, hi)
+        net.finalize()
+        net.set_mode(3)
+    return net
+
+
+def our_net(g, precision, params, ranges=None):
+    net = Net(G.override_precision(g, precision) if precision != "fp32" else g)
+    for k, v in params.items():
+        net.set_param(k, v)
+    if ranges:
+        for k, (lo, hi) in ranges.items():
+            net.set_range(k, lo, hi)
+        net.finalize_quantizers()
+        net.set_quant_mode(QUANTIZED)
+    return net
+
+
+def f32(arr, dt):
+    return ffi.Restatement().cast_float(arr, 1, 0) if dt == 1 else arr.astype(np.float32)
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not ffi.have_reference():
+        pytest.skip("needs oracle/_ref")
+    return ffi.Reference()
+
+
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_alexnet_float_within_tolerance(ref, precision):
+    g = graphs.alexnet(1)
+    shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
+    params = graphs.synth_params(g, shapes)
+    x = graphs.synth_images(2, (3, 227, 227), offset=7)
+    ours = our_net(g, precision, params).forward({"data": x})["prob"]
+    names = [l["name"] for l in g["layers"]]
+    prefix = {"name": "p", "layers": g["layers"][: names.index("fc8") + 1]}
+    pr = {k: v for k, v in params.items() if k.split(".")[0] in names[: names.index("fc8") + 1]}
+    ours_fc8 = our_net(prefix, precision, pr).forward({"data": x})["fc8"]
+    (fc8, dt, _), = ref_net(ref, prefix, precision, pr).forward("data", x).values()
+    a, b = f32(ours_fc8, dt), f32(fc8, dt)
+    rng = float(b.max() - b.min())
+    assert np.abs(a - b).max() <= 1e-2 * rng, (np.abs(a - b).max(), rng)
+    (prob, dt, _), = ref_net(ref, g, precision, params).forward("data", x).values()
+    a, b = f32(ours, dt), f32(prob, dt)
+    rng = float(b.max() - b.min())
+    assert np.abs(a - b).max() <= 1e-2 * rng, (np.abs(a - b).max(), rng)
+
+
+@pytest.mark.parametrize("model", ["vgg16_32", "lenet5"])
+def test_small_int8_nets_bit_exact(ref, model):
+    g = graphs.vgg16(1, res=32) if model == "vgg16_32" else graphs.lenet5(1)
+    with open(os.path.join(HERE, "golden", f"{model}_int8_calib.json")) as f:
+        ranges = json.load(f)["ranges"]
+    shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
+    params = graphs.synth_params(g, shapes)
+    inp = G.input_name(g)
+    x = graphs.synth_images(3, shapes[inp][1:], offset=11)
+    ours = our_net(g, "int8", params, ranges).forward({inp: x})
+    theirs = ref_net(ref, g, "int8", params, ranges).forward(inp, x)
+    (name, out), = ours.items()
+    arr, dt, _ = theirs[name]
+    if dt == 0:
+        d = np.abs(out.view(np.int32).astype(np.int64) - arr.view(np.int32).astype(np.int64))
+        assert d.max() <= 1
+    else:
+        assert np.array_equal(out, arr)
