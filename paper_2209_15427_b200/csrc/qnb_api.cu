@@ -3,6 +3,7 @@
 #include <cuda_fp16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -189,7 +190,10 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   QNB_TRY(d2h(wh.data(), w_dev, wh.size(), s));
   IgemmPacked pk;
   QNB_TRY(igemm_plan_k(g, io.in, &pk));
-  if (g.is_fc) pk.n_per_tile = 64;
+  if (g.is_fc) {
+    pk.n_per_tile = 64;
+    if (const char* e = getenv("QNB_IP_NPT")) pk.n_per_tile = atoi(e);  // test hook
+  }
   QNB_TRY(igemm_pack_b(g, wh.data(), w_dtype, &pk));
 
   IgemmArgs a;
@@ -264,6 +268,18 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     a.bias = bias_dev;
     a.epi = dtype == QNB_FP16 ? EPI_F16 : EPI_F32;
   }
+  if (g.is_fc && quant) {
+    if (const char* e = getenv("QNB_IP_KSPLIT")) {  // test hook: force split-K
+      const int ks = atoi(e);
+      if (ks > 1) {
+        a.kb_per_split = (int32_t)ceil_div(pk.num_kb, ks);
+        a.ksplit = (int32_t)ceil_div(pk.num_kb, a.kb_per_split);
+        int32_t* ws = nullptr;
+        QNB_TRY(tmp.alloc((void**)&ws, (size_t)a.ksplit * a.m_total * pk.n_tiles * pk.n_rows * 4));
+        a.ws = ws;
+      }
+    }
+  }
   a.o_es = (int32_t)out_layout.es();
   uint8_t* yout = (uint8_t*)y;
   if (unpack_nchw) QNB_TRY(tmp.alloc((void**)&yout, (size_t)out_layout.bytes() + 256));
@@ -275,6 +291,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   a.o_vec = (out_layout.pix() % 16 == 0 && (g.og * a.o_es) % 16 == 0 && (pk.n_per_tile * a.o_es) % 16 == 0) ? 1 : 0;
   const int kind = g.kind;
   QNB_TRY(igemm_launch(kind, a, g.groups, s));
+  if (a.ksplit > 1) QNB_TRY(igemm_finalize(a, s));
   if (unpack_nchw) QNB_TRY(launch_nhwc_to_nchw(yout, dtype, out_layout, y, s));
   // Temporaries are released stream-ordered; host vectors must outlive the async copies.
   QNB_CUDA(cudaStreamSynchronize(s));

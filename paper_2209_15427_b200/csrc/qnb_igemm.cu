@@ -567,7 +567,7 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
 // Split-K finalize: sums the ks partial accumulators of each (row, channel) in
 // integer arithmetic (exact, order-free) and applies the INT8 epilogue.
 __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
-  const int64_t n_out = (int64_t)p.groups * p.n_real;  // groups == 1 for the FC layers this serves
+  const int64_t n_out = p.n_real;  // split-K serves the inner products (one group)
   const int64_t total = p.m_total * n_out;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / n_out;

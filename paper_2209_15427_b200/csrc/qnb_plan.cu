@@ -581,10 +581,13 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   // Inner products at small batch have few (m, n) tiles: split K so every SM streams
   // a share of the weights; partial s32 sums are reduced exactly by igemm_finalize.
   if (g.is_fc && quant) {
+    // every CTA streams its own weight slice (no cluster): the m-tiles of one slice hit
+    // in L2, so HBM sees the weights once and all 148 SMs pull in parallel
     const int64_t m_tiles = ceil_div(P.max_batch, 128);
-    const int64_t ctiles = ceil_div(m_tiles, 2) * pk.n_tiles;
-    int64_t ks = (74 + ctiles - 1) / ctiles;
+    const int64_t tiles = m_tiles * pk.n_tiles;
+    int64_t ks = 148 / std::max<int64_t>(tiles, 1);
     ks = std::max<int64_t>(1, std::min<int64_t>(ks, pk.num_kb / 2));
+    a.cluster = 1;
     if (ks > 1) {
       a.ksplit = (int32_t)ks;
       a.kb_per_split = (int32_t)ceil_div(pk.num_kb, ks);

@@ -235,3 +235,23 @@ def test_moe_combine_bit_exact():
     idx = np.stack([rng.permutation(E)[:K] for _ in range(B)]).astype(np.int64)
     w = rng.dirichlet(np.ones(K), B).astype(np.float32)
     assert_bits_equal(ops.moe_combine(eo, idx, w), Restatement().moe_combine(eo, idx, w), "combine")
+
+
+@pytest.mark.parametrize("npt,ks", [(64, 1), (240, 1), (64, 4), (240, 4), (240, 5)])
+def test_inner_product_tiling_and_split_k(oracle_impl, npt, ks, monkeypatch):
+    """Wide B tiles (N=256 with the ones row) and split-K (exact s32 partials +
+    finalize) must stay bit-exact."""
+    monkeypatch.setenv("QNB_IP_NPT", str(npt))
+    monkeypatch.setenv("QNB_IP_KSPLIT", str(ks))
+    N, K, O = 200, 4096, 1000
+    rng = np.random.default_rng(500 + npt + ks)
+    xf = rng.uniform(0, 3, (N, K)).astype(np.float32)
+    wf = rng.uniform(-0.05, 0.05, (K, O)).astype(np.float32)
+    bias = rng.uniform(-0.2, 0.2, O).astype(np.float32)
+    qx, qw = qv_of(oracle_impl, 0, 3), qv_of(oracle_impl, -0.05, 0.05)
+    span = 0.1 * np.sqrt(K)
+    qo = qv_of(oracle_impl, -span, span)
+    x, w = oracle_impl.quantize(xf, qx, INT8Q), oracle_impl.quantize(wf, qw, INT8Q)
+    ours = ops.inner_product(x, INT8Q, w, INT8Q, bias, O, qx, qw, qo)
+    theirs = oracle_impl.inner_product(x, INT8Q, w, INT8Q, bias, O, qx, qw, qo)
+    assert_bits_equal(ours, theirs, f"ip npt={npt} ks={ks}")
