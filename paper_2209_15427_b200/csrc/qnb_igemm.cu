@@ -33,6 +33,7 @@ namespace qnb {
 constexpr int kBM = 128;
 constexpr int kStageA = kBM * 128;
 constexpr int kMaxStages = 8;
+constexpr int kMaxChunkSmem = 2048;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (5 + kEpiWarps) * 32;  // 4 producer warps, 1 MMA warp, 8 epilogue warps
 
@@ -43,7 +44,7 @@ __host__ __device__ inline int igemm_stages(int n_rows) {
 }
 __host__ __device__ inline size_t igemm_smem_bytes(int n_rows) {
   return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16 + 256 +
-         2 * 128 * 8;
+         2 * 128 * 8 + kMaxChunkSmem * 4;
 }
 
 struct TileCoord {
@@ -265,6 +266,12 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
   uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
   int64_t* rowoff = (int64_t*)(relu_lut + 256);  // [2][128] per-tile row base offsets (-1: invalid)
+  int32_t* chunk_s = (int32_t*)(rowoff + 256);    // chunk table copy (kMaxChunkSmem entries)
+  const int n_chunks = p.num_kb * 8;
+  const bool chunks_in_smem = n_chunks <= kMaxChunkSmem;
+  if (chunks_in_smem)
+    for (int i = threadIdx.x; i < n_chunks; i += blockDim.x) chunk_s[i] = __ldg(p.chunk_off + i);
+  const int32_t* chunk_tab = chunks_in_smem ? chunk_s : p.chunk_off;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Cluster of `cs` CTAs sharing each B stage (multicast): cluster-tile ct covers the
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
             bulk_g2s_multicast(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s],
                                cmask);
         }
-        const int32_t off = __ldg(p.chunk_off + kb * 8 + jc);
+        const int32_t off = chunk_tab[kb * 8 + jc];
         uint8_t* dst = sA + (size_t)s * kStageA;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -565,36 +572,70 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
 }
 
 // Split-K finalize: sums the ks partial accumulators of each (row, channel) in
-// integer arithmetic (exact, order-free) and applies the INT8 epilogue.
+// integer arithmetic (exact, order-free) and applies the INT8 epilogue.  A thread
+// owns 4 consecutive channels of one row (16-byte partial loads, one 32-bit store).
+template <bool FAST>
 __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
-  const int64_t n_out = p.n_real;  // split-K serves the inner products (one group)
-  const int64_t total = p.m_total * n_out;
+  const int n_out = p.n_real;  // split-K serves the inner products (one group)
+  const int quads = (n_out + 3) >> 2;
+  const int64_t total = p.m_total * quads;
+  Q8Consts k;
+  k.mult = p.rq.mult;
+  k.s = p.rq.s;
+  k.half = FAST ? (1LL << (p.rq.s - 1)) : 0;
+  k.mask = (k.half << 1) - 1;
+  k.oz = (int32_t)p.rq.out_zero;
+  k.omin = (int32_t)p.rq.out_min;
+  k.omax = (int32_t)p.rq.out_max;
+  const int64_t row_stride = (int64_t)p.n_tiles * p.n_rows;
+  const int64_t split_stride = p.m_total * row_stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / n_out;
-    const int o = (int)(i - row * n_out);
-    const int nt = o / p.n_per_tile, j = o - nt * p.n_per_tile;
-    int64_t dot = 0, rs = 0;
+    const int64_t row = i / quads;
+    const int o0 = (int)(i - row * quads) * 4;
+    const int nt = o0 / p.n_per_tile, j = o0 - nt * p.n_per_tile;
+    const int32_t* w = p.ws + row * row_stride + (int64_t)nt * p.n_rows;
+    int32_t d[4] = {0, 0, 0, 0};
+    int32_t rs = 0;
     for (int ks = 0; ks < p.ksplit; ++ks) {
-      const int32_t* w = p.ws + (((int64_t)ks * p.m_total + row) * p.n_tiles + nt) * p.n_rows;
-      dot += w[j];
-      rs += w[p.ones_col];
+      const int32_t* ws = w + ks * split_stride;
+      const int4 v = *reinterpret_cast<const int4*>(ws + j);  // n_per_tile % 16 == 0
+      d[0] += v.x;
+      d[1] += v.y;
+      d[2] += v.z;
+      d[3] += v.w;
+      rs += ws[p.ones_col];
     }
-    const int64_t pix_per_img = (int64_t)p.oh * p.ow;
-    const int64_t img = row / pix_per_img;
-    const int64_t rem = row - img * pix_per_img;
-    const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-    uint8_t* dst = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
-    int64_t q = requant_clamp(dot + p.chan_const[o] - p.zw * rs, p.rq);
-    if (p.has_relu) q = p.relu_lut ? (int64_t)p.relu_lut[q] : relu_requant(q, p.relu);
-    dst[o] = (uint8_t)q;
+    uint8_t* dst = p.out + row * p.o_img + p.o_origin + o0;  // inner product: oh = ow = 1
+    uint32_t packed = 0;
+    const int cnt = min(4, n_out - o0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u >= cnt) break;
+      int64_t q;
+      if constexpr (FAST) {
+        q = q8_fast<false>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, nullptr);
+      } else {
+        q = requant_clamp((int64_t)d[u] + p.chan_const[o0 + u] - p.zw * (int64_t)rs, p.rq);
+      }
+      if (p.has_relu) q = p.relu_lut ? (int64_t)p.relu_lut[q] : relu_requant(q, p.relu);
+      packed |= ((uint32_t)q & 0xFFu) << (8 * u);
+    }
+    if (cnt == 4 && ((uintptr_t)dst & 3) == 0) {
+      *reinterpret_cast<uint32_t*>(dst) = packed;
+    } else {
+      for (int u = 0; u < cnt; ++u) dst[u] = (uint8_t)(packed >> (8 * u));
+    }
   }
 }
 
 qnb_status igemm_finalize(const IgemmArgs& a, cudaStream_t s) {
-  const int64_t total = a.m_total * a.n_real;
+  const int64_t total = a.m_total * ceil_div(a.n_real, 4);
   int64_t blocks = ceil_div(total, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  igemm_finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+  if (a.fast_rq && a.chan_const32)
+    igemm_finalize_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a);
+  else
+    igemm_finalize_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a);
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;

@@ -163,46 +163,43 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
   }
 }
 
-// FP32 NCHW with <= 4 channels -> u8 NHWC4 (AlexNet/VGG RGB input).  A thread owns
-// 4 consecutive pixels of a row: 4 x C independent loads in flight, one 16-byte store
-// of the 4 packed pixels; 64 threads cover a 256-pixel row, a block 4 rows.
-constexpr int kPackPix = 4;
+// FP32 NCHW with <= 4 channels -> u8 NHWC4 (AlexNet/VGG RGB input).  64 threads
+// cover one image row (pixels l, l+64, l+128, ...), so every load and store
+// instruction of a warp is a contiguous 128-byte (load) / 128-byte (store) access,
+// with 4 x C independent loads in flight per thread; a block covers 4 rows.
+constexpr int kPackLanes = 64;
 __global__ void __launch_bounds__(256) pack_rgb_u8_kernel(const float* __restrict__ src, int C, int H, int W,
                                                           uint8_t* __restrict__ dst, DevLayout L, DevQ q,
                                                           uint32_t fill, int vec_store) {
-  const int tpr = (W + kPackPix - 1) / kPackPix;  // threads per row
-  const int rows_per_block = 256 / tpr;
-  const int t = threadIdx.x;
-  const int ry = t / tpr, x0 = (t - ry * tpr) * kPackPix;
-  const int y = blockIdx.x * rows_per_block + ry;
-  if (ry >= rows_per_block || y >= H) return;
+  (void)vec_store;
+  const int ry = threadIdx.x / kPackLanes, l = threadIdx.x % kPackLanes;
+  const int y = blockIdx.x * (256 / kPackLanes) + ry;
+  if (y >= H) return;
   const int64_t n = blockIdx.y;
   const int64_t plane = (int64_t)H * W;
-  const float* px = src + n * C * plane + (int64_t)y * W + x0;
+  const float* rowp = src + n * C * plane + (int64_t)y * W;
+  uint32_t* orow = reinterpret_cast<uint32_t*>(at(dst, L, n, y, 0));
   const float invf = (float)q.inv;
-  float v[4][kPackPix];
+  for (int xb = 0; xb < W; xb += 4 * kPackLanes) {
+    float v[4][4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
+    for (int i = 0; i < 4; ++i) {
+      const int x = xb + l + kPackLanes * i;
 #pragma unroll
-    for (int i = 0; i < kPackPix; ++i) v[c][i] = (c < C && x0 + i < W) ? __ldg(px + c * plane + i) : 0.0f;
-  uint32_t w[kPackPix];
-#pragma unroll
-  for (int i = 0; i < kPackPix; ++i) {
-    uint32_t word = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const uint32_t b = c < C ? (uint32_t)qz_fast(v[c][i], q, invf) : fill;
-      word |= (b & 0xFFu) << (8 * c);
+      for (int c = 0; c < 4; ++c) v[i][c] = (c < C && x < W) ? __ldg(rowp + c * plane + x) : 0.0f;
     }
-    w[i] = word;
-  }
-  uint8_t* o = at(dst, L, n, y, x0);
-  if (vec_store && x0 + kPackPix <= W) {
-    *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
-  } else {
 #pragma unroll
-    for (int i = 0; i < kPackPix; ++i)
-      if (x0 + i < W) reinterpret_cast<uint32_t*>(o)[i] = w[i];
+    for (int i = 0; i < 4; ++i) {
+      const int x = xb + l + kPackLanes * i;
+      if (x >= W) continue;
+      uint32_t word = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t b = c < C ? (uint32_t)qz_fast(v[i][c], q, invf) : fill;
+        word |= (b & 0xFFu) << (8 * c);
+      }
+      orow[x] = word;
+    }
   }
 }
 
@@ -642,13 +639,10 @@ static unsigned blocks_for(int64_t n, int threads) {
 
 void launch_pack_input(const PackArgs& p, cudaStream_t s) {
   if (p.src_dtype == QNB_FP32 && p.dst_dtype == QNB_INT8Q && p.op == PACK_QUANTIZE && p.L.c_phys == 4 &&
-      p.C <= 4 && p.W <= 1024 && p.L.pix % 4 == 0 && p.L.origin % 4 == 0 && p.L.row % 4 == 0 && p.L.img % 4 == 0) {
-    const int tpr = (int)ceil_div(p.W, kPackPix);
-    const int rpb = 256 / tpr;
-    const int vec = (p.L.origin % 16 == 0 && p.L.row % 16 == 0 && p.L.img % 16 == 0) ? 1 : 0;
-    dim3 grid((unsigned)ceil_div(p.H, rpb), (unsigned)p.N);
+      p.C <= 4 && p.L.pix == 4 && p.L.origin % 4 == 0 && p.L.row % 4 == 0 && p.L.img % 4 == 0) {
+    dim3 grid((unsigned)ceil_div(p.H, 256 / kPackLanes), (unsigned)p.N);
     pack_rgb_u8_kernel<<<grid, 256, 0, s>>>((const float*)p.src, (int)p.C, (int)p.H, (int)p.W, p.dst, p.L, p.q,
-                                            (uint32_t)(int64_t)p.fill, vec);
+                                            (uint32_t)(int64_t)p.fill, 1);
     return;
   }
   const int threads = p.W >= 256 ? 256 : (int)round_up(p.W, 32);
