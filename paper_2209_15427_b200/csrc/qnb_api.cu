@@ -245,7 +245,10 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     cc.resize((size_t)OC);
     for (int64_t oc = 0; oc < OC; ++oc) {
       int64_t wsum = 0;
-      for (int64_t k = 0; k < K; ++k) wsum += wh[(size_t)(g.is_fc ? k * OC + oc : oc * K + k)];
+      for (int64_t k = 0; k < K; ++k) {
+        const size_t wi = (size_t)(g.is_fc ? k * OC + oc : oc * K + k);
+        wsum += dtype == QNB_INT16Q ? (int64_t)reinterpret_cast<const uint16_t*>(wh.data())[wi] : (int64_t)wh[wi];
+      }
       int64_t c = K * zx * zw - zx * wsum;
       if (bias_dev) c += bias_to_acc(bias_h[(size_t)oc], qa.scale, qb.scale);
       cc[(size_t)oc] = c;
@@ -254,7 +257,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     QNB_TRY(tmp.alloc((void**)&d_cc, cc.size() * 8));
     QNB_CUDA(cudaMemcpyAsync(d_cc, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice, s));
     a.chan_const = d_cc;
-    a.fast_rq = igemm_fast_requant_ok(cc, K, zw, a.rq) ? 1 : 0;
+    a.fast_rq = (dtype == QNB_INT8Q && igemm_fast_requant_ok(cc, K, zw, a.rq)) ? 1 : 0;
     if (a.fast_rq) {
       std::vector<int32_t> cc32(cc.begin(), cc.end());
       int32_t* d32 = nullptr;
@@ -263,12 +266,12 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
       QNB_CUDA(cudaStreamSynchronize(s));
       a.chan_const32 = d32;
     }
-    a.epi = EPI_Q8;
+    a.epi = dtype == QNB_INT16Q ? EPI_Q16 : EPI_Q8;
   } else {
     a.bias = bias_dev;
     a.epi = dtype == QNB_FP16 ? EPI_F16 : EPI_F32;
   }
-  if (g.is_fc && quant) {
+  if (g.is_fc && dtype == QNB_INT8Q) {
     if (const char* e = getenv("QNB_IP_KSPLIT")) {  // test hook: force split-K
       const int ks = atoi(e);
       if (ks > 1) {
@@ -407,11 +410,11 @@ qnb_status qnb_conv_forward(const void* x, const int64_t xs[4], qnb_dtype dtype,
   }
   const bool quant = is_quant(dtype);
   if (quant && (!in_qv || !w_qv || !out_qv)) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
-  if (dtype == QNB_INT16Q) return fail(QNB_E_UNSUPPORTED, "INT16 conv not implemented on this backend yet");
   if (quant && w_dtype != dtype) return fail(QNB_E_DTYPE, "quantized conv weight dtype must match input");
   if (xs[0] == 0) return QNB_OK;
   IgemmGeometry g;
   g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
+  g.q16 = dtype == QNB_INT16Q;
   g.groups = cp->groups;
   g.cg = xs[1] / cp->groups;
   g.og = cp->out_channels / cp->groups;
@@ -452,11 +455,11 @@ qnb_status qnb_inner_product(const void* x, int64_t n, int64_t k, qnb_dtype dtyp
   const bool quant = is_quant(dtype);
   if (quant && (!in_qv || !w_qv || !out_qv))
     return fail(QNB_E_QVALS, "quantized inner product requires quantizer values");
-  if (dtype == QNB_INT16Q) return fail(QNB_E_UNSUPPORTED, "INT16 inner product not implemented on this backend yet");
   if (n == 0) return QNB_OK;
   IgemmGeometry g;
   std::memset(&g, 0, sizeof(g));
   g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
+  g.q16 = dtype == QNB_INT16Q;
   g.groups = 1;
   g.cg = k;
   g.og = out_features;

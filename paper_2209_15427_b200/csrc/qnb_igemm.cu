@@ -163,6 +163,40 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
       continue;
     }
+    if constexpr (MODE == EPIM_Q16) {
+      // dot = 65536*HH + 256*(HL + LH) + LL, rowsum = 256*sum(hi) + sum(lo)   (int64)
+      uint32_t o2[2];
+      tmem_ld1(trow + (uint32_t)ones_col, o2[0]);
+      tmem_ld1(trow + (uint32_t)ones_col + 1, o2[1]);
+      tmem_ld_wait();
+      const int64_t rs16 = 256 * (int64_t)(int32_t)o2[1] + (int64_t)(int32_t)o2[0];
+      const int n0q = c.nt * npt;
+      const int nh = min(npt, n_real - n0q);
+      const int chq = c.g * n_real + n0q;
+      for (int cb = half * 16; cb < nh; cb += 32) {
+        uint32_t ll[16], hl[16], lh[16], hh[16];
+        tmem_ld16(trow + (uint32_t)cb, ll);
+        tmem_ld16(trow + (uint32_t)(npt + cb), hl);
+        tmem_ld16(trow + (uint32_t)(2 * npt + cb), lh);
+        tmem_ld16(trow + (uint32_t)(3 * npt + cb), hh);
+        tmem_ld_wait();
+        if (!ok) continue;
+        uint16_t* dst = reinterpret_cast<uint16_t*>(obase + (int64_t)(chq + cb) * o_es);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (cb + i >= nh) continue;
+          const int64_t dot = 65536 * (int64_t)(int32_t)hh[i] +
+                              256 * ((int64_t)(int32_t)hl[i] + (int64_t)(int32_t)lh[i]) + (int64_t)(int32_t)ll[i];
+          int64_t q = requant_clamp(dot + __ldg(p.chan_const + chq + cb + i) - zw * rs16, p.rq);
+          if (has_relu) q = relu_requant(q, p.relu);
+          dst[i] = (uint16_t)q;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      continue;
+    }
     int64_t rowsum = 0;
     if (ones_col >= 0) {
       uint32_t v;
@@ -405,6 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
       case EPIM_F16:
         epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
+      case EPIM_Q16:
+        epilogue_tiles<EPIM_Q16>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+        break;
       case EPIM_RAW32:
         epilogue_tiles<EPIM_RAW32>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
@@ -441,6 +478,25 @@ bool igemm_fast_requant_ok(const std::vector<int64_t>& chan_const, int64_t K, in
 static int kind_es(int kind) { return kind == KIND_I8 ? 1 : (kind == KIND_F16 ? 2 : 4); }
 
 qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk) {
+  if (g.q16) {
+    // byte view: channel c8 = 2c + byte, then map the K index back to (k, byte)
+    IgemmGeometry g8 = g;
+    g8.q16 = false;
+    g8.cg = 2 * g.cg;
+    g8.fc_c = 2 * g.fc_c;
+    ActLayout in8 = in;
+    in8.dtype = QNB_INT8Q;
+    in8.c = 2 * in.c;
+    in8.c_phys = 2 * in.c_phys;
+    QNB_TRY(igemm_plan_k(g8, in8, pk));
+    const int64_t sp = g.is_fc ? g.fc_h * g.fc_w : g.kh * g.kw;
+    for (int64_t& km : pk->kmap) {
+      if (km < 0) continue;
+      const int64_t c8 = km / sp, rest = km % sp;
+      km = ((c8 / 2) * sp + rest) * 2 + (c8 & 1);
+    }
+    return QNB_OK;
+  }
   const int es = kind_es(g.kind);
   if (in.es() != es) return fail(QNB_E_DTYPE, "activation element size does not match MMA kind");
   std::vector<int32_t> off;
@@ -504,7 +560,56 @@ qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked
   return QNB_OK;
 }
 
+static qnb_status igemm_pack_b_q16(const IgemmGeometry& g, const void* w, IgemmPacked* pk) {
+  const int64_t og = g.og;
+  int64_t max_real = 48;  // 4 * 48 + 2 ones rows -> 208 of the 256 B rows
+  if (pk->n_per_tile > 0) max_real = std::min<int64_t>(max_real, pk->n_per_tile);
+  const int64_t n_tiles = ceil_div(og, max_real);
+  const int64_t npt = std::min<int64_t>(round_up(ceil_div(og, n_tiles), 16), max_real);
+  const int64_t n_tiles2 = ceil_div(og, npt);
+  const int64_t n_rows = round_up(4 * npt + 2, 16);
+  pk->n_tiles = (int32_t)n_tiles2;
+  pk->n_per_tile = (int32_t)npt;
+  pk->n_rows = (int32_t)n_rows;
+  pk->ones_col = (int32_t)(4 * npt);  // lo-byte ones row; the hi-byte one follows
+  int tc = 32;
+  while (tc < n_rows) tc *= 2;
+  pk->tmem_cols = tc;
+  const int64_t K = g.is_fc ? g.fc_c * g.fc_h * g.fc_w : g.cg * g.kh * g.kw;
+  const int64_t OC = g.groups * og;
+  const size_t stage_bytes = (size_t)n_rows * 128;
+  pk->b.assign((size_t)g.groups * n_tiles2 * pk->num_kb * stage_bytes, 0);
+  auto wv = [&](int64_t oc, int64_t k) -> uint16_t {
+    const int64_t idx = g.is_fc ? k * OC + oc : oc * K + k;
+    return reinterpret_cast<const uint16_t*>(w)[idx];
+  };
+  for (int64_t gi = 0; gi < g.groups; ++gi)
+    for (int64_t t = 0; t < n_tiles2; ++t)
+      for (int64_t kb = 0; kb < pk->num_kb; ++kb) {
+        uint8_t* stage = pk->b.data() + (((gi * n_tiles2 + t) * pk->num_kb + kb) * stage_bytes);
+        for (int64_t e = 0; e < 128; ++e) {
+          const int64_t km = pk->kmap[(size_t)(kb * 128 + e)];
+          if (km < 0) continue;
+          const int64_t k = km >> 1, b = km & 1;
+          auto put = [&](int64_t r, uint8_t v) {
+            stage[r * 128 + (((e >> 4) ^ (r & 7)) << 4) + (e & 15)] = v;
+          };
+          put(4 * npt + b, 1);  // ones rows: lo (b = 0) and hi (b = 1) activation byte sums
+          for (int64_t j = 0; j < npt; ++j) {
+            const int64_t o = t * npt + j;
+            if (o >= og) break;
+            const uint16_t wvv = wv(gi * og + o, k);
+            const uint8_t wl = (uint8_t)(wvv & 0xFF), wh = (uint8_t)(wvv >> 8);
+            put(j + (b ? npt : 0), wl);            // LL (b = 0) / HL (b = 1)
+            put(j + 2 * npt + (b ? npt : 0), wh);  // LH (b = 0) / HH (b = 1)
+          }
+        }
+      }
+  return QNB_OK;
+}
+
 qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, IgemmPacked* pk) {
+  if (g.q16) return igemm_pack_b_q16(g, w, pk);
   const int es = kind_es(g.kind);
   const bool quant = g.kind == KIND_I8;
   const int64_t og = g.og;
@@ -667,6 +772,8 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   if (a.ksplit == 1) a.kb_per_split = a.num_kb;
   if (a.ksplit > 1) {
     a.epi_mode = EPIM_RAW32;
+  } else if (a.epi == EPI_Q16) {
+    a.epi_mode = EPIM_Q16;
   } else if (a.epi == EPI_Q8) {
     const bool fast = a.fast_rq && a.chan_const32 != nullptr;
     a.epi_mode = fast ? (a.has_relu ? ((a.relu.acc32 && a.relu_lut) ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)

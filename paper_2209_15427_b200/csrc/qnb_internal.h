@@ -66,10 +66,10 @@ struct ActLayout {
 };
 
 // ------------------------------------------------- implicit GEMM (tcgen05)
-enum EpiKind : int { EPI_Q8 = 0, EPI_F16 = 1, EPI_F32 = 2 };
+enum EpiKind : int { EPI_Q8 = 0, EPI_F16 = 1, EPI_F32 = 2, EPI_Q16 = 3 };
 // Epilogue specialisation chosen on the host (igemm_launch).
 enum EpiMode : int { EPIM_Q8_FAST_RELU = 0, EPIM_Q8_FAST = 1, EPIM_Q8_EXACT = 2, EPIM_F16 = 3, EPIM_F32 = 4,
-                     EPIM_RAW32 = 5 };
+                     EPIM_RAW32 = 5, EPIM_Q16 = 6 };
 
 // Device copies of the reference's RequantParams, pre-digested:
 // s = shift_bits + shift (src/quantizer.cpp:202).
@@ -138,6 +138,10 @@ struct IgemmGeometry {
   int64_t oh, ow;
   bool is_fc;          // inner product: K over the flattened (NHWC) sample
   int64_t fc_h, fc_w, fc_c;  // FC input logical dims (reference flatten c,h,w)
+  // INT16Q: u16 operands split into bytes on the u8 tensor cores.  The activation is
+  // read as interleaved lo/hi bytes (K' = 2K); the B tile carries four partial-product
+  // row sets LL, HL, LH, HH (and two ones rows) so one MMA pass yields every cross term.
+  bool q16 = false;
 };
 
 // Packed operand data produced on the host for one layer.

@@ -160,12 +160,15 @@ ActLayout plain_layout(const Blob& b, int64_t batch) {
   return L;
 }
 
-int mma_kind_of(int dtype) { return dtype == QNB_INT8Q ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32); }
+int mma_kind_of(int dtype) {
+  return (dtype == QNB_INT8Q || dtype == QNB_INT16Q) ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
+}
 
 IgemmGeometry geometry_of(const qnb_layer_desc& l, const Blob& in, const Blob& out) {
   IgemmGeometry g;
   std::memset(&g, 0, sizeof(g));
   g.kind = mma_kind_of(l.d_type);
+  g.q16 = l.d_type == QNB_INT16Q;
   if (l.kind == QNB_LAYER_CONV) {
     g.groups = l.conv.groups;
     g.cg = in.c / l.conv.groups;
@@ -343,7 +346,6 @@ qnb_status lower(qnb_plan& P) {
       case QNB_LAYER_CONV:
       case QNB_LAYER_INNER_PRODUCT: {
         op.kind = OP_IGEMM;
-        if (l.d_type == QNB_INT16Q) return fail(QNB_E_UNSUPPORTED, "INT16 contractions are not implemented yet");
         const int j = sole_consumer(P, l.top);
         if (j >= 0 && P.layers[j].kind == QNB_LAYER_RELU && P.layers[j].d_type == l.mo_type &&
             P.layers[j].mo_type == l.mo_type) {
@@ -540,22 +542,24 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
                                default_shift_bits(dtype), &rq));
     a.rq = to_dev(rq);
     a.zw = qw.zero;
-    const uint8_t* w = (const uint8_t*)l.weight;
     std::vector<int64_t> cc((size_t)OC);
     for (int64_t oc = 0; oc < OC; ++oc) {
       int64_t wsum = 0;
-      for (int64_t k = 0; k < K; ++k) wsum += w[g.is_fc ? k * OC + oc : oc * K + k];
+      for (int64_t k = 0; k < K; ++k) {
+        const int64_t wi = g.is_fc ? k * OC + oc : oc * K + k;
+        wsum += dtype == QNB_INT16Q ? (int64_t)((const uint16_t*)l.weight)[wi] : (int64_t)((const uint8_t*)l.weight)[wi];
+      }
       int64_t c = K * (int64_t)qx.zero * qw.zero - (int64_t)qx.zero * wsum;
       if (l.bias_term && l.bias) c += bias_to_acc(l.bias[oc], qa.scale, qb.scale);
       cc[(size_t)oc] = c;
     }
     QNB_TRY(upload(P, cc, const_cast<int64_t**>(&a.chan_const)));
-    a.fast_rq = igemm_fast_requant_ok(cc, K, qw.zero, a.rq) ? 1 : 0;
+    a.fast_rq = (dtype == QNB_INT8Q && igemm_fast_requant_ok(cc, K, qw.zero, a.rq)) ? 1 : 0;
     if (a.fast_rq) {
       std::vector<int32_t> cc32(cc.begin(), cc.end());
       QNB_TRY(upload(P, cc32, const_cast<int32_t**>(&a.chan_const32)));
     }
-    a.epi = EPI_Q8;
+    a.epi = g.q16 ? EPI_Q16 : EPI_Q8;
     if (op.relu >= 0) {
       const Blob& rtop = P.blobs[P.layers[op.relu].top];
       qnb_requant r2;
@@ -563,9 +567,11 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
                                  default_shift_bits(dtype), &r2));
       a.relu = to_dev_relu(r2, dtype);
       a.has_relu = 1;
-      std::vector<uint8_t> lut(256);
-      for (int q = 0; q < 256; ++q) lut[(size_t)q] = (uint8_t)relu_requant_host(q, r2, dtype);
-      QNB_TRY(upload(P, lut, const_cast<uint8_t**>(&a.relu_lut)));
+      if (dtype == QNB_INT8Q) {
+        std::vector<uint8_t> lut(256);
+        for (int q = 0; q < 256; ++q) lut[(size_t)q] = (uint8_t)relu_requant_host(q, r2, dtype);
+        QNB_TRY(upload(P, lut, const_cast<uint8_t**>(&a.relu_lut)));
+      }
     }
   } else {
     if (l.bias_term && l.bias) {
@@ -580,7 +586,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   }
   // Inner products at small batch have few (m, n) tiles: split K so every SM streams
   // a share of the weights; partial s32 sums are reduced exactly by igemm_finalize.
-  if (g.is_fc && quant) {
+  if (g.is_fc && dtype == QNB_INT8Q) {
     // every CTA streams its own weight slice (no cluster): the m-tiles of one slice hit
     // in L2, so HBM sees the weights once and all 148 SMs pull in parallel
     const int64_t m_tiles = ceil_div(P.max_batch, 128);
