@@ -143,7 +143,8 @@ qnb_status qnb_softmax(const float* in, int64_t rows, int64_t cols, float* out, 
 /* conv_forward(in, weight, bias, cp, qv_out, shift_bits)  src/ops.cpp:264-342.
  * x: N x C x H x W (dtype), w: OC x C/g x KH x KW (w_dtype == dtype for quantized,
  * FP32/FP16 for float), bias: FP32 device vector or NULL, y: N x OC x OH x OW.
- * in_qv / w_qv / out_qv required for quantized dtypes (else QNB_E_QVALS). */
+ * in_qv / w_qv / out_qv required for quantized dtypes (else QNB_E_QVALS).
+ * y == NULL is a sizing call: validates and fills y_shape only. */
 qnb_status qnb_conv_forward(const void* x, const int64_t x_shape[4], qnb_dtype dtype,
                             const qnb_qvals* in_qv, const void* w, qnb_dtype w_dtype,
                             const qnb_qvals* w_qv, const float* bias, const qnb_conv_params* cp,
@@ -167,6 +168,23 @@ qnb_status qnb_moe_gate(const float* feats, int64_t batch, int64_t dim, const fl
 float qnb_gating_expf(float x);
 qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, int64_t top_k,
                            const int64_t* idx, const float* weights, float* out, qnb_stream s);
+
+/* Expert dispatch for PER_SAMPLE MoE (src/moe.cpp:220-251), device side.
+ * qnb_moe_route: groups the batch*top_k (sample, expert) pairs of `idx` per expert
+ * (stable: (sample, k) order inside an expert).  counts[n_experts]; pair_sample[p] =
+ * sample of the p-th grouped pair; pair_slot[s*top_k + k] = its grouped position. */
+qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64_t n_experts, int64_t* counts,
+                         int64_t* pair_sample, int64_t* pair_slot, qnb_stream s);
+/* dst[i] = src[rows[i]] for n rows of row_bytes bytes (device pointers). */
+qnb_status qnb_gather_rows(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n, void* dst,
+                           qnb_stream s);
+/* Mixing loop of moe_forward (src/moe.cpp:240-249) over grouped expert output rows
+ * (expert_rows[pair_slot[s*top_k+k]] is expert k's output for sample s, `per` floats),
+ * followed by the MOE layer's output conversion (src/net.cpp:495-505): quantize to
+ * out_qv for INT8Q/INT16Q, RNE narrowing for FP16, identity for FP32. */
+qnb_status qnb_moe_combine_rows(const float* expert_rows, int64_t per, const int64_t* pair_slot,
+                                const float* weights, int64_t batch, int64_t top_k, qnb_dtype out_dtype,
+                                const qnb_qvals* out_qv, void* out, qnb_stream s);
 
 /* ------------------------------------------------------------- plan level */
 /* Layer kinds: qnet::LayerKind codes (include/qnet/graph.hpp:33-44). */

@@ -411,7 +411,7 @@ qnb_status qnb_conv_forward(const void* x, const int64_t xs[4], qnb_dtype dtype,
   const bool quant = is_quant(dtype);
   if (quant && (!in_qv || !w_qv || !out_qv)) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
   if (quant && w_dtype != dtype) return fail(QNB_E_DTYPE, "quantized conv weight dtype must match input");
-  if (xs[0] == 0) return QNB_OK;
+  if (xs[0] == 0 || y == nullptr) return QNB_OK;  // y == NULL: sizing call (ys only)
   IgemmGeometry g;
   g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
   g.q16 = dtype == QNB_INT16Q;

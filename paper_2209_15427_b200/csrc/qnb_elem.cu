@@ -257,6 +257,91 @@ __global__ void moe_combine_kernel(const float* __restrict__ eo, int64_t B, int6
   }
 }
 
+
+// ------------------------------------------------------------ expert dispatch
+// Routing of (sample, expert) pairs for PER_SAMPLE dispatch (src/moe.cpp:220-251):
+// pairs are grouped per expert, in (sample, k) order inside a group, so every
+// expert runs on one contiguous sub-batch.  One CTA; thread e owns expert e, so the
+// order is deterministic without atomics.  B*K is small (1024 for AlexNet-MoE).
+constexpr int kRouteMaxExperts = 256;
+__global__ void moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, int64_t K, int64_t E,
+                                 int64_t* __restrict__ counts, int64_t* __restrict__ pair_sample,
+                                 int64_t* __restrict__ pair_slot) {
+  __shared__ int64_t cnt[kRouteMaxExperts], off[kRouteMaxExperts];
+  const int e = threadIdx.x;
+  if (e < E) {
+    int64_t c = 0;
+    for (int64_t p = 0; p < BK; ++p) c += __ldg(idx + p) == e;
+    cnt[e] = c;
+  }
+  __syncthreads();
+  if (e == 0) {
+    int64_t o = 0;
+    for (int64_t i = 0; i < E; ++i) {
+      off[i] = o;
+      o += cnt[i];
+    }
+  }
+  __syncthreads();
+  if (e < E) {
+    int64_t pos = off[e];
+    for (int64_t p = 0; p < BK; ++p)
+      if (__ldg(idx + p) == e) {
+        pair_sample[pos] = p / K;
+        pair_slot[p] = pos;
+        ++pos;
+      }
+    counts[e] = cnt[e];
+  }
+}
+
+// dst[i] = src[rows[i]] for rows of row_bytes bytes; 16-byte vectors when aligned.
+__global__ void gather_rows16_kernel(const uint4* __restrict__ src, int64_t row_vec, const int64_t* __restrict__ rows,
+                                     int64_t n, uint4* __restrict__ dst) {
+  const int64_t total = n * row_vec;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = o / row_vec, j = o - i * row_vec;
+    dst[o] = __ldg(src + __ldg(rows + i) * row_vec + j);
+  }
+}
+__global__ void gather_rows1_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                    const int64_t* __restrict__ rows, int64_t n, uint8_t* __restrict__ dst) {
+  const int64_t total = n * row_bytes;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = o / row_bytes, j = o - i * row_bytes;
+    dst[o] = src[rows[i] * row_bytes + j];
+  }
+}
+
+// moe_forward's mixing loop (src/moe.cpp:240-249): acc = 0.0f; acc += w_k * out_k in
+// selection order (unfused), reading expert k's output row at pair_slot[s*K + k],
+// then Net::run_layer_typed's MOE tail (src/net.cpp:495-505): quantize to the MoE top
+// grid (or narrow to FP16 / keep FP32).
+__global__ void moe_combine_rows_kernel(const float* __restrict__ y, int64_t per, const int64_t* __restrict__ slot,
+                                        const float* __restrict__ w, int64_t B, int64_t K, QParams q, int out_dtype,
+                                        void* __restrict__ out) {
+  const int64_t total = B * per;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = o / per, j = o - s * per;
+    float acc = 0.0f;
+    for (int64_t k = 0; k < K; ++k)
+      acc = __fadd_rn(acc, __fmul_rn(__ldg(w + s * K + k), __ldg(y + __ldg(slot + s * K + k) * per + j)));
+    switch (out_dtype) {
+      case QNB_INT8Q:
+        reinterpret_cast<uint8_t*>(out)[o] = (uint8_t)quantize_exact(acc, q);
+        break;
+      case QNB_INT16Q:
+        reinterpret_cast<uint16_t*>(out)[o] = (uint16_t)quantize_exact(acc, q);
+        break;
+      case QNB_FP16:
+        reinterpret_cast<uint16_t*>(out)[o] = f32_to_f16_bits(acc);
+        break;
+      default:
+        reinterpret_cast<float*>(out)[o] = acc;
+    }
+  }
+}
+
 // ------------------------------------------------------------ launch helpers
 static inline unsigned grid_for(int64_t n, int threads = 256, int per = 1) {
   int64_t b = ceil_div(ceil_div(n, per), threads);
@@ -477,6 +562,51 @@ qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, 
   if (batch * per <= 0) return QNB_OK;
   moe_combine_kernel<<<grid_for(batch * per), 256, 0, as_stream(s)>>>(expert_out, batch, per, top_k, idx, weights,
                                                                       out);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
+qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64_t n_experts, int64_t* counts,
+                         int64_t* pair_sample, int64_t* pair_slot, qnb_stream s) {
+  QNB_TRY(ensure_device());
+  if (n_experts < 1 || n_experts > kRouteMaxExperts) return fail(QNB_E_UNSUPPORTED, "1..256 experts supported");
+  if (top_k < 1 || top_k > n_experts) return fail(QNB_E_ARG, "top_k out of range");
+  if (batch < 0) return fail(QNB_E_SHAPE, "shape mismatch");
+  moe_route_kernel<<<1, kRouteMaxExperts, 0, as_stream(s)>>>(idx, batch * top_k, top_k, n_experts, counts,
+                                                             pair_sample, pair_slot);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
+qnb_status qnb_gather_rows(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n, void* dst,
+                           qnb_stream s) {
+  QNB_TRY(ensure_device());
+  if (n <= 0 || row_bytes <= 0) return QNB_OK;
+  if (row_bytes % 16 == 0 && ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0)
+    gather_rows16_kernel<<<grid_for(n * (row_bytes / 16)), 256, 0, as_stream(s)>>>(
+        (const uint4*)src, row_bytes / 16, rows, n, (uint4*)dst);
+  else
+    gather_rows1_kernel<<<grid_for(n * row_bytes), 256, 0, as_stream(s)>>>((const uint8_t*)src, row_bytes, rows, n,
+                                                                          (uint8_t*)dst);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
+qnb_status qnb_moe_combine_rows(const float* expert_rows, int64_t per, const int64_t* pair_slot,
+                                const float* weights, int64_t batch, int64_t top_k, qnb_dtype out_dtype,
+                                const qnb_qvals* out_qv, void* out, qnb_stream s) {
+  QNB_TRY(ensure_device());
+  if (batch * per <= 0) return QNB_OK;
+  QParams q{1.0, 1.0, 0, 0, 0};
+  if (out_dtype == QNB_INT8Q || out_dtype == QNB_INT16Q) {
+    if (!out_qv) return fail(QNB_E_QVALS, "quantizer not finalized: moe top");
+    q = QParams{out_qv->scale, 1.0 / out_qv->scale, out_qv->zero, out_qv->i_min, out_qv->i_max};
+  }
+  moe_combine_rows_kernel<<<grid_for(batch * per), 256, 0, as_stream(s)>>>(expert_rows, per, pair_slot, weights, batch,
+                                                                           top_k, q, (int)out_dtype, out);
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;

@@ -235,6 +235,11 @@ qnb_status build_blob_table(qnb_plan& P) {
       t.h = l.input_ndim > 2 ? l.input_shape[2] : 1;
       t.w = l.input_ndim > 3 ? l.input_shape[3] : 1;
       t.external = true;
+      if (is_quant(t.dtype)) {  // quantized INPUT: the tensor carries the blob's qvals (src/net.cpp:395-399)
+        if (!l.top_has_qv) return fail(QNB_E_QVALS, "quantizer not finalized: blob " + std::to_string(l.top));
+        t.has_qv = true;
+        t.qv = l.top_qv;
+      }
       continue;
     }
     if (l.bottom < 0 || l.bottom >= (int)P.blobs.size() || !P.blobs[l.bottom].defined)

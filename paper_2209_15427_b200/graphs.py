@@ -138,8 +138,10 @@ def alexnet_moe(batch: int = 1, dtype: str = "int8", n_experts: int = 16, top_k:
 
     def lrn_q(name, bottom):
         # LRN is FP32-only (src/graph.cpp:208-213): bracket it with quantizers
-        return [_quantizer(f"{bottom}_f", bottom, "fp32"), _lrn(name, f"{bottom}_f"),
-                _quantizer(f"{name}_q", name, dtype)]
+        to_f, to_q = _quantizer(f"{bottom}_f", bottom, "fp32"), _quantizer(f"{name}_q", name, dtype)
+        to_f["bottom_data_type"] = to_f["compute_data_type"] = dtype  # quantizers compute at d = mi
+        to_q["bottom_data_type"] = to_q["compute_data_type"] = "fp32"
+        return [to_f, _lrn(name, f"{bottom}_f"), to_q]
 
     def gating_body(x):
         L = [_conv("g_conv", x, 64, 5, p=2, g=2), _relu("g_relu", "g_conv"), _pool("g_pool", "g_relu", 3, 2)]
@@ -226,3 +228,46 @@ def synth_images(n: int, shape, seed: int = 20261017, offset: int = 0) -> np.nda
     for i in range(n):
         out[i] = np.random.default_rng(seed + offset + i).uniform(0.0, 255.0, shape).astype(np.float32)
     return out
+
+
+def moe_layer(g: dict) -> dict:
+    return next(l for l in g["layers"] if l["kind"] == "moe")
+
+
+def synth_params_moe(g: dict, seed: int = 20261017) -> dict:
+    """Seeded parameters of an MoE graph under the reference's dotted names
+    (include/qnet/net.hpp:36-40): trunk/tail layers by name, "<moe>.gating.<p>",
+    "<moe>.expert<k>.<p>", and the gate matrices "<moe>.gate_a/_b/_c" with
+    W_a ~ U(-0.5, 0.5), W_b = W_c = 0 (noise off)."""
+    from . import graph as G
+    m = moe_layer(g)
+    name, spec = m["name"], m["moe"]
+    main = {"name": g.get("name", ""), "layers": [l for l in g["layers"] if l["kind"] != "moe"]}
+    shapes = {}
+    for b, v in G.infer_blobs(g).items():
+        shapes[b] = v["shape"]
+    params = {}
+    # trunk and tail layers (the MoE layer owns no weight of its own besides the gates)
+    specs = [s for s in param_specs(g, shapes)]
+    for i, (pname, shape, fan) in enumerate(specs):
+        rng = np.random.default_rng(seed + 7919 * (i + 1))
+        b = 0.1 if fan is None else 1.0 / np.sqrt(fan)
+        params[pname] = rng.uniform(-b, b, shape).astype(np.float32)
+    del main
+    gshapes = {b: v["shape"] for b, v in G.infer_blobs(spec["gating"]).items()}
+    for k, v in synth_params(spec["gating"], gshapes, seed=seed + 1).items():
+        params[f"{name}.gating.{k}"] = v
+    eshapes = {b: v["shape"] for b, v in G.infer_blobs(spec["expert"]).items()}
+    for e in range(spec["n_experts"]):
+        for k, v in synth_params(spec["expert"], eshapes, seed=seed + 101 * (e + 2)).items():
+            params[f"{name}.expert{e}.{k}"] = v
+    D = [v for v in G.infer_blobs(spec["gating"]).values() if not v["consumers"]][-1]["shape"][1]
+    N = spec["n_experts"]
+    rng = np.random.default_rng(seed + 99991)
+    params[f"{name}.gate_a"] = rng.uniform(-0.5, 0.5, (N, D)).astype(np.float32)
+    params[f"{name}.gate_b"] = np.zeros((N, D), np.float32)
+    params[f"{name}.gate_c"] = np.zeros((N,), np.float32)
+    return params
+
+
+MODELS["alexnet_moe"] = alexnet_moe

@@ -34,7 +34,9 @@ def observe_one(args):
     net = ref.net(json.dumps(g), DT[precision])
     rg = json.loads(net.graph_json())
     shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
-    for name, arr in graphs.synth_params(g, shapes).items():
+    moe = [l for l in g["layers"] if l["kind"] == "moe"]
+    params = graphs.synth_params_moe(g) if moe else graphs.synth_params(g, shapes)
+    for name, arr in params.items():
         net.set_param(name, arr)
     net.set_mode(1)  # OBSERVE
     inp = G.input_name(g)
@@ -45,6 +47,16 @@ def observe_one(args):
         r = net.range(b)
         if r is not None:
             out[G.range_key(G.range_aliases(rg), b)] = r
+    for m in moe:  # nested nets: "<moe>.gating.<key>", "<moe>.expert<k>.<key>" (src/net.cpp:161-167)
+        subs = [("gating", m["moe"]["gating"])] + [(f"expert{k}", m["moe"]["expert"])
+                                                   for k in range(m["moe"]["n_experts"])]
+        for prefix, sg in subs:
+            al = G.range_aliases(G.normalized(sg))
+            for b in G.infer_blobs(sg):
+                key = G.range_key(al, b)
+                r = net.range(f"{m['name']}.{prefix}.{key}")
+                if r is not None:
+                    out[f"{m['name']}.{prefix}.{key}"] = r
     return out
 
 

@@ -1,0 +1,78 @@
+"""AlexNet-MoE INT8 (BASELINE configs[2]) on the B200 vs the
+unmodified reference qnet::Net: the MoE layer's quantized output is bit-exact and the
+softmax sink is within 1 ulp (libm exp vs device exp in the FP32 island)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2209_15427_b200 import graph as G
+from paper_2209_15427_b200 import graphs
+from paper_2209_15427_b200.net import QUANTIZED
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def setup(reference):
+    g = graphs.alexnet_moe(1)
+    params = graphs.synth_params_moe(g)
+    with open(os.path.join(ROOT, "tests", "golden", "alexnet_moe_int8_calib.json")) as f:
+        ranges = json.load(f)["ranges"]
+    return g, params, ranges
+
+
+def ref_net(reference, graph_json, params, ranges, precision):
+    net = reference.net(graph_json, precision)
+    for k, v in params.items():
+        net.set_param(k, v)
+    for k, (lo, hi) in ranges.items():
+        net.set_range(k, lo, hi)
+    net.finalize()
+    net.set_mode(3)
+    return net
+
+
+def our_net(g, params, ranges):
+    from paper_2209_15427_b200.moe import MoeNet
+    net = MoeNet(G.override_precision(g, "int8"))
+    for k, v in params.items():
+        net.set_param(k, v)
+    for k, (lo, hi) in ranges.items():
+        net.set_range(k, lo, hi)
+    net.finalize_quantizers()
+    net.set_quant_mode(QUANTIZED)
+    return net
+
+
+def test_alexnet_moe_int8_matches_reference(reference, setup):
+    import torch
+    g, params, ranges = setup
+    batch = 3
+    x = graphs.synth_images(batch, (3, 227, 227), offset=0)
+    ours = our_net(g, params, ranges)
+    out = ours.forward({"data": x})["prob"]
+    counts = ours.last_stats["counts"]
+    assert counts.sum() == batch * 4
+
+    rn = ref_net(reference, json.dumps(g), params, ranges, 2)
+    full = json.loads(rn.graph_json())
+    prob_ref = rn.forward("data", x)["prob"][0]
+    d = np.abs(out.view(np.int32).astype(np.int64) - prob_ref.view(np.int32).astype(np.int64))
+    assert d.max() <= 1, d.max()
+
+    # the MoE layer's own quantized output, bit for bit (reference prefix net ending at it)
+    names = [l["name"] for l in full["layers"]]
+    prefix = {"name": "moe_prefix", "layers": full["layers"][: names.index("moe") + 1],
+              "range_aliases": full.get("range_aliases", {})}
+    keep = {l["name"] for l in prefix["layers"]}
+    pp = {k: v for k, v in params.items() if k.split(".")[0] in keep}
+    rp = ref_net(reference, json.dumps(prefix), pp, ranges, -1)
+    (m_ref, dt, qv), = rp.forward("data", x).values()
+    assert dt == 2
+    p = ours._pipe(batch)
+    m_ours = p["bufs"]["M"].cpu().numpy()[: m_ref.size].reshape(m_ref.shape)
+    assert np.array_equal(m_ours, m_ref), int((m_ours != m_ref).sum())
+    torch.cuda.synchronize()
