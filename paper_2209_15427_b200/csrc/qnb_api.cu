@@ -202,7 +202,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   a.a_img = io.in.img();
   a.a_row = io.in.row();
   a.a_pix = io.in.pix();
-  a.a_group = g.cg * io.in.es();
+  a.a_group = pk.all_groups ? 0 : g.cg * io.in.es();
   a.a_origin = (io.in.hh - g.ph) * io.in.row() + (io.in.hw - g.pw) * io.in.pix();
   a.stride_h = (int32_t)g.sh;
   a.stride_w = (int32_t)g.sw;

@@ -526,19 +526,21 @@ qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked
                         in.pix() % 16 == 0;
     const int64_t tap_chunks = g.kh * g.kw * ceil_div(cg_bytes, 16);
     const int64_t run_bytes = g.kw * in.pix();
-    const bool run_ok = g.groups == 1 && (g.sw * in.pix()) % 16 == 0 && in.row() % 16 == 0 &&
+    const bool run_ok = (g.groups == 1 || !tap_ok) && (g.sw * in.pix()) % 16 == 0 && in.row() % 16 == 0 &&
                         in.interior_offset() % 16 == 0;
     const int64_t run_chunks = g.kh * ceil_div(run_bytes, 16);
     const bool use_run = run_ok && (!tap_ok || run_chunks < tap_chunks);
     if (!tap_ok && !run_ok) return fail(QNB_E_UNSUPPORTED, "channel layout not 16-byte aligned");
     if (use_run) {
+      pk->all_groups = g.groups > 1;
+      const int64_t c_lim = pk->all_groups ? g.cg * g.groups : g.cg;
       const int64_t nrun = ceil_div(run_bytes, 16);
       for (int64_t r = 0; r < g.kh; ++r)
         for (int64_t jj = 0; jj < nrun; ++jj)
           push_chunk(r * in.row() + jj * 16, [&](int e) -> int64_t {
             const int64_t b = jj * 16 + (int64_t)e * es;
             const int64_t s = b / in.pix(), c = (b % in.pix()) / es;
-            if (s >= g.kw || c >= g.cg) return -1;
+            if (s >= g.kw || c >= c_lim) return -1;
             return (c * g.kh + r) * g.kw + s;
           });
     } else {
@@ -590,7 +592,8 @@ static qnb_status igemm_pack_b_q16(const IgemmGeometry& g, const void* w, IgemmP
         for (int64_t e = 0; e < 128; ++e) {
           const int64_t km = pk->kmap[(size_t)(kb * 128 + e)];
           if (km < 0) continue;
-          const int64_t k = km >> 1, b = km & 1;
+          const int64_t k = igemm_local_k(g, *pk, km >> 1, gi), b = km & 1;
+          if (k < 0) continue;
           auto put = [&](int64_t r, uint8_t v) {
             stage[r * 128 + (((e >> 4) ^ (r & 7)) << 4) + (e & 15)] = v;
           };
@@ -657,7 +660,7 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
           if (!real && !ones) continue;
           for (int64_t e = 0; e < elems_per_stage; ++e) {
             const int64_t kk = kb * elems_per_stage + e;
-            const int64_t k = pk->kmap[(size_t)kk];
+            const int64_t k = igemm_local_k(g, *pk, pk->kmap[(size_t)kk], gi);
             if (k < 0) continue;
             const int64_t byte = e * es;
             const int64_t dst = r * 128 + (((byte >> 4) ^ (r & 7)) << 4) + (byte & 15);

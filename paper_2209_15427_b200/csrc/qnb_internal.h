@@ -151,7 +151,20 @@ struct IgemmPacked {
   int32_t num_kb = 0;
   int32_t n_rows = 0, n_tiles = 0, n_per_tile = 0, ones_col = -1, tmem_cols = 0;
   std::vector<uint8_t> b;           // [G][n_tiles][num_kb][n_rows][128]
+  // Grouped conv whose per-group channel slice is not 16-byte aligned: the A rows are
+  // whole kernel-row runs over ALL channels (shared by every group, a_group = 0) and
+  // kmap holds the group-global reference index (c_global*KH + r)*KW + s; the packer
+  // zeroes the other groups' channels (weights and ones row).
+  bool all_groups = false;
 };
+
+// kmap entry -> group-local reference K index for group gi (or -1: not this group's).
+inline int64_t igemm_local_k(const IgemmGeometry& g, const IgemmPacked& pk, int64_t km, int64_t gi) {
+  if (km < 0 || !pk.all_groups) return km;
+  const int64_t sp = g.kh * g.kw, c = km / sp;
+  if (c / g.cg != gi) return -1;
+  return (c - gi * g.cg) * sp + km % sp;
+}
 
 // Builds the chunk table + K map for an input layout and geometry.
 qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk);

@@ -519,7 +519,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   a.a_img = Lin.img();
   a.a_row = Lin.row();
   a.a_pix = Lin.pix();
-  a.a_group = g.cg * Lin.es();
+  a.a_group = pk.all_groups ? 0 : g.cg * Lin.es();
   a.a_origin = (Lin.hh - g.ph) * Lin.row() + (Lin.hw - g.pw) * Lin.pix();
   a.stride_h = (int32_t)g.sh;
   a.stride_w = (int32_t)g.sw;
@@ -656,8 +656,8 @@ qnb_status emit(qnb_plan& P) {
         p.src = nullptr;
         st.src_sym = SYM_INPUT;
         p.src_dtype = src.dtype;
-        if (src.dtype != QNB_FP32 && src.dtype != QNB_FP16)
-          return fail(QNB_E_UNSUPPORTED, "quantized INPUT blobs");
+        if ((src.dtype == QNB_INT8Q || src.dtype == QNB_INT16Q) && (op.pack_op != PACK_COPY || dst.dtype != src.dtype))
+          return fail(QNB_E_UNSUPPORTED, "quantized INPUT blobs feed their own dtype only");
         p.N = P.max_batch;
         p.C = src.c;
         p.H = src.h;

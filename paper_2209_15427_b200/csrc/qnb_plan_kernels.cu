@@ -127,9 +127,20 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
   const int64_t y = blockIdx.y, n = blockIdx.z;
   const int64_t plane = H * W;
   uint8_t* o = at(dst, L, n, y, x);
-  const int ses = src_dtype == QNB_FP32 ? 4 : 2;
+  const int ses = src_dtype == QNB_FP32 ? 4 : (src_dtype == QNB_INT8Q ? 1 : 2);
   const uint8_t* s = src + ((n * C) * plane + y * W + x) * ses;
   const float invf = (float)q.inv;
+  if (src_dtype == QNB_INT8Q || src_dtype == QNB_INT16Q) {
+    // quantized INPUT (the tensor already carries the blob's grid, src/net.cpp:395-399): copy
+    for (int64_t c = 0; c < L.c_phys; ++c) {
+      const int64_t v = c >= C ? (int64_t)fill
+                               : (src_dtype == QNB_INT8Q ? (int64_t)s[c * plane]
+                                                          : (int64_t)reinterpret_cast<const uint16_t*>(s)[c * plane]);
+      if (dst_dtype == QNB_INT8Q) o[c] = (uint8_t)v;
+      else reinterpret_cast<uint16_t*>(o)[c] = (uint16_t)v;
+    }
+    return;
+  }
   if (dst_dtype == QNB_INT8Q && L.c_phys <= 16 && (L.c_phys & 3) == 0) {
     uint32_t words[4] = {0, 0, 0, 0};
 #pragma unroll 4

@@ -152,6 +152,9 @@ CONV_CASES = [
     (3, 16, 9, 11, dict(out_channels=20, kernel_h=3, kernel_w=3, stride_h=2, stride_w=1, pad_h=1, pad_w=0)),
     (2, 32, 8, 8, dict(out_channels=300, kernel_h=1, kernel_w=1)),
     (5, 1, 28, 28, dict(out_channels=20, kernel_h=5, kernel_w=5)),  # LeNet conv1
+    # AlexNet-MoE expert/gating conv1: 24 channels per group (not 16-byte aligned)
+    (2, 48, 27, 27, dict(out_channels=64, kernel_h=5, kernel_w=5, pad_h=2, pad_w=2, groups=2)),
+    (2, 96, 13, 13, dict(out_channels=64, kernel_h=3, kernel_w=3, pad_h=1, pad_w=1, groups=4)),
 ]
 
 
@@ -162,7 +165,7 @@ def test_conv_int8_bit_exact(oracle_impl, case):
 
 
 @pytest.mark.parametrize("dtype", [FP32, FP16])
-@pytest.mark.parametrize("case", [0, 1, 2, 5])
+@pytest.mark.parametrize("case", [0, 1, 2, 5, 8])
 def test_conv_float_tolerance(oracle_impl, dtype, case):
     N, C, H, W, cp = CONV_CASES[case]
     _conv_case(oracle_impl, np.random.default_rng(200 + case), N, C, H, W, cp, dtype)
