@@ -130,6 +130,11 @@ struct qnb_plan {
   const void* g_in = nullptr;
   void* g_out = nullptr;
   int64_t g_batch = -1;
+  int32_t g_flags = -1;
+  // host-buffer pipeline: H2D of chunk i+1 on copy_stream overlaps the forward of chunk i
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr;
+  std::vector<cudaEvent_t> ev_copy;
   int64_t launches_per_forward = 0;
   cudaStream_t capture_stream = nullptr;
   int device = 0;
@@ -902,24 +907,86 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
   return QNB_OK;
 }
 
+// Host-buffer forwards are pipelined: the batch is cut into chunks (>= 32 images,
+// at most 8), chunk i's H2D copy runs on the plan's copy stream while chunk i-1 runs
+// through the network on the compute stream, and each chunk's result is copied back
+// as soon as it is done.  Sub-batches reuse the activation arena in order (the
+// compute stream serialises them), so no extra device memory is needed.
+static int64_t pipeline_chunks(int64_t batch) {
+  if (batch < 64) return 1;
+  return std::min<int64_t>(8, batch / 32);
+}
+
+static qnb_status forward_body(qnb_plan& P, int64_t batch, const void* input, bool in_host, void* output,
+                               bool out_host, bool pinned_in, cudaStream_t s) {
+  void* out_dev = out_host ? P.out_staging : output;
+  if (!in_host) {
+    QNB_TRY(launch_steps(P, batch, input, out_dev, s));
+    if (out_host)
+      QNB_CUDA(cudaMemcpyAsync(output, out_dev, (size_t)(P.out_bytes_per_sample * batch), cudaMemcpyDeviceToHost, s));
+    return QNB_OK;
+  }
+  const int64_t nch = pipeline_chunks(batch), per = ceil_div(batch, nch);
+  const size_t ib = (size_t)P.in_bytes_per_sample, ob = (size_t)P.out_bytes_per_sample;
+  uint8_t* stage = (uint8_t*)P.in_staging;
+  if (pinned_in) {
+    // all copies queued on the copy stream up front; each chunk's compute waits for its copy
+    QNB_CUDA(cudaEventRecord(P.ev_fork, s));
+    QNB_CUDA(cudaStreamWaitEvent(P.copy_stream, P.ev_fork, 0));
+    for (int64_t i = 0, b0 = 0; b0 < batch; ++i, b0 += per) {
+      const int64_t b = std::min(per, batch - b0);
+      QNB_CUDA(cudaMemcpyAsync(stage + b0 * ib, (const uint8_t*)input + b0 * ib, b * ib, cudaMemcpyHostToDevice,
+                               P.copy_stream));
+      QNB_CUDA(cudaEventRecord(P.ev_copy[(size_t)i], P.copy_stream));
+    }
+  }
+  for (int64_t i = 0, b0 = 0; b0 < batch; ++i, b0 += per) {
+    const int64_t b = std::min(per, batch - b0);
+    if (pinned_in) {
+      QNB_CUDA(cudaStreamWaitEvent(s, P.ev_copy[(size_t)i], 0));
+    } else {
+      // pageable source: the copy call itself blocks the host, so issue it right before
+      // its chunk; the device keeps computing the previous chunk meanwhile
+      QNB_CUDA(cudaMemcpyAsync(stage + b0 * ib, (const uint8_t*)input + b0 * ib, b * ib, cudaMemcpyHostToDevice, s));
+    }
+    QNB_TRY(launch_steps(P, b, stage + b0 * ib, (uint8_t*)out_dev + b0 * ob, s));
+    if (out_host)
+      QNB_CUDA(cudaMemcpyAsync((uint8_t*)output + b0 * ob, (uint8_t*)out_dev + b0 * ob, b * ob,
+                               cudaMemcpyDeviceToHost, s));
+  }
+  return QNB_OK;
+}
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32_t input_on_host, void* output,
                             int32_t output_on_host, qnb_stream s_) {
   if (!P) return fail(QNB_E_ARG, "null plan");
   if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
   cudaStream_t s = as_stream(s_);
-  const void* in_dev = input;
-  void* out_dev = output;
-  if (input_on_host) {
-    if (!P->in_staging) QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
-    QNB_CUDA(cudaMemcpyAsync(P->in_staging, input, (size_t)(P->in_bytes_per_sample * batch), cudaMemcpyHostToDevice, s));
-    in_dev = P->in_staging;
+  if (input_on_host && !P->in_staging)
+    QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
+  if (output_on_host && !P->out_staging)
+    QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
+  if (input_on_host && !P->copy_stream) {
+    QNB_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+    QNB_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+    P->ev_copy.resize(8);
+    for (auto& e : P->ev_copy) QNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if (output_on_host) {
-    if (!P->out_staging) QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
-    out_dev = P->out_staging;
-  }
-  if (P->use_graph) {
-    if (!P->exec || P->g_in != in_dev || P->g_out != out_dev || P->g_batch != batch) {
+  const bool pinned_in = input_on_host && is_pinned(input);
+  const bool pinned_out = !output_on_host || is_pinned(output);
+  // pageable host buffers cannot be captured: run those forwards eagerly
+  if (P->use_graph && (!input_on_host || pinned_in) && pinned_out) {
+    const int32_t flags = (input_on_host ? 1 : 0) | (output_on_host ? 2 : 0);
+    if (!P->exec || P->g_in != input || P->g_out != output || P->g_batch != batch || P->g_flags != flags) {
       if (P->exec) {
         cudaGraphExecDestroy(P->exec);
         P->exec = nullptr;
@@ -927,24 +994,25 @@ qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32
       cudaGraph_t graph;
       if (!P->capture_stream) QNB_CUDA(cudaStreamCreateWithFlags(&P->capture_stream, cudaStreamNonBlocking));
       QNB_CUDA(cudaStreamBeginCapture(P->capture_stream, cudaStreamCaptureModeThreadLocal));
-      qnb_status st = launch_steps(*P, batch, in_dev, out_dev, P->capture_stream);
+      qnb_status st = forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in,
+                                   P->capture_stream);
       cudaError_t e = cudaStreamEndCapture(P->capture_stream, &graph);
       if (st != QNB_OK) return st;
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
       e = cudaGraphInstantiate(&P->exec, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-      P->g_in = in_dev;
-      P->g_out = out_dev;
+      P->g_in = input;
+      P->g_out = output;
       P->g_batch = batch;
+      P->g_flags = flags;
     }
     QNB_CUDA(cudaGraphLaunch(P->exec, s));
   } else {
-    QNB_TRY(launch_steps(*P, batch, in_dev, out_dev, s));
+    QNB_TRY(forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in, s));
   }
-  count_launch((uint64_t)P->launches_per_forward);
-  if (output_on_host)
-    QNB_CUDA(cudaMemcpyAsync(output, out_dev, (size_t)(P->out_bytes_per_sample * batch), cudaMemcpyDeviceToHost, s));
+  const int64_t nch = input_on_host ? pipeline_chunks(batch) : 1;
+  count_launch((uint64_t)(P->launches_per_forward * nch));
   return QNB_OK;
 }
 
@@ -1019,6 +1087,9 @@ qnb_status qnb_plan_destroy(qnb_plan* P) {
   if (!P) return QNB_OK;
   if (P->exec) cudaGraphExecDestroy(P->exec);
   if (P->capture_stream) cudaStreamDestroy(P->capture_stream);
+  if (P->copy_stream) cudaStreamDestroy(P->copy_stream);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  for (auto e : P->ev_copy) cudaEventDestroy(e);
   if (P->arena) cudaFree(P->arena);
   for (void* p : P->weight_allocs) cudaFree(p);
   if (P->in_staging) cudaFree(P->in_staging);

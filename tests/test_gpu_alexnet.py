@@ -110,3 +110,28 @@ def test_alexnet_int8_bit_exact(setup):
     prob_ref = res["prob"][0]
     d = np.abs(out.view(np.int32).astype(np.int64) - prob_ref.view(np.int32).astype(np.int64))
     assert d.max() <= 1, d.max()
+
+
+def test_host_buffer_pipeline_matches_device_forward(setup):
+    """qnb_plan_forward with host buffers cuts the batch into chunks whose H2D copies
+    overlap the previous chunk's forward; pinned (CUDA-graph) and pageable (eager)
+    sources must give exactly the device-resident result."""
+    import torch
+    ref, g, params, ranges, ours = setup
+    batch = 100  # 3 chunks of 34 / 34 / 32
+    x = graphs.synth_images(batch, (3, 227, 227), offset=500)
+    plan = ours.compile(batch)
+    xd = torch.from_numpy(x).cuda()
+    od = torch.empty((batch, 1000), dtype=torch.float32, device="cuda")
+    plan.forward_device(xd.data_ptr(), od.data_ptr(), batch)
+    torch.cuda.synchronize()
+    want = od.cpu().numpy()
+    xp = torch.from_numpy(x).pin_memory()
+    op = torch.empty((batch, 1000), dtype=torch.float32).pin_memory()
+    for _ in range(2):  # capture, then replay
+        op.zero_()
+        plan.forward_device(xp.data_ptr(), op.data_ptr(), batch, in_host=True, out_host=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(op.numpy(), want)
+    got = plan.forward_host(x)  # pageable numpy buffers
+    assert np.array_equal(got, want)
