@@ -3,6 +3,7 @@
 #include <cuda_fp16.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -129,7 +130,13 @@ ActLayout choose_input_layout(const IgemmGeometry& g, int dtype, int64_t n, int6
     while (R.row() % 16 != 0) ++R.wx;
     // window origins (a_origin + oy*sh*row + ox*sw*pix, a_origin = 0 as halo == pad)
     // must be 16-byte aligned for the 16-byte run chunks
-    if ((g.sw * R.pix()) % 16 == 0) return R;
+    if ((g.sw * R.pix()) % 16 == 0) {
+      ActLayout Q = R;  // row-Hankel conv: image-pair interleaved, 1024-byte row slots
+      Q.wx = 0;
+      Q.pair_slot = kHkSlot;
+      if (hk_geometry_ok(g, Q)) return Q;
+      return R;
+    }
   }
   L.c_phys = round_up(c * es, 16) / es;
   return L;
@@ -189,10 +196,33 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   std::vector<uint8_t> wh((size_t)(OC * K) * dtype_size(w_dtype));
   QNB_TRY(d2h(wh.data(), w_dev, wh.size(), s));
   IgemmPacked pk;
-  QNB_TRY(igemm_plan_k(g, io.in, &pk));
+  int32_t hk_kpr = 0;
+  const bool hk = igemm_hk_eligible(g, io.in);
+  static const bool no_tma = std::getenv("QNB_NO_TMA") != nullptr;  // A/B switch for profiling
+  // Patch mode is opt-in (QNB_PATCH=1) until it beats the cp.async gather; TMA im2col
+  // is used where a tap's channels fill whole 128-byte stages (measured faster there).
+  static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
+  const bool patch = !hk && use_patch && igemm_patch_eligible(g, io.in);
+  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, io.in) && (g.cg * io.in.es()) % 128 == 0;
+  int32_t pt_pairs = 0;
+  if (hk)
+    QNB_TRY(igemm_plan_hk(g, io.in, &pk, &hk_kpr));
+  else if (patch)
+    QNB_TRY(igemm_plan_patch(g, io.in, &pk, &pt_pairs));
+  else if (tma)
+    QNB_TRY(igemm_plan_tma(g, io.in, &pk));
+  else
+    QNB_TRY(igemm_plan_k(g, io.in, &pk));
   if (g.is_fc) {
     pk.n_per_tile = 64;
     if (const char* e = getenv("QNB_IP_NPT")) pk.n_per_tile = atoi(e);  // test hook
+  }
+  int32_t pt_bstat_npt = 0;
+  if (patch && g.kind == KIND_I8 && !std::getenv("QNB_NO_BSTAT")) {
+    const int64_t wp = io.in.w + 2 * g.pw;
+    const int64_t rows = (wp + 125 + g.kw) / wp + g.kh;
+    pt_bstat_npt = igemm_patch_bstat_npt(g, pk.num_kb, (int32_t)(round_up(rows * wp * 16, 128) + 64));
+    if (pt_bstat_npt > 0) pk.n_per_tile = pt_bstat_npt;
   }
   QNB_TRY(igemm_pack_b(g, wh.data(), w_dtype, &pk));
 
@@ -202,7 +232,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   a.a_img = io.in.img();
   a.a_row = io.in.row();
   a.a_pix = io.in.pix();
-  a.a_group = pk.all_groups ? 0 : g.cg * io.in.es();
+  a.a_group = pk.all_groups ? 0 : (tma ? g.cg : g.cg * io.in.es());
   a.a_origin = (io.in.hh - g.ph) * io.in.row() + (io.in.hw - g.pw) * io.in.pix();
   a.stride_h = (int32_t)g.sh;
   a.stride_w = (int32_t)g.sw;
@@ -210,6 +240,31 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   a.ow = (int32_t)g.ow;
   a.m_total = io.in.n * g.oh * g.ow;
   a.num_kb = pk.num_kb;
+  a.kbytes = pk.kbytes;
+  if (patch) {
+    a.patch = 1;
+    a.pt_wp = (int32_t)(io.in.w + 2 * g.pw);
+    a.pt_hp = (int32_t)(io.in.h + 2 * g.ph);
+    a.pt_rows = (int32_t)((a.pt_wp + 125 + g.kw) / a.pt_wp + g.kh);
+    a.pt_plane = (int32_t)(round_up((int64_t)a.pt_rows * a.pt_wp * 16, 128) + 64);  // +64: plane 1 on other banks
+    a.pt_pairs = pt_pairs;
+    a.pt_kh = (int32_t)g.kh;
+    a.pt_kw = (int32_t)g.kw;
+    a.pt_cblk = (int32_t)(16 / io.in.es());
+    a.pt_nblk = (int32_t)(g.cg * io.in.es() / 16);
+    a.pt_bstat = pt_bstat_npt > 0 ? 1 : 0;
+  }
+  if (tma) {
+    a.a_tma = 1;
+    QNB_TRY(igemm_encode_tma(g, io.in, (const uint8_t*)xin, pk.kbytes, &a.tmap_a));
+  }
+  if (hk) {
+    a.hk = 1;
+    a.hk_rows = (int32_t)g.kh;
+    a.hk_kpr = hk_kpr;
+    a.hk_copy = (int32_t)(g.kh * io.in.row());           // kh rows of one image pair
+    a.hk_pairs = (int32_t)ceil_div(io.in.n, 2);
+  }
   a.n_rows = pk.n_rows;
   a.n_tiles = pk.n_tiles;
   a.n_real = (int32_t)g.og;
@@ -283,6 +338,13 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
       }
     }
   }
+  uint8_t* dump = nullptr;
+  const char* dump_path = std::getenv("QNB_PATCH_DUMP");
+  if (patch && dump_path) {  // debug: first tile's A stage + B stage 0
+    QNB_TRY(tmp.alloc((void**)&dump, (size_t)(2 * a.pt_plane + pk.n_rows * 128 + 128 * pk.n_rows * 4)));
+    a.ws = (int32_t*)dump;
+    a.dbg |= 8;
+  }
   a.o_es = (int32_t)out_layout.es();
   uint8_t* yout = (uint8_t*)y;
   if (unpack_nchw) QNB_TRY(tmp.alloc((void**)&yout, (size_t)out_layout.bytes() + 256));
@@ -294,6 +356,14 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   a.o_vec = (out_layout.pix() % 16 == 0 && (g.og * a.o_es) % 16 == 0 && (pk.n_per_tile * a.o_es) % 16 == 0) ? 1 : 0;
   const int kind = g.kind;
   QNB_TRY(igemm_launch(kind, a, g.groups, s));
+  if (dump) {
+    std::vector<uint8_t> h((size_t)(2 * a.pt_plane + pk.n_rows * 128 + 128 * pk.n_rows * 4));
+    QNB_TRY(d2h(h.data(), dump, h.size(), s));
+    if (FILE* f = std::fopen(dump_path, "wb")) {
+      std::fwrite(h.data(), 1, h.size(), f);
+      std::fclose(f);
+    }
+  }
   if (a.ksplit > 1) QNB_TRY(igemm_finalize(a, s));
   if (unpack_nchw) QNB_TRY(launch_nhwc_to_nchw(yout, dtype, out_layout, y, s));
   // Temporaries are released stream-ordered; host vectors must outlive the async copies.

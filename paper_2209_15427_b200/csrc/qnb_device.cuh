@@ -70,6 +70,28 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
+// TMA im2col load of a 4-D NHWC tensor: `pixels` (tensor-map) consecutive filter-window
+// positions starting at window (w, h, n), channels [c, c + channelsPerPixel), each
+// shifted by the filter tap (ow, oh); completes on `bar`.
+__device__ __forceinline__ void tma_im2col_4d(void* smem_dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                              uint16_t ow, uint16_t oh, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+
+// TMA tile load of a 3-D tensor box at (c0, c1, c2); completes on `bar`.
+__device__ __forceinline__ void tma_tile_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -126,6 +148,16 @@ __device__ __forceinline__ void tc_commit_multicast(uint64_t* bar, uint16_t mask
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync): lets a whole warp run the MMA-issue loop
+// in uniform registers while exactly one thread issues each tcgen05 instruction.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // Instruction kinds of the implicit-GEMM engine.
 enum MmaKind : int { KIND_I8 = 0, KIND_F16 = 1, KIND_TF32 = 2 };
 
@@ -166,6 +198,15 @@ __device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t& r) {
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// Wait that also pins the 16 destination registers of an earlier tmem_ld16: their
+// uses cannot be scheduled above the wait (the asynchronous load writes them).
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
 
 // UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, rows of 128
 // bytes grouped in 1024-byte atoms (SBO = 1024).  Start must lie in a
@@ -178,6 +219,32 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* base) {
   d |= (1024ull >> 4) << 32;              // SBO
   d |= 1ull << 46;                        // descriptor version (sm_100)
   d |= 2ull << 61;                        // SWIZZLE_128B
+  return d;
+}
+
+// K-major swizzled descriptor for kbytes-wide rows (128 / 64 / 32: SWIZZLE_128B /
+// _64B / _32B; an atom is 8 rows, SBO = 8 * kbytes).
+__device__ __forceinline__ uint64_t smem_desc_sw(const void* base, int kbytes) {
+  const uint64_t addr = smem_u32(base);
+  const uint64_t layout = kbytes == 128 ? 2ull : (kbytes == 64 ? 4ull : 6ull);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= 1ull << 16;
+  d |= (uint64_t)((8 * kbytes) >> 4) << 32;
+  d |= 1ull << 46;
+  d |= layout << 61;
+  return d;
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE: core matrices of 8 rows x 16
+// bytes; element (m, k) at (m%8)*16 + (m/8)*sbo + (k%16) + (k/16)*lbo bytes.
+__device__ __forceinline__ uint64_t smem_desc_none(const void* base, uint32_t lbo, uint32_t sbo) {
+  const uint64_t addr = smem_u32(base);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100); layout type 0 = SWIZZLE_NONE
   return d;
 }
 

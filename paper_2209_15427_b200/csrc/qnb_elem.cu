@@ -221,14 +221,16 @@ __global__ void softmax_kernel(const float* __restrict__ in, int64_t F, float* _
 template <typename T>
 __global__ void nchw_to_nhwc_kernel(const T* __restrict__ in, int64_t N, int64_t C, int64_t H, int64_t W,
                                     int64_t hh, int64_t hw, int64_t Hp, int64_t Wp, int64_t cp, T fill,
-                                    T* __restrict__ out) {
+                                    T* __restrict__ out, int64_t row_e, int64_t pslot_e) {
+  // row_e / pslot_e: row pitch and pair slot in elements (pslot_e = 0: plain NHWC)
   const int64_t total = N * Hp * Wp * cp;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = o % cp, x = (o / cp) % Wp, y = (o / (cp * Wp)) % Hp, n = o / (cp * Wp * Hp);
     const int64_t iy = y - hh, ix = x - hw;
     T v = fill;
     if (c < C && iy >= 0 && iy < H && ix >= 0 && ix < W) v = in[((n * C + c) * H + iy) * W + ix];
-    out[o] = v;
+    const int64_t img = pslot_e ? (n >> 1) * Hp * row_e + (n & 1) * pslot_e : n * Hp * row_e;
+    out[img + y * row_e + x * cp + c] = v;
   }
 }
 
@@ -357,20 +359,22 @@ qnb_status launch_nchw_to_nhwc(const void* in, int dtype, int64_t N, int64_t C, 
   switch (dtype) {
     case QNB_INT8Q:
       nchw_to_nhwc_kernel<uint8_t><<<g, 256, 0, s>>>((const uint8_t*)in, N, C, H, W, L.hh, L.hw, L.hp(), L.wp(), L.c_phys,
-                                                     (uint8_t)fill, (uint8_t*)out);
+                                                     (uint8_t)fill, (uint8_t*)out, L.row() / L.es(),
+                                                     L.pair_slot / L.es());
       break;
     case QNB_INT16Q:
       nchw_to_nhwc_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)in, N, C, H, W, L.hh, L.hw, L.hp(), L.wp(), L.c_phys,
-                                                      (uint16_t)fill, (uint16_t*)out);
+                                                      (uint16_t)fill, (uint16_t*)out, L.row() / L.es(),
+                                                      L.pair_slot / L.es());
       break;
     case QNB_FP16: {
       nchw_to_nhwc_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)in, N, C, H, W, L.hh, L.hw, L.hp(), L.wp(), L.c_phys,
-                                                      (uint16_t)0, (uint16_t*)out);
+                                                      (uint16_t)0, (uint16_t*)out, L.row() / L.es(), L.pair_slot / L.es());
       break;
     }
     default:
       nchw_to_nhwc_kernel<float><<<g, 256, 0, s>>>((const float*)in, N, C, H, W, L.hh, L.hw, L.hp(), L.wp(), L.c_phys,
-                                                   (float)fill, (float*)out);
+                                                   (float)fill, (float*)out, L.row() / L.es(), L.pair_slot / L.es());
   }
   count_launch();
   QNB_CUDA(cudaGetLastError());

@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "qnb_device.cuh"
@@ -37,14 +38,14 @@ constexpr int kMaxChunkSmem = 2048;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (5 + kEpiWarps) * 32;  // 4 producer warps, 1 MMA warp, 8 epilogue warps
 
-__host__ __device__ inline int igemm_stages(int n_rows) {
-  const int per = kStageA + n_rows * 128;
+__host__ __device__ inline int igemm_stages(int n_rows, int kbytes = 128) {
+  const int per = (kBM + n_rows) * kbytes;
   const int s = (200 * 1024) / per;
   return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
 }
-__host__ __device__ inline size_t igemm_smem_bytes(int n_rows) {
-  return 1024 + (size_t)igemm_stages(n_rows) * (kStageA + (size_t)n_rows * 128) + (2 * kMaxStages + 4) * 8 + 16 + 256 +
-         2 * 128 * 8 + kMaxChunkSmem * 4;
+__host__ __device__ inline size_t igemm_smem_bytes(int n_rows, int kbytes = 128) {
+  return 1024 + (size_t)igemm_stages(n_rows, kbytes) * ((size_t)(kBM + n_rows) * kbytes) + (2 * kMaxStages + 4) * 8 +
+         16 + 256 + 2 * 128 * 8 + kMaxChunkSmem * 4;
 }
 
 struct TileCoord {
@@ -76,53 +77,95 @@ __device__ __forceinline__ int64_t requant_fast(int32_t acc, const Requant& rq) 
 // ---------------------------------------------------------------- epilogue
 // Per-element tails, specialised per layer so the per-element code is branch-free.
 struct Q8Consts {
-  int64_t mult, half, mask;
-  int32_t s, oz, omin, omax;
-  int32_t rz, rsb, rsh, rzo, rmin, rmax;
-  int64_t rmult;
+  int64_t halfm1;  // 2^(s-1) - 1
+  int32_t mult32;  // rq.mult (< 2^31, host-proven)
+  int32_t s, sh;   // s = shift_bits + shift; sh = s - 32 (HI form, s >= 32)
+  int32_t oz, omin, omax;
 };
 
-// requant_clamp (fast form, see requant_fast) followed by the truncating INT8 ReLU
-// requant (src/ops.cpp:156-181) with 32-bit Acctype wrap-around.
-template <bool RELU>
-__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const uint8_t* lut) {
-  const int64_t pr = (int64_t)acc * k.mult;
-  const int64_t t = pr + k.half;
-  int64_t q = t >> k.s;
-  if ((t & k.mask) == 0) q &= ~1LL;  // exact tie -> even
-  int32_t v = (int32_t)q + k.oz;
-  v = v < k.omin ? k.omin : (v > k.omax ? k.omax : v);
-  if constexpr (RELU) return lut[v];  // relu_quant of the 256 possible inputs, tabulated on the host
+__device__ __forceinline__ Q8Consts q8_consts(const Requant& rq) {
+  Q8Consts k;
+  k.s = rq.s;
+  k.sh = rq.s - 32;
+  k.mult32 = (int32_t)rq.mult;
+  k.halfm1 = (rq.s >= 1 && rq.s <= 62) ? (1LL << (rq.s - 1)) - 1 : 0;
+  k.oz = (int32_t)rq.out_zero;
+  k.omin = (int32_t)rq.out_min;
+  k.omax = (int32_t)rq.out_max;
+  return k;
+}
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// requant_clamp (src/quantizer.cpp:201-217) when the host proved |acc| < 2^31 and
+// mult < 2^31: P = acc * mult is one 32x32->64 multiply, and round-half-to-even at
+// bit s is floor((P + 2^(s-1) - 1 + lsb(floor(P / 2^s))) / 2^s) -- exact for every P,
+// ties included, with no compare.  HI (s >= 32): the quotient lives in the high word
+// (one funnel-free shift).  RELU: the truncating INT8 ReLU requant (src/ops.cpp:156-181)
+// of the 256 possible clamped values, tabulated on the host, read from shared memory.
+// Truncating INT8 ReLU requant (src/ops.cpp:156-181) of a clamped conv output v in
+// [0, 255]: d = max(v - in_zero, 0); reg = (d * mult) >> shift_bits; reg >>= shift (or
+// <<= -shift); out = clamp(reg + out_zero).  The host proved (relu_fast_ok) that no
+// stage reaches the 32-bit Acctype wrap, so the two floor shifts run on 32/64-bit
+// unsigned values.  (A 256-entry smem table was 1 shared wavefront per distinct byte:
+// ~27 per warp load -- the arithmetic form is cheaper.)
+struct ReluFastK {
+  int32_t zin;
+  uint32_t mult;
+  int32_t sb, rs, ls, zout, omin, omax;
+};
+__device__ __forceinline__ ReluFastK relu_fast_consts(const ReluRequant& r) {
+  ReluFastK k;
+  k.zin = (int32_t)r.in_zero;
+  k.mult = (uint32_t)r.mult;
+  k.sb = r.shift_bits;
+  k.rs = r.shift >= 0 ? r.shift : 0;
+  k.ls = r.shift < 0 ? -r.shift : 0;
+  k.zout = (int32_t)r.out_zero;
+  k.omin = (int32_t)r.out_min;
+  k.omax = (int32_t)r.out_max;
+  return k;
+}
+__device__ __forceinline__ uint32_t relu_fast(int32_t v, const ReluFastK& r) {
+  const uint32_t d = (uint32_t)max(v - r.zin, 0);
+  uint32_t t = (uint32_t)(((uint64_t)d * r.mult) >> r.sb);
+  t = (t >> r.rs) << r.ls;
+  return (uint32_t)min(max((int32_t)t + r.zout, r.omin), r.omax);
+}
+
+template <bool RELU, bool HI>
+__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk) {
+  const int64_t pr = (int64_t)acc * (int64_t)k.mult32;
+  int32_t v;
+  if constexpr (HI) {
+    const uint32_t b = ((uint32_t)(pr >> 32) >> k.sh) & 1u;
+    const int64_t t = pr + k.halfm1 + (int64_t)b;
+    v = ((int32_t)(t >> 32) >> k.sh) + k.oz;
+    v = min(max(v, k.omin), k.omax);
+  } else {
+    const int64_t b = (pr >> k.s) & 1;
+    int64_t q = ((pr + k.halfm1 + b) >> k.s) + k.oz;
+    q = q < k.omin ? k.omin : (q > k.omax ? k.omax : q);
+    v = (int32_t)q;
+  }
+  if constexpr (RELU) return relu_fast(v, rk);
   return (uint32_t)v;
 }
 
-template <int MODE>
+template <int MODE, bool HI = false>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
                                                uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
                                                int64_t ncl, int cs, int rank, int warp, int lane, uint8_t* lut) {
-  if constexpr (MODE == EPIM_Q8_FAST_RELU) {
-    const int et = threadIdx.x - 5 * 32;  // 0 .. 255 across the epilogue warps
-    lut[et] = p.relu_lut[et];
-    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-  }
+  (void)lut;
+  const ReluFastK lut_s = relu_fast_consts(p.relu);
   const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
   const int half = (warp - 5) >> 2;  // which 16-column blocks of the tile
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
-  Q8Consts k;
-  k.mult = p.rq.mult;
-  k.s = p.rq.s;
-  k.half = (MODE == EPIM_Q8_FAST || MODE == EPIM_Q8_FAST_RELU) ? (1LL << (p.rq.s - 1)) : 0;
-  k.mask = (k.half << 1) - 1;
-  k.oz = (int32_t)p.rq.out_zero;
-  k.omin = (int32_t)p.rq.out_min;
-  k.omax = (int32_t)p.rq.out_max;
-  k.rz = (int32_t)p.relu.in_zero;
-  k.rmult = p.relu.mult;
-  k.rsb = p.relu.shift_bits;
-  k.rsh = p.relu.shift;
-  k.rzo = (int32_t)p.relu.out_zero;
-  k.rmin = (int32_t)p.relu.out_min;
-  k.rmax = (int32_t)p.relu.out_max;
+  const Q8Consts k = q8_consts(p.rq);
   const int n_tiles = p.n_tiles, n_real = p.n_real, npt = p.n_per_tile, tcols = p.tmem_cols;
   const int ones_col = p.ones_col, o_es = p.o_es, o_vec = p.o_vec, has_relu = p.has_relu;
   const int64_t zw = p.zw;
@@ -137,15 +180,39 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     const uint32_t buf = j & 1;
     mbar_wait(&acc_full[buf], (j >> 1) & 1);
     tc_fence_after();
+    if (p.dbg & 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      continue;
+    }
     const uint32_t trow = tmem + buf * (uint32_t)tcols + ((uint32_t)(32 * quarter) << 16);
-    const int64_t row = mt * kBM + 32 * quarter + lane;
-    const bool ok = row < p.m_total;
+    int64_t row = mt * kBM + 32 * quarter + lane;
+    bool ok;
     uint8_t* obase = p.out;
-    if (ok) {
-      const int64_t img = row / pix_per_img;
-      const int64_t rem = row - img * pix_per_img;
-      const int64_t oy = rem / p.ow, ox = rem - oy * p.ow;
-      obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+    if (p.patch) {  // padded-grid pixel P -> (image, oy, ox); grid cells outside the output are dropped
+      const uint32_t P = (uint32_t)(mt * kBM) + 32 * quarter + lane;
+      const uint32_t Y = P / (uint32_t)p.pt_wp, X = P - Y * (uint32_t)p.pt_wp;
+      const uint32_t img = Y / (uint32_t)p.pt_hp, oy = Y - img * (uint32_t)p.pt_hp;
+      ok = X < (uint32_t)p.ow && oy < (uint32_t)p.oh && (int64_t)img * pix_per_img < p.m_total;
+      if (ok) obase = p.out + (int64_t)img * p.o_img + (int64_t)oy * p.o_row + (int64_t)X * p.o_pix + p.o_origin;
+      row = 0;
+    } else if (p.hk) {  // row-Hankel tile: output row oy of images 2q and 2q+1, 64 M rows each
+      const int r = 32 * quarter + lane;
+      const uint32_t q = (uint32_t)mt / (uint32_t)p.oh;  // tile = (image pair q, output row oy)
+      const int64_t oy = (uint32_t)mt - q * (uint32_t)p.oh, ox = r & 63;
+      const int64_t img = 2 * (int64_t)q + (r >> 6);
+      ok = ox < p.ow && img * pix_per_img < p.m_total;
+      if (ok) obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+      row = 0;  // (split-K is never combined with hk)
+    } else {
+      ok = row < p.m_total;
+      if (ok) {  // 32-bit divisions: m_total < 2^31 (host-checked)
+        const uint32_t img = (uint32_t)row / (uint32_t)pix_per_img;
+        const uint32_t rem = (uint32_t)row - img * (uint32_t)pix_per_img;
+        const uint32_t oy = rem / (uint32_t)p.ow, ox = rem - oy * (uint32_t)p.ow;
+        obase = p.out + img * p.o_img + oy * p.o_row + ox * p.o_pix + p.o_origin;
+      }
     }
     if constexpr (MODE == EPIM_RAW32) {
       int32_t* wrow = p.ws + (((int64_t)ks * p.m_total + row) * n_tiles + c.nt) * p.n_rows;
@@ -208,10 +275,65 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     const int n0 = c.nt * npt;
     const int n_here = min(npt, n_real - n0);
     const int ch0 = c.g * n_real + n0;
+    if constexpr (MODE == EPIM_Q8_FAST || MODE == EPIM_Q8_FAST_RELU) {
+      if (o_vec && (n_here & 15) == 0 && !(p.dbg & 8)) {
+        // Software-pipelined drain: the TMEM load and the per-channel constants of the
+        // next 16-column block are in flight while this block is requantized.
+        constexpr bool RELU = MODE == EPIM_Q8_FAST_RELU;
+        const int4* ccp = reinterpret_cast<const int4*>(p.chan_const32 + ch0);
+        uint32_t r0[16], r1[16];
+        int4 c0[4], c1[4];
+        auto issue = [&](int cb, uint32_t (&r)[16], int4 (&cc)[4]) {
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) cc[qd] = __ldg(ccp + (cb >> 2) + qd);
+          tmem_ld16(trow + (uint32_t)cb, r);
+        };
+        auto process = [&](int cb, const uint32_t (&r)[16], const int4 (&cc)[4]) {
+          if (!ok) return;
+          uint32_t w[4];
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) {
+            const uint32_t b0 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 0] + cc[qd].x + rowterm32, k, lut_s);
+            const uint32_t b1 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 1] + cc[qd].y + rowterm32, k, lut_s);
+            const uint32_t b2 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 2] + cc[qd].z + rowterm32, k, lut_s);
+            const uint32_t b3 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 3] + cc[qd].w + rowterm32, k, lut_s);
+            w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+          }
+          *reinterpret_cast<uint4*>(obase + (int64_t)(ch0 + cb)) = make_uint4(w[0], w[1], w[2], w[3]);
+        };
+        int cb = half * 16;
+        if (cb < n_here) issue(cb, r0, c0);
+        for (; cb < n_here; cb += 64) {
+          const int cb1 = cb + 32;
+          tmem_ld_wait(r0);
+          if (cb1 < n_here) issue(cb1, r1, c1);
+          process(cb, r0, c0);
+          if (cb1 >= n_here) break;
+          tmem_ld_wait(r1);
+          if (cb1 + 32 < n_here) issue(cb1 + 32, r0, c0);
+          process(cb1, r1, c1);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        continue;
+      }
+    }
     for (int cb = half * 16; cb < n_here; cb += 32) {
       uint32_t r[16];
       tmem_ld16(trow + (uint32_t)cb, r);
       tmem_ld_wait();
+      if ((p.dbg & 8) && p.ws && cid == 0 && j == 0) {  // debug: raw accumulators of the first tile
+        int32_t* d = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(p.ws) + 2 * p.pt_plane + p.n_rows * 128);
+        const int m = 32 * quarter + lane;
+        for (int i = 0; i < 16; ++i) d[m * p.n_rows + cb + i] = (int32_t)r[i];
+        if (cb == half * 16) {
+          uint32_t v1;
+          tmem_ld1(trow + (uint32_t)ones_col, v1);
+          tmem_ld_wait();
+          d[m * p.n_rows + ones_col] = (int32_t)v1;
+        }
+      }
       if (!ok) continue;
       const int cnt = min(16, n_here - cb);
       uint8_t* dst = obase + (int64_t)(ch0 + cb) * o_es;
@@ -223,10 +345,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int qd = 0; qd < 4; ++qd) {
             const int4 cc = __ldg(cc4 + qd);
-            const uint32_t b0 = q8_fast<RELU>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut);
-            const uint32_t b1 = q8_fast<RELU>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut);
-            const uint32_t b2 = q8_fast<RELU>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut);
-            const uint32_t b3 = q8_fast<RELU>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut);
+            const uint32_t b0 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut_s);
+            const uint32_t b1 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut_s);
+            const uint32_t b2 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut_s);
+            const uint32_t b3 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut_s);
             w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           if (o_vec) {
@@ -239,7 +361,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (i < cnt)
-              dst[i] = (uint8_t)q8_fast<RELU>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut);
+              dst[i] = (uint8_t)q8_fast<RELU, HI>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut_s);
         }
       } else if constexpr (MODE == EPIM_Q8_EXACT) {
 #pragma unroll
@@ -289,10 +411,12 @@ template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constant__ IgemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int S = igemm_stages(p.n_rows);
-  const int b_stage = p.n_rows * 128;
+  const int kbytes = p.kbytes;
+  const int S = igemm_stages(p.n_rows, kbytes);
+  const int a_stage = kBM * kbytes;
+  const int b_stage = p.n_rows * kbytes;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)S * kStageA;
+  uint8_t* sB = smem + (size_t)S * a_stage;
   uint64_t* full = (uint64_t*)(sB + (size_t)S * b_stage);
   uint64_t* empty = full + kMaxStages;
   uint64_t* acc_full = empty + kMaxStages;
@@ -321,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 129);  // 128 cp.async arrivals + 1 expect_tx arrival
+      mbar_init(&full[i], p.a_tma ? 1 : 129);  // TMA: 1 expect_tx arrival; else + 128 cp.async arrivals
       mbar_init(&empty[i], (uint32_t)cs);  // one MMA commit per CTA of the cluster
     }
     for (int i = 0; i < 2; ++i) {
@@ -340,7 +464,41 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
+  if (warp < 4 && p.a_tma) {
+    // ------------------------------------------------------- TMA im2col producer
+    // One thread: per K stage one im2col tensor load (128 output pixels x kbytes of
+    // one tap's channels, hardware-swizzled) + the B stage bulk copy.
+    if (threadIdx.x == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_a)) : "memory");
+      uint32_t it = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        const TileCoord c = tile_of(ct, m_groups, p.n_tiles * p.ksplit);
+        const int64_t mt = c.mt * cs + rank;
+        const uint32_t row0 = (uint32_t)(mt * kBM);
+        const uint32_t img = row0 / (uint32_t)pix_per_img;
+        const uint32_t rem = row0 - img * (uint32_t)pix_per_img;
+        const uint32_t oy = rem / (uint32_t)p.ow, ox = rem - oy * (uint32_t)p.ow;
+        const int w0 = (int)(ox * p.stride_w), h0 = (int)(oy * p.stride_h);
+        const int cg0 = c.g * (int)p.a_group;  // group channel offset (elements)
+        const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + ntile) * p.num_kb * b_stage;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = (int)(it % S);
+          mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(a_stage + b_stage));
+          const int32_t* st = chunk_tab + kb * 8;  // {c0, s, r}
+          tma_im2col_4d(sA + (size_t)s * a_stage, &p.tmap_a, cg0 + st[0], w0, h0, (int)img, (uint16_t)st[1],
+                        (uint16_t)st[2], &full[s]);
+          if (cs == 1)
+            bulk_g2s(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s]);
+          else if (rank == 0)
+            bulk_g2s_multicast(sB + (size_t)s * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &full[s],
+                               cmask);
+        }
+      }
+    }
+  } else if (warp < 4) {
     // ---------------------------------------------------------------- producers
     // Coalesced gather: lane l copies chunk (l & 7) of rows w*32 + (l >> 3) + 4*i,
     // i = 0..7, so the 8 lanes of a row fetch its 128 contiguous K bytes together.
@@ -354,9 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         const int64_t row = mt * kBM + t;
         int64_t off = -1;
         if (row < p.m_total) {
-          const int64_t img = row / pix_per_img;
-          const int32_t rem = (int32_t)(row - img * pix_per_img);
-          const int32_t oy = rem / p.ow, ox = rem - oy * p.ow;
+          const uint32_t img = (uint32_t)row / (uint32_t)pix_per_img;
+          const uint32_t rem = (uint32_t)row - img * (uint32_t)pix_per_img;
+          const uint32_t oy = rem / (uint32_t)p.ow, ox = rem - oy * (uint32_t)p.ow;
           off = img * p.a_img + (int64_t)oy * p.stride_h * p.a_row + (int64_t)ox * p.stride_w * p.a_pix +
                 (int64_t)c.g * p.a_group + p.a_origin;
         }
@@ -386,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
                                cmask);
         }
         const int32_t off = chunk_tab[kb * 8 + jc];
-        uint8_t* dst = sA + (size_t)s * kStageA;
+        uint8_t* dst = sA + (size_t)s * a_stage;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int row = warp * 32 + rr + 4 * i;
@@ -397,8 +555,12 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     }
   } else if (warp == 4) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // The whole warp runs the loop (uniform registers, no per-MMA broadcast); one
+    // elected lane issues each tcgen05 instruction.
+    {
       const uint32_t idesc = make_idesc<KIND>(p.n_rows);
+      const bool mma_on = !(p.dbg & 2);
+      const int nk = kbytes >> 5;
       uint32_t it = 0, j = 0;
       for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
         const uint32_t buf = j & 1;
@@ -411,27 +573,36 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
           const int s = (int)(it % S);
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw128(sA + (size_t)s * kStageA);
-          const uint64_t bd = smem_desc_sw128(sB + (size_t)s * b_stage);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) umma<KIND>(dt, ad + 2 * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
-          if (cs == 1)
-            tc_commit(&empty[s]);
-          else
-            tc_commit_multicast(&empty[s], cmask);
+          const uint64_t ad = smem_desc_sw(sA + (size_t)s * a_stage, kbytes);
+          const uint64_t bd = smem_desc_sw(sB + (size_t)s * b_stage, kbytes);
+          if (elect_one()) {
+            if (mma_on)
+              for (int k = 0; k < nk; ++k) umma<KIND>(dt, ad + 2 * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
+            if (cs == 1)
+              tc_commit(&empty[s]);
+            else
+              tc_commit_multicast(&empty[s], cmask);
+          }
+          __syncwarp();
         }
-        tc_commit(&acc_full[buf]);
+        if (elect_one()) tc_commit(&acc_full[buf]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
     // ---------------------------------------------------------------- epilogue
     switch (p.epi_mode) {
       case EPIM_Q8_FAST_RELU:
-        epilogue_tiles<EPIM_Q8_FAST_RELU>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+        if (p.rq.s >= 32)
+          epilogue_tiles<EPIM_Q8_FAST_RELU, true>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+        else
+          epilogue_tiles<EPIM_Q8_FAST_RELU, false>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       case EPIM_Q8_FAST:
-        epilogue_tiles<EPIM_Q8_FAST>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+        if (p.rq.s >= 32)
+          epilogue_tiles<EPIM_Q8_FAST, true>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+        else
+          epilogue_tiles<EPIM_Q8_FAST, false>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
         break;
       case EPIM_Q8_EXACT:
         epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
@@ -457,6 +628,529 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     tc_fence_after();
     tmem_dealloc(tmem, (uint32_t)(2 * p.tmem_cols));
   }
+}
+
+
+// ---------------------------------------------------------------- row-Hankel kernel
+// Small-channel strided convolutions (AlexNet conv1: C = 3 -> 4 padded, stride 4,
+// 11 x 11).  With c_phys * stride_w == 16 bytes, output pixel m of an input row reads
+// the K bytes [16 m, 16 m + kw * c_phys) of that row: consecutive pixels are 16 bytes
+// apart, which is exactly the row pitch of a non-swizzled K-major UMMA core matrix.
+// So the A operand is the raw input row in smem, addressed with LBO = 16 (next 16 K
+// bytes) and SBO = 128 (next 8 pixels): the im2col expansion (11 x per input byte for
+// conv1) never exists, in HBM, L2 or smem.  Per tile (two output rows): 2 x kh bulk
+// row copies, kh x kpr/32 MMAs against the resident B.
+//   warp 0 (lane 0)  producer: B once, then per tile the 2 x kh input rows
+//   warp 4           TMEM allocator + MMA issuer
+//   warps 5-12       epilogue (shared with the general kernel)
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) igemm_hk_kernel(const __grid_constant__ IgemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int b_stage = p.n_rows * 128;
+  const int b_bytes = p.num_kb * b_stage;
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + ((b_bytes + 1023) & ~1023);
+  const int a_tile = (p.hk_copy + 64 + 127) & ~127;  // + slack: the last pixels' K overrun meets zero weights
+  uint64_t* b_full = (uint64_t*)(sA + 2 * a_tile);
+  uint64_t* a_full = b_full + 1;
+  uint64_t* a_empty = a_full + 2;
+  uint64_t* acc_full = a_empty + 2;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+  uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)p.hk_pairs * p.oh;  // tile = (image pair, output row)
+
+  if (threadIdx.x == 0) {
+    mbar_init(b_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc(tmem_slot, (uint32_t)(2 * p.tmem_cols));
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(b_full, (uint32_t)b_bytes);
+      for (int kb = 0; kb < p.num_kb; ++kb)
+        bulk_g2s(sB + (size_t)kb * b_stage, p.b + (size_t)kb * b_stage, (uint32_t)b_stage, b_full);
+      uint32_t j = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+        const uint32_t buf = j & 1;
+        mbar_wait(&a_empty[buf], ((j >> 1) & 1) ^ 1);
+        const uint32_t q = (uint32_t)t / (uint32_t)p.oh, oy = (uint32_t)t - q * (uint32_t)p.oh;
+        mbar_arrive_expect_tx(&a_full[buf], (uint32_t)p.hk_copy);
+        bulk_g2s(sA + (size_t)buf * a_tile, p.a + (int64_t)q * p.a_img + p.a_origin + (int64_t)oy * p.stride_h * p.a_row,
+                 (uint32_t)p.hk_copy, &a_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    {  // whole warp: uniform loop, elected issue
+      const uint32_t idesc = make_idesc<KIND>(p.n_rows);
+      const bool mma_on = !(p.dbg & 2);
+      mbar_wait(b_full, 0);
+      const int ksteps = p.hk_kpr / 32;
+      const uint64_t bd0 = smem_desc_sw128(sB);
+      const uint32_t b_units = (uint32_t)(b_stage >> 4);
+      uint32_t j = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+        const uint32_t buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&a_full[buf], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
+        // M rows 0-63: image 2q, pixel m at 16 m; rows 64-127: image 2q+1 (+1024)
+        const uint64_t ad0 = smem_desc_none(sA + (size_t)buf * a_tile, 16, 128);
+        if (elect_one()) {
+          if (mma_on)
+            for (int r = 0; r < p.hk_rows; ++r)
+              for (int q = 0; q < ksteps; ++q) {
+                const uint32_t kk = (uint32_t)(r * p.hk_kpr + q * 32);  // K byte in the packed B order
+                umma<KIND>(dt, ad0 + (uint32_t)((r * p.a_row + q * 32) >> 4),
+                           bd0 + (kk >> 7) * b_units + 2 * ((kk & 127) >> 5), idesc, (r | q) != 0);
+              }
+          tc_commit(&a_empty[buf]);
+          tc_commit(&acc_full[buf]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 5) {
+    switch (p.epi_mode) {
+      case EPIM_Q8_FAST_RELU:
+        if (p.rq.s >= 32)
+          epilogue_tiles<EPIM_Q8_FAST_RELU, true>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
+        else
+          epilogue_tiles<EPIM_Q8_FAST_RELU, false>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
+        break;
+      case EPIM_Q8_FAST:
+        if (p.rq.s >= 32)
+          epilogue_tiles<EPIM_Q8_FAST, true>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
+        else
+          epilogue_tiles<EPIM_Q8_FAST, false>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
+        break;
+      default:
+        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, (uint32_t)(2 * p.tmem_cols));
+  }
+}
+
+// Driver-API entry points resolved through the runtime (no link-time libcuda
+// dependency: libqnb.so must load on hosts without a driver, where every compute call
+// then fails with QNB_E_CUDA).
+template <typename F>
+static F driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(fn);
+}
+
+// ---------------------------------------------------------------- TMA im2col A
+bool igemm_tma_eligible(const IgemmGeometry& g, const ActLayout& in) {
+  if (g.q16 || g.is_fc || in.pair_slot != 0) return false;
+  const int64_t es = in.es();
+  if ((g.cg * es) % 16 != 0 || in.pix() % 16 != 0 || in.row() % 16 != 0 || in.img() % 16 != 0) return false;
+  if (((in.hh - g.ph) * in.row() + (in.hw - g.pw) * in.pix()) % 16 != 0) return false;
+  if (in.hh < g.ph || in.hw < g.pw) return false;
+  if (g.sh < 1 || g.sh > 8 || g.sw < 1 || g.sw > 8 || g.kh > 128 || g.kw > 128) return false;
+  if (g.kh != g.kw) return false;  // corner order independent (square filters only)
+  return true;
+}
+
+qnb_status igemm_plan_tma(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk) {
+  const int64_t es = in.es(), cgb = g.cg * es;
+  // stage width: the swizzle span that wastes the fewest K bytes per tap (ties: wider)
+  int kb = 128;
+  int64_t best = ceil_div(cgb, 128) * 128;
+  for (int cand : {64, 32}) {
+    const int64_t w = ceil_div(cgb, cand) * cand;
+    if (w < best) {
+      best = w;
+      kb = cand;
+    }
+  }
+  pk->kbytes = kb;
+  const int64_t per = kb / es;  // channels per stage
+  std::vector<int32_t> off;
+  std::vector<int64_t> kmap;
+  for (int64_t r = 0; r < g.kh; ++r)
+    for (int64_t s = 0; s < g.kw; ++s)
+      for (int64_t c0 = 0; c0 < g.cg; c0 += per) {
+        off.push_back((int32_t)c0);
+        off.push_back((int32_t)s);
+        off.push_back((int32_t)r);
+        for (int i = 0; i < 5; ++i) off.push_back(0);
+        for (int64_t e = 0; e < per; ++e) {
+          const int64_t c = c0 + e;
+          kmap.push_back(c < g.cg ? (c * g.kh + r) * g.kw + s : -1);
+        }
+      }
+  pk->chunk_off = std::move(off);
+  pk->kmap = std::move(kmap);
+  pk->num_kb = (int32_t)(pk->chunk_off.size() / 8);
+  return QNB_OK;
+}
+
+qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base, int32_t kbytes,
+                            CUtensorMap* map) {
+  const int64_t es = in.es();
+  const CUtensorMapDataType dt =
+      es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : (es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  // the tensor is the padded activation seen from the conv's own padding origin
+  const uint8_t* base = a_base + (in.hh - g.ph) * in.row() + (in.hw - g.pw) * in.pix();
+  const int64_t W = in.w + 2 * g.pw, H = in.h + 2 * g.ph;
+  const cuuint64_t dims[4] = {(cuuint64_t)in.c_phys, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)in.n};
+  const cuuint64_t strides[3] = {(cuuint64_t)in.pix(), (cuuint64_t)in.row(), (cuuint64_t)in.img()};
+  const int lower[2] = {0, 0};
+  const int upper[2] = {(int)-(g.kw - 1), (int)-(g.kh - 1)};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g.sw, (cuuint32_t)g.sh, 1};
+  const CUtensorMapSwizzle sw = kbytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                              : (kbytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  using EncodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static const EncodeIm2col encode = driver_fn<EncodeIm2col>("cuTensorMapEncodeIm2col");
+  if (!encode) return fail(QNB_E_CUDA, "cuTensorMapEncodeIm2col unavailable (driver too old?)");
+  const CUresult r = encode(map, dt, 4, (void*)base, dims, strides, lower, upper, (cuuint32_t)(kbytes / es),
+                            (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(QNB_E_CUDA, "cuTensorMapEncodeIm2col failed: " + std::to_string((int)r));
+  return QNB_OK;
+}
+
+
+// ---------------------------------------------------------------- patch kernel
+// Stride-1 convolutions (AlexNet conv2-5, VGG-16): see IgemmArgs::patch.
+//   warps 0-3       producers: per tile and channel-block pair, the two 16-byte
+//                   channel-block planes of the patch by cp.async (ring of kPatchStages
+//                   A stages); B stages (4 K steps = 128 B of K, SW128) stream through
+//                   their own ring (thread 0, bulk copies)
+//   warp 4          TMEM allocator + MMA issuer: per A stage kh*kw taps -> MMAs
+//   warps 5-12      epilogue (shared)
+constexpr int kPatchStages = 4;
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_constant__ IgemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int b_stage = p.n_rows * 128;
+  const int a_stage = 2 * p.pt_plane;
+  const bool bstat = p.pt_bstat != 0;
+  const int SB = bstat ? p.num_kb : p.kb_per_split;  // resident B, or the B ring depth
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (((size_t)kPatchStages * a_stage + 1023) & ~(size_t)1023);  // SW128 B needs 1024-B atoms
+  uint64_t* a_full = (uint64_t*)(sB + (size_t)SB * b_stage);
+  uint64_t* a_empty = a_full + kPatchStages;
+  uint64_t* b_full = a_empty + kPatchStages;
+  uint64_t* b_empty = b_full + kMaxStages;
+  uint64_t* acc_full = b_empty + kMaxStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
+  uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t grid_pix = (p.m_total / ((int64_t)p.oh * p.ow)) * p.pt_hp * p.pt_wp;
+  const int64_t m_tiles = (grid_pix + kBM - 1) / kBM;
+  const int taps = p.pt_kh * p.pt_kw;
+  // Tile walk, in tile_of's linear index (m fastest):
+  //   streamed B:   ct = blockIdx.x, +gridDim.x, ... < m_tiles * n_tiles * groups
+  //   resident B:   combination cmb = blockIdx.x % combos owns ct in [cmb*m_tiles, (cmb+1)*m_tiles)
+  int64_t ct0, ct_step, ct_end;
+  if (bstat) {
+    const int combos = p.n_tiles * p.groups;
+    const int cmb = blockIdx.x % combos, per = gridDim.x / combos;
+    ct0 = (int64_t)cmb * m_tiles + blockIdx.x / combos;
+    ct_step = per;
+    ct_end = (int64_t)(cmb + 1) * m_tiles;
+  } else {
+    ct0 = blockIdx.x;
+    ct_step = gridDim.x;
+    ct_end = m_tiles * p.n_tiles * p.groups;
+  }
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPatchStages; ++i) {
+      mbar_init(&a_full[i], 128);  // one cp.async arrival per producer thread
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < kMaxStages; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc(tmem_slot, (uint32_t)(2 * p.tmem_cols));
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // 128 producer threads: per (tile, channel-block pair) the tile's input patch as two
+    // [pixel][16 B] planes -- chunk i = (pixel i/2, block i%2), so each pair of lanes
+    // reads one pixel's 32 contiguous bytes; thread 0 also moves B (once if resident).
+    const int t = threadIdx.x;
+    const int64_t y_tot = (p.m_total / ((int64_t)p.oh * p.ow)) * p.pt_hp;  // rows of the merged N*H_p grid
+    const int chunks = 2 * p.pt_rows * p.pt_wp;
+    if (bstat && t == 0 && ct0 < ct_end) {
+      const TileCoord c = tile_of(ct0, m_tiles, p.n_tiles);
+      const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
+      mbar_arrive_expect_tx(&b_full[0], (uint32_t)(p.num_kb * b_stage));
+      for (int kb = 0; kb < p.num_kb; ++kb)
+        bulk_g2s(sB + (size_t)kb * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &b_full[0]);
+    }
+    uint32_t ia = 0, ib = 0;
+    for (int64_t ct = ct0; ct < ct_end; ct += ct_step) {
+      const TileCoord c = tile_of(ct, m_tiles, p.n_tiles);
+      const uint32_t P0 = (uint32_t)(c.mt * kBM);
+      const uint32_t y0 = P0 / (uint32_t)p.pt_wp;
+      const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
+      int kb = 0;
+      for (int j = 0; j < p.pt_pairs; ++j, ++ia) {
+        const int s = (int)(ia % kPatchStages);
+        mbar_wait(&a_empty[s], ((ia / kPatchStages) & 1) ^ 1);
+        const int64_t cbyte = (int64_t)(c.g * p.pt_nblk + 2 * j) * 16;  // first block of the pair
+        uint8_t* dst = sA + (size_t)s * a_stage;
+        for (int i = t; i < chunks; i += 128) {
+          const uint32_t q = (uint32_t)i >> 1, b = (uint32_t)i & 1u;
+          const uint32_t dy = q / (uint32_t)p.pt_wp, x = q - dy * (uint32_t)p.pt_wp;
+          int64_t y = (int64_t)y0 + dy;
+          y = y < y_tot ? y : y_tot - 1;  // rows past the last image only feed discarded outputs
+          cp_async_16(dst + b * p.pt_plane + q * 16, p.a + y * p.a_row + (int64_t)x * p.a_pix + cbyte + b * 16);
+        }
+        cp_async_arrive_noinc(&a_full[s]);
+        if (!bstat && t == 0) {
+          const int kb_end = ((j + 1) * taps + 3) / 4;
+          for (; kb < kb_end && kb < p.num_kb; ++kb, ++ib) {
+            const int sb = (int)(ib % SB);
+            mbar_wait(&b_empty[sb], ((ib / SB) & 1) ^ 1);
+            mbar_arrive_expect_tx(&b_full[sb], (uint32_t)b_stage);
+            bulk_g2s(sB + (size_t)sb * b_stage, btile + (int64_t)kb * b_stage, (uint32_t)b_stage, &b_full[sb]);
+          }
+        }
+      }
+    }
+  } else if (warp == 4) {
+    {  // whole warp: uniform loop, elected issue; descriptors advance by adding 16-B units
+      const uint32_t idesc = make_idesc<KIND>(p.n_rows);
+      const bool mma_on = !(p.dbg & 2);
+      if (bstat) {
+        mbar_wait(&b_full[0], 0);
+        tc_fence_after();
+      }
+      const uint32_t b_units = (uint32_t)(b_stage >> 4);
+      const uint32_t wp = (uint32_t)p.pt_wp;
+      uint32_t ia = 0, ib = 0, j_t = 0;
+      for (int64_t ct = ct0; ct < ct_end; ct += ct_step, ++j_t) {
+        const TileCoord c = tile_of(ct, m_tiles, p.n_tiles);
+        const uint32_t P0 = (uint32_t)(c.mt * kBM);
+        const uint32_t off0 = P0 - (P0 / wp) * wp;  // tile start inside row y0
+        const uint32_t buf = j_t & 1;
+        mbar_wait(&acc_empty[buf], ((j_t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
+        int k = 0;  // K step within the tile
+        for (int j = 0; j < p.pt_pairs; ++j, ++ia) {
+          const int s = (int)(ia % kPatchStages);
+          mbar_wait(&a_full[s], (ia / kPatchStages) & 1);
+          tc_fence_after();
+          const uint64_t ad0 = smem_desc_none(sA + (size_t)s * a_stage, (uint32_t)p.pt_plane, 128) + off0;
+          if (bstat) {
+            const uint64_t bd0 = smem_desc_sw128(sB);
+            if (elect_one()) {
+              int kk = k;
+              if (mma_on)
+                for (int r = 0; r < p.pt_kh; ++r)
+                  for (int t = 0; t < p.pt_kw; ++t, ++kk)
+                    umma<KIND>(dt, ad0 + (uint32_t)(r * wp + t), bd0 + (uint32_t)(kk >> 2) * b_units + 2 * (kk & 3),
+                               idesc, kk != 0);
+              tc_commit(&a_empty[s]);
+            }
+            __syncwarp();
+            k += p.pt_kh * p.pt_kw;
+          } else {
+            for (int r = 0; r < p.pt_kh; ++r)
+              for (int t = 0; t < p.pt_kw; ++t, ++k) {
+                const int sb = (int)(ib % SB);
+                if ((k & 3) == 0) {
+                  mbar_wait(&b_full[sb], (ib / SB) & 1);
+                  tc_fence_after();
+                }
+                const uint64_t bd = smem_desc_sw128(sB + (size_t)sb * b_stage) + 2 * (k & 3);
+                if (elect_one()) {
+                  if (mma_on) umma<KIND>(dt, ad0 + (uint32_t)(r * wp + t), bd, idesc, k != 0);
+                  if ((k & 3) == 3) tc_commit(&b_empty[sb]);
+                }
+                __syncwarp();
+                if ((k & 3) == 3) ++ib;
+              }
+            if (elect_one()) tc_commit(&a_empty[s]);
+            __syncwarp();
+          }
+        }
+        if (!bstat && (k & 3)) {  // partially used last B stage
+          if (elect_one()) tc_commit(&b_empty[(int)(ib % SB)]);
+          __syncwarp();
+          ++ib;
+        }
+        if (elect_one()) tc_commit(&acc_full[buf]);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 5) {
+    switch (p.epi_mode) {
+      case EPIM_Q8_FAST_RELU:
+        if (p.rq.s >= 32)
+          epilogue_tiles<EPIM_Q8_FAST_RELU, true>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        else
+          epilogue_tiles<EPIM_Q8_FAST_RELU, false>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        break;
+      case EPIM_Q8_FAST:
+        if (p.rq.s >= 32)
+          epilogue_tiles<EPIM_Q8_FAST, true>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        else
+          epilogue_tiles<EPIM_Q8_FAST, false>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        break;
+      case EPIM_Q8_EXACT:
+        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        break;
+      case EPIM_F16:
+        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        break;
+      case EPIM_Q16:
+        epilogue_tiles<EPIM_Q16>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+        break;
+      default:
+        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem, (uint32_t)(2 * p.tmem_cols));
+  }
+}
+
+static size_t igemm_patch_smem_bytes(const IgemmArgs& a, int sb) {
+  return 1024 + (((size_t)kPatchStages * 2 * a.pt_plane + 1023) & ~(size_t)1023) + (size_t)sb * a.n_rows * 128 +
+         (2 * kPatchStages + 2 * kMaxStages + 4) * 8 + 16 + 256;
+}
+
+bool igemm_patch_eligible(const IgemmGeometry& g, const ActLayout& in) {
+  if (g.q16 || g.is_fc || in.pair_slot != 0 || g.sh != 1 || g.sw != 1) return false;
+  const int64_t es = in.es();
+  if ((g.cg * es) % 16 != 0 || in.pix() % 16 != 0 || in.row() % 16 != 0 || in.img() != in.hp() * in.row()) return false;
+  if (in.hh != g.ph || in.hw != g.pw) return false;  // the halo is the conv's padding
+  const int64_t wp = in.w + 2 * g.pw;
+  if (wp > 256 || g.kh > 32 || g.kw > 32) return false;
+  const int64_t rows = (wp + kBM - 3 + g.kw) / wp + g.kh;
+  if (rows > 256) return false;
+  const int64_t plane = round_up(rows * wp * 16, 128);
+  if (2 * kPatchStages * (plane + 64) > 120 * 1024) return false;
+  return true;
+}
+
+qnb_status igemm_plan_patch(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* pairs_out) {
+  const int64_t es = in.es();
+  const int64_t per_blk = 16 / es;                  // channels per 16-byte block
+  const int64_t nblk = (g.cg * es) / 16;
+  const int64_t pairs = (nblk + 1) / 2;
+  std::vector<int64_t> kmap;
+  for (int64_t j = 0; j < pairs; ++j)
+    for (int64_t r = 0; r < g.kh; ++r)
+      for (int64_t s = 0; s < g.kw; ++s)
+        for (int64_t e = 0; e < 32 / es; ++e) {   // one K step: block 2j then block 2j+1
+          const int64_t blk = 2 * j + (e * es) / 16;
+          const int64_t c = blk * per_blk + (e * es % 16) / es;
+          kmap.push_back(c < g.cg ? (c * g.kh + r) * g.kw + s : -1);
+        }
+  while (kmap.size() % (size_t)(128 / es) != 0) kmap.push_back(-1);
+  pk->kmap = std::move(kmap);
+  pk->num_kb = (int32_t)(pk->kmap.size() / (size_t)(128 / es));
+  pk->chunk_off.assign((size_t)pk->num_kb * 8, 0);
+  pk->kbytes = 128;
+  *pairs_out = (int32_t)pairs;
+  return QNB_OK;
+}
+
+// Largest n-tile width (real output channels) whose whole B (num_kb stages of
+// round_up(npt + 1, 16) rows) fits in shared memory next to the patch ring; 0 = none.
+int igemm_patch_bstat_npt(const IgemmGeometry& g, int64_t num_kb, int32_t plane) {
+  const size_t a_bytes = ((size_t)kPatchStages * 2 * plane + 1023) & ~(size_t)1023;
+  for (int npt : {240, 192, 128, 112, 96, 64, 48, 32}) {
+    if (npt > round_up(g.og, 16) && npt != 32) continue;
+    const int64_t nrows = round_up(npt + 1, 16);
+    const size_t bytes = 1024 + a_bytes + (size_t)num_kb * nrows * 128 + 1024;
+    if (bytes <= 220 * 1024) return npt;
+  }
+  return 0;
+}
+
+static size_t igemm_hk_smem_bytes(const IgemmArgs& a) {
+  return 1024 + (size_t)(((a.num_kb * a.n_rows * 128) + 1023) & ~1023) + 2 * (size_t)((a.hk_copy + 64 + 127) & ~127) +
+         9 * 8 + 16 + 256;
+}
+
+bool hk_geometry_ok(const IgemmGeometry& g, const ActLayout& in) {
+  if (g.kind != KIND_I8 || g.q16 || g.is_fc || g.groups != 1) return false;
+  if (g.sw * in.pix() != 16 || in.es() != 1) return false;   // pixel pitch in the MMA row = 16 bytes
+  if (g.ow > 64) return false;                                 // one output row per 64-row M half
+  if (in.hh < g.ph || in.hw < g.pw) return false;
+  if (in.wp() * in.pix() > kHkSlot) return false;              // a row fits its slot
+  if (16 * (g.ow - 1) + g.kw * in.pix() > kHkSlot) return false;  // valid pixels read their own slot only
+  if (((in.hw - g.pw) * in.pix()) % 16 != 0) return false;
+  const int64_t kpr = round_up(g.kw * in.pix(), 32);
+  if (g.kh * kpr > 1024) return false;                         // B (<= 256 rows) stays resident
+  if (g.kh * 2 * kHkSlot > 64 * 1024) return false;            // two tile blocks in smem
+  return true;
+}
+
+bool igemm_hk_eligible(const IgemmGeometry& g, const ActLayout& in) {
+  return in.pair_slot == kHkSlot && hk_geometry_ok(g, in);
+}
+
+qnb_status igemm_plan_hk(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* kpr_out) {
+  const int64_t kpr = round_up(g.kw * in.pix(), 32);
+  std::vector<int64_t> kmap;
+  for (int64_t r = 0; r < g.kh; ++r)
+    for (int64_t b = 0; b < kpr; ++b) {
+      const int64_t s = b / in.pix(), c = b % in.pix();
+      kmap.push_back((s < g.kw && c < g.cg) ? (c * g.kh + r) * g.kw + s : -1);
+    }
+  while (kmap.size() % 128 != 0) kmap.push_back(-1);
+  pk->kmap = std::move(kmap);
+  pk->num_kb = (int32_t)(pk->kmap.size() / 128);
+  pk->chunk_off.assign((size_t)pk->num_kb * 8, 0);
+  *kpr_out = (int32_t)kpr;
+  return QNB_OK;
 }
 
 bool igemm_fast_requant_ok(const std::vector<int64_t>& chan_const, int64_t K, int64_t zw, const Requant& rq) {
@@ -633,8 +1327,14 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
 
   const int64_t K = g.is_fc ? g.fc_c * g.fc_h * g.fc_w : g.cg * g.kh * g.kw;
   const int64_t OC = g.groups * og;
-  const int64_t elems_per_stage = 128 / es;
-  const size_t stage_bytes = (size_t)n_rows * 128;
+  const int kbytes = pk->kbytes;
+  const int64_t elems_per_stage = kbytes / es;
+  const size_t stage_bytes = (size_t)n_rows * kbytes;
+  // K-major swizzle of a kbytes-wide row: 16-byte chunk j of row r lands at chunk
+  // j ^ f(r) (SWIZZLE_128B: r & 7, _64B: (r >> 1) & 3, _32B: (r >> 2) & 1).
+  auto swz = [kbytes](int64_t r) -> int64_t {
+    return kbytes == 128 ? (r & 7) : (kbytes == 64 ? ((r >> 1) & 3) : ((r >> 2) & 1));
+  };
   pk->b.assign((size_t)g.groups * n_tiles2 * pk->num_kb * stage_bytes, 0);
   const size_t wes = dtype_size(w_dtype);
   auto wval_f = [&](int64_t oc, int64_t k) -> float {
@@ -663,7 +1363,7 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
             const int64_t k = igemm_local_k(g, *pk, pk->kmap[(size_t)kk], gi);
             if (k < 0) continue;
             const int64_t byte = e * es;
-            const int64_t dst = r * 128 + (((byte >> 4) ^ (r & 7)) << 4) + (byte & 15);
+            const int64_t dst = r * kbytes + (((byte >> 4) ^ swz(r)) << 4) + (byte & 15);
             if (quant) {
               stage[dst] = ones ? 1 : wval_q(gi * og + o, k);
             } else if (g.kind == KIND_F16) {
@@ -687,14 +1387,7 @@ __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
   const int n_out = p.n_real;  // split-K serves the inner products (one group)
   const int quads = (n_out + 3) >> 2;
   const int64_t total = p.m_total * quads;
-  Q8Consts k;
-  k.mult = p.rq.mult;
-  k.s = p.rq.s;
-  k.half = FAST ? (1LL << (p.rq.s - 1)) : 0;
-  k.mask = (k.half << 1) - 1;
-  k.oz = (int32_t)p.rq.out_zero;
-  k.omin = (int32_t)p.rq.out_min;
-  k.omax = (int32_t)p.rq.out_max;
+  const Q8Consts k = q8_consts(p.rq);
   const int64_t row_stride = (int64_t)p.n_tiles * p.n_rows;
   const int64_t split_stride = p.m_total * row_stride;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -721,7 +1414,7 @@ __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
       if (u >= cnt) break;
       int64_t q;
       if constexpr (FAST) {
-        q = q8_fast<false>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, nullptr);
+        q = q8_fast<false, false>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, ReluFastK{});
       } else {
         q = requant_clamp((int64_t)d[u] + p.chan_const[o0 + u] - p.zw * (int64_t)rs, p.rq);
       }
@@ -760,16 +1453,82 @@ static int num_sms() {
   return n;
 }
 
+// Host proof for relu_fast: every stage of relu_quant stays below the INT8 Acctype
+// wrap (2^31) for all 256 inputs, so the device may use unsigned shifts.
+static bool relu_fast_ok(const ReluRequant& r) {
+  if (!r.acc32 || r.mult < 0 || r.mult >= (int64_t(1) << 32) || r.shift_bits < 0 || r.shift_bits > 62) return false;
+  if (r.in_zero < -(int64_t(1) << 30) || r.in_zero > (int64_t(1) << 30)) return false;
+  const int64_t tmax = (255 * r.mult) >> r.shift_bits;
+  if (tmax >= (int64_t(1) << 31)) return false;
+  if (r.shift < -31 || r.shift > 62) return false;
+  const int64_t t2 = r.shift >= 0 ? (tmax >> r.shift) : (tmax << -r.shift);
+  const int64_t az = r.out_zero < 0 ? -r.out_zero : r.out_zero;
+  return t2 + az < (int64_t(1) << 31) && r.out_min >= INT32_MIN && r.out_max <= INT32_MAX;
+}
+
+template <int KIND>
+static qnb_status launch_hk(const IgemmArgs& a, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    QNB_CUDA(cudaFuncSetAttribute(igemm_hk_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
+  const size_t smem = igemm_hk_smem_bytes(a);
+  if (smem > 227 * 1024) return fail(QNB_E_UNSUPPORTED, "row-Hankel tile exceeds shared memory");
+  const int64_t tiles = (int64_t)a.hk_pairs * a.oh;
+  const int64_t grid = std::min<int64_t>(tiles, num_sms());
+  igemm_hk_kernel<KIND><<<(unsigned)grid, kThreads, smem, s>>>(a);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
+template <int KIND>
+static qnb_status launch_patch(const IgemmArgs& a0, int64_t groups, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    QNB_CUDA(cudaFuncSetAttribute(igemm_patch_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
+  IgemmArgs a = a0;
+  a.groups = (int32_t)groups;
+  // B ring: as deep as shared memory allows (<= kMaxStages)
+  int sb = kMaxStages;
+  if (a.pt_bstat) {
+    sb = a.num_kb;  // all of B resident
+  } else {
+    while (sb > 2 && igemm_patch_smem_bytes(a, sb) > 220 * 1024) --sb;
+  }
+  const size_t smem = igemm_patch_smem_bytes(a, sb);
+  if (smem > 227 * 1024) return fail(QNB_E_UNSUPPORTED, "patch tile exceeds shared memory");
+  a.kb_per_split = sb;
+  const int64_t grid_pix = (a.m_total / ((int64_t)a.oh * a.ow)) * a.pt_hp * a.pt_wp;
+  const int64_t m_tiles = ceil_div(grid_pix, kBM);
+  const int64_t tiles = m_tiles * a.n_tiles * groups;
+  int64_t grid = std::min<int64_t>(tiles, num_sms());
+  if (a.pt_bstat) {  // whole CTAs per (group, n-tile), each walking m-tiles
+    const int64_t combos = (int64_t)a.n_tiles * groups;
+    const int64_t per = std::max<int64_t>(1, std::min<int64_t>(num_sms() / combos, m_tiles));
+    grid = per * combos;
+  }
+  igemm_patch_kernel<KIND><<<(unsigned)grid, kThreads, smem, s>>>(a);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
 template <int KIND>
 static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     size_t mx = 0;
-    for (int r = 16; r <= 256; r += 16) mx = std::max(mx, igemm_smem_bytes(r));
+    for (int r = 16; r <= 256; r += 16)
+      for (int kb : {128, 64, 32}) mx = std::max(mx, igemm_smem_bytes(r, kb));
     QNB_CUDA(cudaFuncSetAttribute(igemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
     attr_set = true;
   }
   IgemmArgs a = a0;
+  if (a.kbytes == 0) a.kbytes = 128;
   a.groups = (int32_t)groups;
   if (a.ksplit < 1) a.ksplit = 1;
   if (a.ksplit == 1) a.kb_per_split = a.num_kb;
@@ -779,10 +1538,15 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     a.epi_mode = EPIM_Q16;
   } else if (a.epi == EPI_Q8) {
     const bool fast = a.fast_rq && a.chan_const32 != nullptr;
-    a.epi_mode = fast ? (a.has_relu ? ((a.relu.acc32 && a.relu_lut) ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
+    a.epi_mode = fast ? (a.has_relu ? (relu_fast_ok(a.relu) ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
                       : EPIM_Q8_EXACT;
   } else {
     a.epi_mode = a.epi == EPI_F16 ? EPIM_F16 : EPIM_F32;
+  }
+  if (a.patch) return launch_patch<KIND>(a, groups, s);
+  if (a.hk) {
+    if constexpr (KIND == KIND_I8) return launch_hk<KIND>(a, s);
+    return fail(QNB_E_ARG, "row-Hankel mode is INT8 only");
   }
   const int64_t m_tiles = ceil_div(a.m_total, kBM);
   a.cluster = (m_tiles >= 2 && a.cluster != 1) ? 2 : 1;
@@ -791,7 +1555,8 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nclusters * a.cluster));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = igemm_smem_bytes(a.n_rows);
+  if (a.kbytes != 128 && !a.a_tma) return fail(QNB_E_ARG, "cp.async producers need 128-byte stages");
+  cfg.dynamicSmemBytes = igemm_smem_bytes(a.n_rows, a.kbytes);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -806,8 +1571,15 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   return QNB_OK;
 }
 
-qnb_status igemm_launch(int kind, const IgemmArgs& a, int64_t groups, cudaStream_t s) {
-  if (a.m_total <= 0) return QNB_OK;
+qnb_status igemm_launch(int kind, const IgemmArgs& a_in, int64_t groups, cudaStream_t s) {
+  if (a_in.m_total <= 0) return QNB_OK;
+  IgemmArgs a = a_in;
+  static const int dbg = [] {
+    const char* e = std::getenv("QNB_IGEMM_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg |= dbg;
+  if (a.m_total >= (int64_t(1) << 31)) return fail(QNB_E_UNSUPPORTED, "more than 2^31 output pixels in one launch");
   switch (kind) {
     case KIND_I8:
       return launch_kind<KIND_I8>(a, groups, s);

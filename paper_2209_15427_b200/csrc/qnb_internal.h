@@ -1,6 +1,7 @@
 // Host-side internals shared by the qnb translation units (not part of the ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -54,14 +55,19 @@ struct ActLayout {
   int64_t n = 0, h = 0, w = 0, c = 0;
   int64_t hh = 0, hw = 0, c_phys = 0;
   int64_t wx = 0;  // extra columns on the right (keeps rows 16-byte aligned)
+  // Image-pair interleaving (row-Hankel conv inputs): images 2q and 2q+1 share one
+  // "pair image" whose rows are [row of image 2q | row of image 2q+1], each in a
+  // pair_slot-byte slot; image n starts at (n/2)*img() + (n%2)*pair_slot.
+  int64_t pair_slot = 0;
   int dtype = QNB_INT8Q;
   int64_t es() const { return (int64_t)dtype_size(dtype); }
   int64_t hp() const { return h + 2 * hh; }
   int64_t wp() const { return w + 2 * hw + wx; }
   int64_t pix() const { return c_phys * es(); }
-  int64_t row() const { return wp() * pix(); }
+  int64_t row() const { return pair_slot ? 2 * pair_slot : wp() * pix(); }
   int64_t img() const { return hp() * row(); }
-  int64_t bytes() const { return n * img(); }
+  int64_t bytes() const { return (pair_slot ? (n + 1) / 2 : n) * img(); }
+  int64_t image_offset(int64_t i) const { return pair_slot ? (i >> 1) * img() + (i & 1) * pair_slot : i * img(); }
   int64_t interior_offset() const { return hh * row() + hw * pix(); }
 };
 
@@ -86,6 +92,12 @@ struct ReluRequant {
 };
 
 struct IgemmArgs {
+  // TMA im2col descriptor of the A operand (a_tma = 1): the NHWC activation as a 4-D
+  // tensor {C, W, H, N}; one cp.async.bulk.tensor.im2col per K stage fetches the
+  // stage's (tap, channel chunk) for 128 consecutive output pixels, swizzled.
+  alignas(64) CUtensorMap tmap_a;
+  int32_t a_tma;
+  int32_t kbytes;  // K bytes per smem stage (128 / 64 / 32 = the swizzle span)
   // A operand: implicit im2col rows over an NHWC activation.
   const uint8_t* a;
   int64_t a_img, a_row, a_pix, a_group, a_origin;  // byte strides / origin offset
@@ -122,7 +134,30 @@ struct IgemmArgs {
   // 1 <= s <= 62, so the requant runs as one 32x32->64 multiply + 64-bit round;
   // 0: exact 128-bit path (src/quantizer.cpp:201-212 verbatim).
   int32_t fast_rq;
+  // Row-Hankel mode (hk = 1; small-channel strided convs such as AlexNet conv1): the
+  // tile is two output rows of one image (M rows 0-63 / 64-127); per kernel row r the
+  // two input rows are bulk-copied to smem 1024 bytes apart and the A operand is read
+  // IN PLACE through a non-swizzled K-major descriptor with LBO = 16 and SBO = 128:
+  // output pixel m's K bytes start at byte 16*m = m*stride_w*pixel of the input row,
+  // so no im2col is ever materialised.  B (weights) stays resident in smem.
+  int32_t hk, hk_rows, hk_kpr, hk_copy, hk_pairs;  // hk_copy: bytes per tile; hk_pairs: image pairs
+  int32_t dbg;  // profiling probes (env QNB_IGEMM_DBG): 1 epilogue skips its math, 2 no MMAs
+  // Patch mode (patch = 1; stride-1 convs over NHWC): output pixels live on the padded
+  // grid of the input (row pitch pt_wp, pt_hp rows per image; rows/columns outside the
+  // real output are computed and discarded).  Per tile and per pair of 16-byte channel
+  // blocks, the producers copy the tile's input patch (pt_rows x pt_wp pixels) as two
+  // [pixel][16 B] planes; every filter tap is then an MMA whose A operand starts at
+  // tap offset (r * pt_wp + s) pixels inside the planes (non-swizzled K-major: pixel
+  // pitch 16 B, LBO = plane bytes).  A leaves L2 once per tile instead of kh*kw times.
+  int32_t patch, pt_wp, pt_hp, pt_rows, pt_plane, pt_pairs, pt_kh, pt_kw, pt_cblk, pt_nblk;
+  // pt_bstat = 1: the whole B of one (group, n-tile) stays resident in smem; each CTA
+  // owns one such combination and walks its pixel tiles (weights leave L2 once per CTA).
+  int32_t pt_bstat;
 };
+// Row-Hankel mode: the input is image-pair interleaved with 1024-byte row slots, so
+// one tile (output row oy of images 2q and 2q+1) needs input rows
+// [oy*stride_h, oy*stride_h + kh) of pair q -- ONE contiguous block of kh*2048 bytes.
+constexpr int kHkSlot = 1024;
 
 // Host proof for IgemmArgs::fast_rq: bounds of the int64 accumulator over all
 // inputs (u8 x u8 dot in [0, 255*255*K], rowsum in [0, 255*K]).
@@ -150,7 +185,8 @@ struct IgemmPacked {
   std::vector<int64_t> kmap;        // per packed K element -> reference k, or -1
   int32_t num_kb = 0;
   int32_t n_rows = 0, n_tiles = 0, n_per_tile = 0, ones_col = -1, tmem_cols = 0;
-  std::vector<uint8_t> b;           // [G][n_tiles][num_kb][n_rows][128]
+  std::vector<uint8_t> b;           // [G][n_tiles][num_kb][n_rows][kbytes]
+  int32_t kbytes = 128;             // K bytes per stage (swizzle span of A and B)
   // Grouped conv whose per-group channel slice is not 16-byte aligned: the A rows are
   // whole kernel-row runs over ALL channels (shared by every group, a_group = 0) and
   // kmap holds the group-global reference index (c_global*KH + r)*KW + s; the packer
@@ -172,6 +208,22 @@ qnb_status igemm_plan_k(const IgemmGeometry& g, const ActLayout& in, IgemmPacked
 // tiles.  `w` is raw host bytes of element type w_es; quantized kinds add the
 // ones row used for the per-row input sum.
 qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, IgemmPacked* pk);
+// TMA im2col A operand (see IgemmArgs::tmap_a): eligibility, stage list (chunk_off
+// holds {c0, s, r} per stage) and K map; then the tensor map over the activation.
+bool igemm_tma_eligible(const IgemmGeometry& g, const ActLayout& in);
+qnb_status igemm_plan_tma(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk);
+qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base, int32_t kbytes,
+                            CUtensorMap* map);
+// Patch mode (see IgemmArgs::patch): eligibility and K map (K steps ordered
+// (channel-block pair, tap), 32 bytes each, 4 per 128-byte B stage).
+bool igemm_patch_eligible(const IgemmGeometry& g, const ActLayout& in);
+qnb_status igemm_plan_patch(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* pairs);
+int igemm_patch_bstat_npt(const IgemmGeometry& g, int64_t num_kb, int32_t plane);
+
+// Row-Hankel eligibility (see IgemmArgs::hk) and its K map / stage count.
+bool hk_geometry_ok(const IgemmGeometry& g, const ActLayout& in);
+bool igemm_hk_eligible(const IgemmGeometry& g, const ActLayout& in);
+qnb_status igemm_plan_hk(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* kpr);
 // Launches the tcgen05 kernel.
 qnb_status igemm_launch(int kind, const IgemmArgs& a, int64_t groups, cudaStream_t s);
 // Split-K reduction + INT8 epilogue (same arithmetic as the fused epilogue).

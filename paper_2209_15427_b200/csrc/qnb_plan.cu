@@ -22,6 +22,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -515,8 +516,31 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     return fail(QNB_E_QVALS, "quantizer not finalized: weight of layer " + std::to_string(op.layer));
   if (quant && !in.has_qv) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
   IgemmPacked pk;
-  QNB_TRY(igemm_plan_k(g, Lin, &pk));
+  int32_t hk_kpr = 0;
+  const bool hk = igemm_hk_eligible(g, Lin);
+  static const bool no_tma = std::getenv("QNB_NO_TMA") != nullptr;  // A/B switch for profiling
+  // Patch mode is opt-in (QNB_PATCH=1) until it beats the cp.async gather; TMA im2col
+  // is used where a tap's channels fill whole 128-byte stages (measured faster there).
+  static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
+  const bool patch = !hk && use_patch && igemm_patch_eligible(g, Lin);
+  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % 128 == 0;
+  int32_t pt_pairs = 0;
+  if (hk)
+    QNB_TRY(igemm_plan_hk(g, Lin, &pk, &hk_kpr));
+  else if (patch)
+    QNB_TRY(igemm_plan_patch(g, Lin, &pk, &pt_pairs));
+  else if (tma)
+    QNB_TRY(igemm_plan_tma(g, Lin, &pk));
+  else
+    QNB_TRY(igemm_plan_k(g, Lin, &pk));
   if (g.is_fc && !quant) pk.n_per_tile = 128;
+  int32_t pt_bstat_npt = 0;
+  if (patch && g.kind == KIND_I8 && !std::getenv("QNB_NO_BSTAT")) {
+    const int64_t wp = Lin.w + 2 * g.pw;
+    const int64_t rows = (wp + 125 + g.kw) / wp + g.kh;
+    pt_bstat_npt = igemm_patch_bstat_npt(g, pk.num_kb, (int32_t)(round_up(rows * wp * 16, 128) + 64));
+    if (pt_bstat_npt > 0) pk.n_per_tile = pt_bstat_npt;
+  }
   QNB_TRY(igemm_pack_b(g, l.weight, l.weight_dtype, &pk));
   IgemmArgs& a = st.ig;
   std::memset(&a, 0, sizeof(a));
@@ -524,7 +548,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   a.a_img = Lin.img();
   a.a_row = Lin.row();
   a.a_pix = Lin.pix();
-  a.a_group = pk.all_groups ? 0 : g.cg * Lin.es();
+  a.a_group = pk.all_groups ? 0 : (tma ? g.cg : g.cg * Lin.es());
   a.a_origin = (Lin.hh - g.ph) * Lin.row() + (Lin.hw - g.pw) * Lin.pix();
   a.stride_h = (int32_t)g.sh;
   a.stride_w = (int32_t)g.sw;
@@ -532,6 +556,31 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   a.ow = (int32_t)g.ow;
   a.m_total = P.max_batch * g.oh * g.ow;
   a.num_kb = pk.num_kb;
+  a.kbytes = pk.kbytes;
+  if (patch) {
+    a.patch = 1;
+    a.pt_wp = (int32_t)(Lin.w + 2 * g.pw);
+    a.pt_hp = (int32_t)(Lin.h + 2 * g.ph);
+    a.pt_rows = (int32_t)((a.pt_wp + 125 + g.kw) / a.pt_wp + g.kh);
+    a.pt_plane = (int32_t)(round_up((int64_t)a.pt_rows * a.pt_wp * 16, 128) + 64);  // +64: plane 1 on other banks
+    a.pt_pairs = pt_pairs;
+    a.pt_kh = (int32_t)g.kh;
+    a.pt_kw = (int32_t)g.kw;
+    a.pt_cblk = (int32_t)(16 / Lin.es());
+    a.pt_nblk = (int32_t)(g.cg * Lin.es() / 16);
+    a.pt_bstat = pt_bstat_npt > 0 ? 1 : 0;
+  }
+  if (tma) {
+    a.a_tma = 1;
+    QNB_TRY(igemm_encode_tma(g, Lin, blob_ptr(P, op.in), pk.kbytes, &a.tmap_a));
+  }
+  if (hk) {
+    a.hk = 1;
+    a.hk_rows = (int32_t)g.kh;
+    a.hk_kpr = hk_kpr;
+    a.hk_copy = (int32_t)(g.kh * Lin.row());           // kh rows of one image pair
+    a.hk_pairs = (int32_t)ceil_div(Lin.n, 2);
+  }
   a.n_rows = pk.n_rows;
   a.n_tiles = pk.n_tiles;
   a.n_real = (int32_t)g.og;

@@ -107,12 +107,15 @@ __device__ __forceinline__ void store_from_float(uint8_t* p, int dtype, float v,
   }
 }
 
+__device__ __forceinline__ int64_t img_off(const DevLayout& L, int64_t n) {
+  return L.pslot ? (n >> 1) * L.img + (n & 1) * L.pslot : n * L.img;
+}
 __device__ __forceinline__ uint8_t* at(uint8_t* base, const DevLayout& L, int64_t n, int64_t y, int64_t x) {
-  return base + n * L.img + y * L.row + x * L.pix + L.origin;
+  return base + img_off(L, n) + y * L.row + x * L.pix + L.origin;
 }
 __device__ __forceinline__ const uint8_t* at(const uint8_t* base, const DevLayout& L, int64_t n, int64_t y,
                                              int64_t x) {
-  return base + n * L.img + y * L.row + x * L.pix + L.origin;
+  return base + img_off(L, n) + y * L.row + x * L.pix + L.origin;
 }
 
 // ------------------------------------------------------------- pack_input

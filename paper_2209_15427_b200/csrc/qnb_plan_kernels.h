@@ -15,6 +15,7 @@ struct DevLayout {
   int64_t n, h, w, c, c_phys;
   int64_t img, row, pix, origin;
   int32_t es;
+  int64_t pslot;  // ActLayout::pair_slot (0: plain NHWC)
 };
 
 inline DevLayout dev_layout(const ActLayout& L) {
@@ -29,6 +30,7 @@ inline DevLayout dev_layout(const ActLayout& L) {
   d.pix = L.pix();
   d.origin = L.interior_offset();
   d.es = (int32_t)L.es();
+  d.pslot = L.pair_slot;
   return d;
 }
 

@@ -6,7 +6,11 @@ through libm (LRN pow, softmax exp) are allowed 1 ulp on a tiny fraction of
 elements; tensor-core float convolutions use the north-star tolerance
 (max-abs <= 1e-2 x output range).
 """
+import os
+
 import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 import pytest
 
 from paper_2209_15427_b200 import ops
@@ -258,3 +262,26 @@ def test_inner_product_tiling_and_split_k(oracle_impl, npt, ks, monkeypatch):
     ours = ops.inner_product(x, INT8Q, w, INT8Q, bias, O, qx, qw, qo)
     theirs = oracle_impl.inner_product(x, INT8Q, w, INT8Q, bias, O, qx, qw, qo)
     assert_bits_equal(ours, theirs, f"ip npt={npt} ks={ks}")
+
+
+@pytest.mark.parametrize("mode", ["patch", "cpasync"])
+@pytest.mark.parametrize("case", [1, 2, 3, 4])
+def test_conv_int8_operand_paths(oracle_impl, case, mode):
+    """The alternative A-operand engines (patch planes / plain cp.async gather) are
+    bit-exact too; each runs in its own process (the mode switch is read once)."""
+    import subprocess, sys, json
+    env = dict(os.environ)
+    env.pop("QNB_PATCH", None)
+    if mode == "patch":
+        env["QNB_PATCH"] = "1"
+    else:
+        env["QNB_NO_TMA"] = "1"
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r); "
+        "from test_gpu_ops import _conv_case, CONV_CASES; from oracle import ffi; "
+        "o = ffi.Reference() if ffi.have_reference() else ffi.Restatement(); "
+        "N, C, H, W, cp = CONV_CASES[%d]; "
+        "_conv_case(o, np.random.default_rng(300 + %d), N, C, H, W, cp, 2); print('ok')"
+        % (ROOT, os.path.join(ROOT, "tests"), case, case))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
