@@ -28,6 +28,16 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "AlexNet INT8 images/sec (batch 256 per GPU, 227x227)"
+METRICS = {
+    "alexnet": "AlexNet {P} images/sec (batch {B} per GPU, 227x227)",
+    "alexnet_moe": "AlexNet-MoE {P} images/sec (16 experts top-4, batch {B} per GPU, 227x227)",
+    "vgg16": "VGG-16 {P} images/sec (batch {B} per GPU, 224x224)",
+}
+CONFIG_IDX = {"alexnet": 1, "alexnet_moe": 2, "vgg16": 3}
+
+
+def metric_name(model, precision, batch):
+    return METRICS.get(model, "{M} {P} images/sec (batch {B})").format(M=model, P=precision.upper(), B=batch)
 DT = {"fp32": 0, "fp16": 1, "int8": 2, "int16": 3}
 
 
@@ -134,7 +144,10 @@ def model_setup(model: str, precision: str):
     from paper_2209_15427_b200 import graphs
     g = graphs.MODELS[model](1)
     shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
-    params = graphs.synth_params(g, shapes)
+    if any(l["kind"] == "moe" for l in g["layers"]):
+        params = graphs.synth_params_moe(g)
+    else:
+        params = graphs.synth_params(g, shapes)
     with open(os.path.join(ROOT, "tests", "golden", f"{model}_{precision}_calib.json")) as f:
         ranges = json.load(f)["ranges"]
     return g, shapes, params, ranges
@@ -190,11 +203,11 @@ def run_reference(a):
         cpu_forward_rate(nets, x, 4000)
     dt = time.perf_counter() - t0
     v = T * a.steps / dt
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": a.gpus,
+    line = {"impl": "reference", "metric": metric_name(a.model, a.precision, a.batch), "value": v, "unit": "images/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic U(0,255) images, seeded random-init weights",
-            "config": {"workload": f"{a.model} {a.precision} forward, 227x227, bounded sample of {T} images "
+            "config": {"workload": f"{a.model} {a.precision} forward, bounded sample of {T} images "
                                    f"per step (reference Net::forward, QUANTIZED mode)", "global_batch": T,
                        "parallelism": f"{T} host threads, one Net each"},
             "cpu_baseline": {"value": v, "unit": "images/s", "cores": T, "kind": "reference",
@@ -203,35 +216,79 @@ def run_reference(a):
     print(json.dumps(line))
 
 
+class Workload:
+    """The measured hot path for one rank: a compiled plan (chain nets) or the MoE
+    executor, with device input/output buffers and a step() that runs one forward."""
+
+    def __init__(self, a, rank, ws):
+        import torch
+        from paper_2209_15427_b200 import graph as G
+        from paper_2209_15427_b200 import graphs
+        from paper_2209_15427_b200.net import QUANTIZED, Net
+        g, shapes, params, ranges = model_setup(a.model, a.precision)
+        self.g, self.shapes, self.params, self.ranges = g, shapes, params, ranges
+        self.moe = any(l["kind"] == "moe" for l in g["layers"])
+        gg = G.override_precision(g, a.precision) if a.precision != "fp32" else g
+        if self.moe:
+            from paper_2209_15427_b200.moe import MoeNet
+            net = MoeNet(gg, rank=rank, world=ws)
+        else:
+            net = Net(gg)
+        for k, v in params.items():
+            net.set_param(k, v)
+        for k, (lo, hi) in ranges.items():
+            net.set_range(k, lo, hi)
+        net.finalize_quantizers()
+        net.set_quant_mode(QUANTIZED)
+        self.net = net
+        B = self.B = a.batch
+        self.x_host = graphs.synth_images(B, shapes["data"][1:], offset=rank * B)
+        self.x_dev = torch.from_numpy(self.x_host).cuda()
+        self.n_out = 1000
+        self.out_dev = torch.empty((B, self.n_out), dtype=torch.float32, device="cuda")
+        self.sp = torch.cuda.current_stream().cuda_stream
+        if self.moe:
+            self.plan = None
+            self.kernels = None
+        else:
+            self.plan = net.compile(B)
+            self.kernels = self.plan.stats()["kernels_per_forward"]
+
+    def step(self):
+        if self.moe:
+            self.net.forward_device(self.x_dev.data_ptr(), self.out_dev.data_ptr(), self.B)
+        else:
+            self.plan.forward_device(self.x_dev.data_ptr(), self.out_dev.data_ptr(), self.B, self.sp)
+
+    def step_e2e(self, x_pin, o_pin):
+        if self.moe:  # the MoE executor stages host buffers itself
+            self.x_dev.copy_(x_pin, non_blocking=True)
+            self.net.forward_device(self.x_dev.data_ptr(), self.out_dev.data_ptr(), self.B)
+            o_pin.copy_(self.out_dev, non_blocking=True)
+        else:
+            self.plan.forward_device(x_pin.data_ptr(), o_pin.data_ptr(), self.B, self.sp, in_host=True,
+                                     out_host=True)
+
+
 def run_qnb(a):
     import torch
     ws, rank, local = dist_setup(use_cuda=True)
     torch.cuda.set_device(local)
-    from paper_2209_15427_b200 import graph as G
-    from paper_2209_15427_b200 import graphs
     from paper_2209_15427_b200._lib import check, lib
-    from paper_2209_15427_b200.net import QUANTIZED, Net
 
     check(lib().qnb_device_check(local))
-    g, shapes, params, ranges = model_setup(a.model, a.precision)
-    net = Net(G.override_precision(g, a.precision) if a.precision != "fp32" else g)
-    for k, v in params.items():
-        net.set_param(k, v)
-    for k, (lo, hi) in ranges.items():
-        net.set_range(k, lo, hi)
-    net.finalize_quantizers()
-    net.set_quant_mode(QUANTIZED)
-    B = a.batch
-    plan = net.compile(B)
-    kernels = plan.stats()["kernels_per_forward"]
-    x_host = graphs.synth_images(B, shapes["data"][1:], offset=rank * B)
-    x_dev = torch.from_numpy(x_host).cuda()
-    out_dev = torch.empty((B, 1000), dtype=torch.float32, device="cuda")
+    wl = Workload(a, rank, ws)
+    B = wl.B
     stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
+    # N > 1: every rank classifies its own batch shard; the final logits are gathered
+    # over NCCL (the path's only data-path collective besides the MoE all-to-all)
+    gathered = torch.empty((ws * B, wl.n_out), dtype=torch.float32, device="cuda") if ws > 1 else None
 
     def step():
-        plan.forward_device(x_dev.data_ptr(), out_dev.data_ptr(), B, sp)
+        wl.step()
+        if ws > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(gathered, wl.out_dev)
 
     for _ in range(max(a.warmup, 3)):
         step()
@@ -253,29 +310,29 @@ def run_qnb(a):
     value = ws * B * a.steps / (ms_max / 1e3)
 
     # end to end through the C-ABI with pinned host buffers (H2D input + D2H result per step)
-    x_pin = torch.from_numpy(x_host).pin_memory()
-    o_pin = torch.empty((B, 1000), dtype=torch.float32).pin_memory()
-
-    def step_e2e():
-        plan.forward_device(x_pin.data_ptr(), o_pin.data_ptr(), B, sp, in_host=True, out_host=True)
-
+    x_pin = torch.from_numpy(wl.x_host).pin_memory()
+    o_pin = torch.empty((B, wl.n_out), dtype=torch.float32).pin_memory()
     for _ in range(2):
-        step_e2e()
+        wl.step_e2e(x_pin, o_pin)
     torch.cuda.synchronize()
     barrier(ws, local)
     e0.record(stream)
     for _ in range(a.steps):
-        step_e2e()
+        wl.step_e2e(x_pin, o_pin)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(ws, local)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws, local)
     e2e_value = ws * B * a.steps / (e2e_ms / 1e3)
+    # the PCIe bound of that number: the same pinned H2D copy alone
+    h2d = torch.empty_like(wl.x_dev)
+    e0.record(stream)
+    for _ in range(a.steps):
+        h2d.copy_(x_pin, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    h2d_ms = e0.elapsed_time(e1) / a.steps
 
-    # per-step profile (events between steps, eager) -> roofline of the dominant kernel
-    ms_steps = plan.profile(x_dev.data_ptr(), out_dev.data_ptr(), B, a.profile_reps, sp)
-    steps_info = plan.steps()
-    names = [l["name"] for l in net.graph["layers"]]
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -286,30 +343,36 @@ def run_qnb(a):
         peak_src = "fallback"
     int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 = 2x dense bf16 on B200
     hbm_peak = peaks["hbm_gbs"]
-    per_layer = []
-    conv_ops = conv_ms = 0.0
-    for (li, kind, ops_, by), t in zip(steps_info, ms_steps):
-        per_layer.append({"layer": names[li] if 0 <= li < len(names) else str(li), "kernel": kind,
-                          "ms": round(t, 4),
-                          "tops": round(ops_ / (t * 1e-3) / 1e12, 1) if ops_ else None,
-                          "gbs": round(by / (t * 1e-3) / 1e9, 1)})
-        if kind == "igemm" and names[li].startswith("conv"):
-            conv_ops += ops_
-            conv_ms += t
-    dom = int(np.argmax(ms_steps))
-    li, kind, ops_, by = steps_info[dom]
-    t = ms_steps[dom]
-    if kind == "igemm":
-        roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",
-                "kernel": f"igemm {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
-    else:
-        roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "kernel": f"{kind} {names[li]}", "algorithmic_bytes": by, "launch_ms": t}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
-    roof["peak_source"] = (f"{peak_src}: 2 x bf16_tflops {peaks['bf16_tflops']} (dense int8 = 2x bf16)"
-                           if kind == "igemm" else f"{peak_src}: hbm_gbs")
-    conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
+    per_layer, roof, conv_tops = [], None, None
+    if wl.plan is not None:
+        # per-step profile (events between steps, eager) -> roofline of the dominant kernel
+        plan, net = wl.plan, wl.net
+        ms_steps = plan.profile(wl.x_dev.data_ptr(), wl.out_dev.data_ptr(), B, a.profile_reps, wl.sp)
+        steps_info = plan.steps()
+        names = [l["name"] for l in net.graph["layers"]]
+        conv_ops = conv_ms = 0.0
+        for (li, kind, ops_, by), t in zip(steps_info, ms_steps):
+            per_layer.append({"layer": names[li] if 0 <= li < len(names) else str(li), "kernel": kind,
+                              "ms": round(t, 4),
+                              "tops": round(ops_ / (t * 1e-3) / 1e12, 1) if ops_ else None,
+                              "gbs": round(by / (t * 1e-3) / 1e9, 1)})
+            if kind == "igemm" and names[li].startswith("conv"):
+                conv_ops += ops_
+                conv_ms += t
+        dom = int(np.argmax(ms_steps))
+        li, kind, ops_, by = steps_info[dom]
+        t = ms_steps[dom]
+        if kind == "igemm":
+            roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",
+                    "kernel": f"igemm {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
+        else:
+            roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "kernel": f"{kind} {names[li]}", "algorithmic_bytes": by, "launch_ms": t}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["peak_source"] = (f"{peak_src}: 2 x bf16_tflops {peaks['bf16_tflops']} (dense int8 = 2x bf16)"
+                               if kind == "igemm" else f"{peak_src}: hbm_gbs")
+        conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
 
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:
@@ -317,8 +380,10 @@ def run_qnb(a):
             from oracle import ffi
             if ffi.have_reference():
                 T = min(a.cpu_threads, os.cpu_count() or 1)
-                nets = reference_nets(g, a.precision, params, ranges, T)
-                xs = x_host[:T]
+                if wl.moe:
+                    T = min(T, 4)  # the MoE reference evaluates all 16 experts per image
+                nets = reference_nets(wl.g, a.precision, wl.params, wl.ranges, T)
+                xs = wl.x_host[:T]
                 v = cpu_forward_rate(nets, xs, 4000)
                 cpu = {"value": v, "unit": "images/s", "cores": T, "kind": "reference",
                        "sample": f"{T} images of the same batch, one reference Net::forward thread each"}
@@ -327,20 +392,31 @@ def run_qnb(a):
             cpu = {"value": None, "error": str(e)[:200]}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "u8 (s32 accumulate)",
-                "data": "synthetic U(0,255) images, seeded random-init weights",
-                "config": {"workload": f"{a.model} {a.precision} forward, batch {B} per GPU, 227x227 (BASELINE "
-                                       f"configs[1])", "model": a.model, "global_batch": B * ws,
-                           "parallelism": f"dp{ws} (independent replicas, no collective)",
-                           "l2": "input batch 158 MB > 126 MB L2 (no flush needed)"},
+        res = wl.x_host.shape[-1]
+        line = {"metric": metric_name(a.model, a.precision, B), "value": value, "unit": "images/s", "n_gpus": ws,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "u8 (s32 accumulate)" if a.precision in ("int8", "int16") else a.precision,
+                "data": f"synthetic U(0,255) images, seeded random-init weights",
+                "config": {"workload": f"{a.model} {a.precision} forward, batch {B} per GPU, {res}x{res} "
+                                       f"(BASELINE configs[{CONFIG_IDX.get(a.model, '?')}])",
+                           "model": a.model, "global_batch": B * ws,
+                           "parallelism": (f"dp{ws}: batch shard per GPU, NCCL all-gather of the logits"
+                                           + (", expert-parallel all-to-all" if wl.moe else "")) if ws > 1
+                           else "dp1 (single GPU)",
+                           "l2": f"input batch {wl.x_host.nbytes / 1e6:.0f} MB "
+                                 + ("> 126 MB L2 (no flush needed)" if wl.x_host.nbytes > 126e6
+                                    else "<= L2: activations are rewritten every step")},
                 "e2e": {"value": e2e_value, "unit": "images/s",
-                        "h2d_bytes_per_step": int(x_host.nbytes), "d2h_bytes_per_step": int(B * 1000 * 4)},
-                "gpu_launches": int(launches), "kernels_per_forward": kernels,
+                        "h2d_bytes_per_step": int(wl.x_host.nbytes), "d2h_bytes_per_step": int(B * wl.n_out * 4),
+                        "h2d_only_ms": h2d_ms, "pcie_bound_images_per_s": B / (h2d_ms / 1e3)},
+                "gpu_launches": int(launches), "kernels_per_forward": wl.kernels,
                 "roofline": roof, "conv_tops": conv_tops, "conv_frac_of_int8_peak":
                     (conv_tops / int8_peak if conv_tops else None),
                 "cpu_baseline": cpu, "clocks": clk.summary(), "per_layer": per_layer}
+        if wl.moe:
+            line["moe_expert_counts_last_step"] = [int(c) for c in wl.net.last_stats["counts"]] \
+                if hasattr(wl.net, "last_stats") else None
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist

@@ -309,7 +309,8 @@ class MoeNet:
         check(lib.qnb_moe_combine_rows(y.data_ptr(), p["per"], b["pair_slot"].data_ptr(), b["w"].data_ptr(), B,
                                        self.top_k, p["top_dtype"], qv, b["M"].data_ptr(), sp))
         p["tail"].forward_device(b["M"].data_ptr(), out_ptr, B, s)
-        return {"counts": counts}
+        self.last_stats = {"counts": counts}
+        return self.last_stats
 
     def forward(self, inputs: dict) -> dict:
         """Net::forward (src/net.cpp:305-330) with host arrays in and out."""
