@@ -114,54 +114,74 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
 // unsigned values.  (A 256-entry smem table was 1 shared wavefront per distinct byte:
 // ~27 per warp load -- the arithmetic form is cheaper.)
 struct ReluFastK {
-  int32_t zin;
-  uint32_t mult;
-  int32_t sb, rs, ls, zout, omin, omax;
+  int32_t zdiff, dmax, dmin;  // d = max(min(q + zdiff, dmax), dmin) = max(clamp(q + oz) - zin, 0)
+  uint32_t mult, mask;
+  int32_t n, zout, omin, omax;  // t = ((d * mult) >> n) & mask, n = shift_bits + shift (>= 0)
 };
-__device__ __forceinline__ ReluFastK relu_fast_consts(const ReluRequant& r) {
+__device__ __forceinline__ ReluFastK relu_fast_consts(const ReluRequant& r, const Requant& rq) {
   ReluFastK k;
-  k.zin = (int32_t)r.in_zero;
+  const int32_t zin = (int32_t)r.in_zero;
+  k.zdiff = (int32_t)rq.out_zero - zin;
+  k.dmax = (int32_t)rq.out_max - zin;
+  k.dmin = max((int32_t)rq.out_min - zin, 0);
   k.mult = (uint32_t)r.mult;
-  k.sb = r.shift_bits;
-  k.rs = r.shift >= 0 ? r.shift : 0;
-  k.ls = r.shift < 0 ? -r.shift : 0;
+  const int ls = r.shift < 0 ? -r.shift : 0;
+  k.n = r.shift_bits + r.shift;  // floor(floor(P / 2^sb) * 2^ls) = floor(P / 2^(sb-ls)) with the low ls bits cleared
+  k.mask = ~((1u << ls) - 1u);
   k.zout = (int32_t)r.out_zero;
   k.omin = (int32_t)r.out_min;
   k.omax = (int32_t)r.out_max;
   return k;
 }
-__device__ __forceinline__ uint32_t relu_fast(int32_t v, const ReluFastK& r) {
-  const uint32_t d = (uint32_t)max(v - r.zin, 0);
-  uint32_t t = (uint32_t)(((uint64_t)d * r.mult) >> r.sb);
-  t = (t >> r.rs) << r.ls;
+__device__ __forceinline__ int64_t mulwide_s32(int32_t a, int32_t b) {
+  int64_t r;
+  asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t mulwide_u32(uint32_t a, uint32_t b) {
+  uint64_t r;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+// RN32: n >= 32 (the product's high word alone holds the quotient)
+template <bool RN32>
+__device__ __forceinline__ uint32_t relu_tail(int32_t q, const ReluFastK& r) {
+  const uint32_t d = (uint32_t)max(min(q + r.zdiff, r.dmax), r.dmin);
+  const uint64_t P = mulwide_u32(d, r.mult);
+  uint32_t t;
+  if constexpr (RN32) t = (uint32_t)(P >> 32) >> (r.n - 32);
+  else t = __funnelshift_r((uint32_t)P, (uint32_t)(P >> 32), (uint32_t)r.n);
+  t &= r.mask;
   return (uint32_t)min(max((int32_t)t + r.zout, r.omin), r.omax);
 }
 
-template <bool RELU, bool HI>
+// F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32.
+template <bool RELU, int F>
 __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk) {
-  const int64_t pr = (int64_t)acc * (int64_t)k.mult32;
-  int32_t v;
-  if constexpr (HI) {
+  int32_t q;  // RNE quotient (before the output zero point)
+  if constexpr ((F & 1) != 0) {
+    const int64_t pr = mulwide_s32(acc, k.mult32);
     const uint32_t b = ((uint32_t)(pr >> 32) >> k.sh) & 1u;
-    const int64_t t = pr + k.halfm1 + (int64_t)b;
-    v = ((int32_t)(t >> 32) >> k.sh) + k.oz;
-    v = min(max(v, k.omin), k.omax);
+    const int64_t t = pr + (k.halfm1 + (int64_t)b);
+    q = (int32_t)(t >> 32) >> k.sh;
   } else {
+    const int64_t pr = mulwide_s32(acc, k.mult32);
     const int64_t b = (pr >> k.s) & 1;
-    int64_t q = ((pr + k.halfm1 + b) >> k.s) + k.oz;
-    q = q < k.omin ? k.omin : (q > k.omax ? k.omax : q);
-    v = (int32_t)q;
+    int64_t qq = (pr + k.halfm1 + b) >> k.s;
+    const int64_t lim = (int64_t)1 << 40;  // keep the int32 add below exact (clamped right after)
+    qq = qq < -lim ? -lim : (qq > lim ? lim : qq);
+    q = (int32_t)max(min(qq, (int64_t)INT32_MAX / 2), (int64_t)INT32_MIN / 2);
   }
-  if constexpr (RELU) return relu_fast(v, rk);
-  return (uint32_t)v;
+  if constexpr (RELU) return relu_tail<(F & 2) != 0>(q, rk);
+  return (uint32_t)min(max(q + k.oz, k.omin), k.omax);
 }
 
-template <int MODE, bool HI = false>
+template <int MODE, int F = 0>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
                                                uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
                                                int64_t ncl, int cs, int rank, int warp, int lane, uint8_t* lut) {
   (void)lut;
-  const ReluFastK lut_s = relu_fast_consts(p.relu);
+  const ReluFastK lut_s = relu_fast_consts(p.relu, p.rq);
   const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
   const int half = (warp - 5) >> 2;  // which 16-column blocks of the tile
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
@@ -293,10 +313,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
           uint32_t w[4];
 #pragma unroll
           for (int qd = 0; qd < 4; ++qd) {
-            const uint32_t b0 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 0] + cc[qd].x + rowterm32, k, lut_s);
-            const uint32_t b1 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 1] + cc[qd].y + rowterm32, k, lut_s);
-            const uint32_t b2 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 2] + cc[qd].z + rowterm32, k, lut_s);
-            const uint32_t b3 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 3] + cc[qd].w + rowterm32, k, lut_s);
+            const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[4 * qd + 0] + cc[qd].x + rowterm32, k, lut_s);
+            const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[4 * qd + 1] + cc[qd].y + rowterm32, k, lut_s);
+            const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[4 * qd + 2] + cc[qd].z + rowterm32, k, lut_s);
+            const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[4 * qd + 3] + cc[qd].w + rowterm32, k, lut_s);
             w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           *reinterpret_cast<uint4*>(obase + (int64_t)(ch0 + cb)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -345,10 +365,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int qd = 0; qd < 4; ++qd) {
             const int4 cc = __ldg(cc4 + qd);
-            const uint32_t b0 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut_s);
-            const uint32_t b1 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut_s);
-            const uint32_t b2 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut_s);
-            const uint32_t b3 = q8_fast<RELU, HI>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut_s);
+            const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut_s);
+            const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut_s);
+            const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut_s);
+            const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut_s);
             w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           if (o_vec) {
@@ -361,7 +381,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (i < cnt)
-              dst[i] = (uint8_t)q8_fast<RELU, HI>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut_s);
+              dst[i] = (uint8_t)q8_fast<RELU, F>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut_s);
         }
       } else if constexpr (MODE == EPIM_Q8_EXACT) {
 #pragma unroll
@@ -396,6 +416,34 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     __syncwarp();
     if (lane == 0) mbar_arrive(&acc_empty[buf]);
   }
+}
+
+// Epilogue specialisation switch shared by the three kernels.
+__device__ __forceinline__ void run_epilogue(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full, uint64_t* acc_empty,
+                                             int64_t m_groups, int64_t total, int64_t cid, int64_t ncl, int cs,
+                                             int rank, int warp, int lane, uint8_t* lut) {
+#define QNB_EPI(M, F) epilogue_tiles<M, F>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, lut)
+  const int f = (p.rq.s >= 32 ? 1 : 0) | (p.relu.shift_bits + p.relu.shift >= 32 ? 2 : 0);
+  switch (p.epi_mode) {
+    case EPIM_Q8_FAST_RELU:
+      switch (f) {
+        case 0: QNB_EPI(EPIM_Q8_FAST_RELU, 0); break;
+        case 1: QNB_EPI(EPIM_Q8_FAST_RELU, 1); break;
+        case 2: QNB_EPI(EPIM_Q8_FAST_RELU, 2); break;
+        default: QNB_EPI(EPIM_Q8_FAST_RELU, 3);
+      }
+      break;
+    case EPIM_Q8_FAST:
+      if (f & 1) QNB_EPI(EPIM_Q8_FAST, 1);
+      else QNB_EPI(EPIM_Q8_FAST, 0);
+      break;
+    case EPIM_Q8_EXACT: QNB_EPI(EPIM_Q8_EXACT, 0); break;
+    case EPIM_F16: QNB_EPI(EPIM_F16, 0); break;
+    case EPIM_Q16: QNB_EPI(EPIM_Q16, 0); break;
+    case EPIM_RAW32: QNB_EPI(EPIM_RAW32, 0); break;
+    default: QNB_EPI(EPIM_F32, 0);
+  }
+#undef QNB_EPI
 }
 
 // Persistent, warp-specialised implicit GEMM.  One CTA per SM loops over output
@@ -591,34 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    switch (p.epi_mode) {
-      case EPIM_Q8_FAST_RELU:
-        if (p.rq.s >= 32)
-          epilogue_tiles<EPIM_Q8_FAST_RELU, true>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        else
-          epilogue_tiles<EPIM_Q8_FAST_RELU, false>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        break;
-      case EPIM_Q8_FAST:
-        if (p.rq.s >= 32)
-          epilogue_tiles<EPIM_Q8_FAST, true>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        else
-          epilogue_tiles<EPIM_Q8_FAST, false>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        break;
-      case EPIM_Q8_EXACT:
-        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        break;
-      case EPIM_F16:
-        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        break;
-      case EPIM_Q16:
-        epilogue_tiles<EPIM_Q16>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        break;
-      case EPIM_RAW32:
-        epilogue_tiles<EPIM_RAW32>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-        break;
-      default:
-        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
-    }
+    run_epilogue(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
   }
 
   tc_fence_before();
@@ -729,22 +750,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_hk_kernel(const __grid_cons
       }
     }
   } else if (warp >= 5) {
-    switch (p.epi_mode) {
-      case EPIM_Q8_FAST_RELU:
-        if (p.rq.s >= 32)
-          epilogue_tiles<EPIM_Q8_FAST_RELU, true>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
-        else
-          epilogue_tiles<EPIM_Q8_FAST_RELU, false>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
-        break;
-      case EPIM_Q8_FAST:
-        if (p.rq.s >= 32)
-          epilogue_tiles<EPIM_Q8_FAST, true>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
-        else
-          epilogue_tiles<EPIM_Q8_FAST, false>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
-        break;
-      default:
-        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
-    }
+    run_epilogue(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
   }
   tc_fence_before();
   __syncthreads();
@@ -1025,31 +1031,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
       }
     }
   } else if (warp >= 5) {
-    switch (p.epi_mode) {
-      case EPIM_Q8_FAST_RELU:
-        if (p.rq.s >= 32)
-          epilogue_tiles<EPIM_Q8_FAST_RELU, true>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        else
-          epilogue_tiles<EPIM_Q8_FAST_RELU, false>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        break;
-      case EPIM_Q8_FAST:
-        if (p.rq.s >= 32)
-          epilogue_tiles<EPIM_Q8_FAST, true>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        else
-          epilogue_tiles<EPIM_Q8_FAST, false>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        break;
-      case EPIM_Q8_EXACT:
-        epilogue_tiles<EPIM_Q8_EXACT>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        break;
-      case EPIM_F16:
-        epilogue_tiles<EPIM_F16>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        break;
-      case EPIM_Q16:
-        epilogue_tiles<EPIM_Q16>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-        break;
-      default:
-        epilogue_tiles<EPIM_F32>(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
-    }
+    run_epilogue(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
   }
   tc_fence_before();
   __syncthreads();
@@ -1414,7 +1396,7 @@ __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
       if (u >= cnt) break;
       int64_t q;
       if constexpr (FAST) {
-        q = q8_fast<false, false>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, ReluFastK{});
+        q = q8_fast<false, 0>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, ReluFastK{});
       } else {
         q = requant_clamp((int64_t)d[u] + p.chan_const[o0 + u] - p.zw * (int64_t)rs, p.rq);
       }
@@ -1461,6 +1443,7 @@ static bool relu_fast_ok(const ReluRequant& r) {
   const int64_t tmax = (255 * r.mult) >> r.shift_bits;
   if (tmax >= (int64_t(1) << 31)) return false;
   if (r.shift < -31 || r.shift > 62) return false;
+  if (r.shift_bits + r.shift < 0 || r.shift_bits + r.shift > 63) return false;  // combined right shift n
   const int64_t t2 = r.shift >= 0 ? (tmax >> r.shift) : (tmax << -r.shift);
   const int64_t az = r.out_zero < 0 ? -r.out_zero : r.out_zero;
   return t2 + az < (int64_t(1) << 31) && r.out_min >= INT32_MIN && r.out_max <= INT32_MAX;
