@@ -179,11 +179,13 @@ __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, cons
 template <int MODE, int F = 0>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
                                                uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
-                                               int64_t ncl, int cs, int rank, int warp, int lane, uint8_t* lut) {
+                                               int64_t ncl, int cs, int rank, int warp, int lane, uint8_t* lut,
+                                               int slot, int nslots) {
   (void)lut;
   const ReluFastK lut_s = relu_fast_consts(p.relu, p.rq);
   const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
-  const int half = (warp - 5) >> 2;  // which 16-column blocks of the tile
+  // this warp drains the 16-column blocks slot, slot + nslots, ... of its lane quarter
+  const int half = slot, cstep = 16 * nslots;
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
   const Q8Consts k = q8_consts(p.rq);
   const int n_tiles = p.n_tiles, n_real = p.n_real, npt = p.n_per_tile, tcols = p.tmem_cols;
@@ -236,7 +238,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     }
     if constexpr (MODE == EPIM_RAW32) {
       int32_t* wrow = p.ws + (((int64_t)ks * p.m_total + row) * n_tiles + c.nt) * p.n_rows;
-      for (int cb = half * 16; cb < p.n_rows; cb += 32) {
+      for (int cb = half * 16; cb < p.n_rows; cb += cstep) {
         uint32_t r[16];
         tmem_ld16(trow + (uint32_t)cb, r);
         tmem_ld_wait();
@@ -260,7 +262,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       const int n0q = c.nt * npt;
       const int nh = min(npt, n_real - n0q);
       const int chq = c.g * n_real + n0q;
-      for (int cb = half * 16; cb < nh; cb += 32) {
+      for (int cb = half * 16; cb < nh; cb += cstep) {
         uint32_t ll[16], hl[16], lh[16], hh[16];
         tmem_ld16(trow + (uint32_t)cb, ll);
         tmem_ld16(trow + (uint32_t)(npt + cb), hl);
@@ -323,14 +325,14 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
         };
         int cb = half * 16;
         if (cb < n_here) issue(cb, r0, c0);
-        for (; cb < n_here; cb += 64) {
-          const int cb1 = cb + 32;
+        for (; cb < n_here; cb += 2 * cstep) {
+          const int cb1 = cb + cstep;
           tmem_ld_wait(r0);
           if (cb1 < n_here) issue(cb1, r1, c1);
           process(cb, r0, c0);
           if (cb1 >= n_here) break;
           tmem_ld_wait(r1);
-          if (cb1 + 32 < n_here) issue(cb1 + 32, r0, c0);
+          if (cb1 + cstep < n_here) issue(cb1 + cstep, r0, c0);
           process(cb1, r1, c1);
         }
         tc_fence_before();
@@ -339,7 +341,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
         continue;
       }
     }
-    for (int cb = half * 16; cb < n_here; cb += 32) {
+    for (int cb = half * 16; cb < n_here; cb += cstep) {
       uint32_t r[16];
       tmem_ld16(trow + (uint32_t)cb, r);
       tmem_ld_wait();
@@ -421,8 +423,9 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 // Epilogue specialisation switch shared by the three kernels.
 __device__ __forceinline__ void run_epilogue(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full, uint64_t* acc_empty,
                                              int64_t m_groups, int64_t total, int64_t cid, int64_t ncl, int cs,
-                                             int rank, int warp, int lane, uint8_t* lut) {
-#define QNB_EPI(M, F) epilogue_tiles<M, F>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, lut)
+                                             int rank, int warp, int lane, uint8_t* lut, int slot, int nslots) {
+#define QNB_EPI(M, F) \
+  epilogue_tiles<M, F>(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, lut, slot, nslots)
   const int f = (p.rq.s >= 32 ? 1 : 0) | (p.relu.shift_bits + p.relu.shift >= 32 ? 2 : 0);
   switch (p.epi_mode) {
     case EPIM_Q8_FAST_RELU:
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    run_epilogue(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut);
+    run_epilogue(p, tmem, acc_full, acc_empty, m_groups, total, cid, ncl, cs, rank, warp, lane, relu_lut, (warp - 5) >> 2, 2);
   }
 
   tc_fence_before();
@@ -664,8 +667,10 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
 //   warp 0 (lane 0)  producer: B once, then per tile the 2 x kh input rows
 //   warp 4           TMEM allocator + MMA issuer
 //   warps 5-12       epilogue (shared with the general kernel)
+constexpr int kHkThreads = 14 * 32;  // warps 0-3, 5-12 epilogue (3 per TMEM lane quarter), 4 MMA, 13 producer
+constexpr int kHkEpiWarps = 12;
 template <int KIND>
-__global__ void __launch_bounds__(kThreads, 1) igemm_hk_kernel(const __grid_constant__ IgemmArgs p) {
+__global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_constant__ IgemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int b_stage = p.n_rows * 128;
@@ -689,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_hk_kernel(const __grid_cons
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], kEpiWarps);
+      mbar_init(&acc_empty[i], kHkEpiWarps);
     }
     fence_barrier_init();
   }
@@ -702,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_hk_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 13) {
     if (lane == 0) {
       mbar_arrive_expect_tx(b_full, (uint32_t)b_bytes);
       for (int kb = 0; kb < p.num_kb; ++kb)
@@ -749,8 +754,9 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_hk_kernel(const __grid_cons
         __syncwarp();
       }
     }
-  } else if (warp >= 5) {
-    run_epilogue(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut);
+  } else if (warp != 4) {  // epilogue warps 0-3, 5-12
+    run_epilogue(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut,
+                 warp < 4 ? 0 : 1 + ((warp - 5) >> 2), 3);
   }
   tc_fence_before();
   __syncthreads();
@@ -1031,7 +1037,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
       }
     }
   } else if (warp >= 5) {
-    run_epilogue(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut);
+    run_epilogue(p, tmem, acc_full, acc_empty, m_tiles, ct_end, ct0, ct_step, 1, 0, warp, lane, relu_lut, (warp - 5) >> 2, 2);
   }
   tc_fence_before();
   __syncthreads();
@@ -1460,7 +1466,7 @@ static qnb_status launch_hk(const IgemmArgs& a, cudaStream_t s) {
   if (smem > 227 * 1024) return fail(QNB_E_UNSUPPORTED, "row-Hankel tile exceeds shared memory");
   const int64_t tiles = (int64_t)a.hk_pairs * a.oh;
   const int64_t grid = std::min<int64_t>(tiles, num_sms());
-  igemm_hk_kernel<KIND><<<(unsigned)grid, kThreads, smem, s>>>(a);
+  igemm_hk_kernel<KIND><<<(unsigned)grid, kHkThreads, smem, s>>>(a);
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;
