@@ -204,11 +204,11 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
   const bool patch = !hk && use_patch && igemm_patch_eligible(g, io.in);
   const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, io.in) && (g.cg * io.in.es()) % 128 == 0;
-  int32_t pt_pairs = 0;
+  int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, io.in, &pk, &hk_kpr));
   else if (patch)
-    QNB_TRY(igemm_plan_patch(g, io.in, &pk, &pt_pairs));
+    QNB_TRY(igemm_plan_patch(g, io.in, &pk, &pt_pairs, &pt_kb));
   else if (tma)
     QNB_TRY(igemm_plan_tma(g, io.in, &pk));
   else
@@ -218,11 +218,17 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     if (const char* e = getenv("QNB_IP_NPT")) pk.n_per_tile = atoi(e);  // test hook
   }
   int32_t pt_bstat_npt = 0;
-  if (patch && g.kind == KIND_I8 && !std::getenv("QNB_NO_BSTAT")) {
+  int pt_ppst = 1, pt_astg = 2;
+  if (patch) {
     const int64_t wp = io.in.w + 2 * g.pw;
     const int64_t rows = (wp + 125 + g.kw) / wp + g.kh;
-    pt_bstat_npt = igemm_patch_bstat_npt(g, pk.num_kb, (int32_t)(round_up(rows * wp * 16, 128) + 64));
-    if (pt_bstat_npt > 0) pk.n_per_tile = pt_bstat_npt;
+    int npt = 0;
+    const bool bstat = igemm_patch_config(g, pk.num_kb, (int32_t)round_up(rows * wp * pt_kb, 1024), pt_pairs, &npt,
+                                          &pt_ppst, &pt_astg);
+    if (bstat && g.kind == KIND_I8 && !std::getenv("QNB_NO_BSTAT")) {
+      pt_bstat_npt = npt;
+      pk.n_per_tile = npt;
+    }
   }
   QNB_TRY(igemm_pack_b(g, wh.data(), w_dtype, &pk));
 
@@ -246,13 +252,16 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     a.pt_wp = (int32_t)(io.in.w + 2 * g.pw);
     a.pt_hp = (int32_t)(io.in.h + 2 * g.ph);
     a.pt_rows = (int32_t)((a.pt_wp + 125 + g.kw) / a.pt_wp + g.kh);
-    a.pt_plane = (int32_t)(round_up((int64_t)a.pt_rows * a.pt_wp * 16, 128) + 64);  // +64: plane 1 on other banks
+    a.pt_plane = (int32_t)round_up((int64_t)a.pt_rows * a.pt_wp * pt_kb, 1024);  // one 1024-aligned chunk slab
+    a.pt_kb = pt_kb;
     a.pt_pairs = pt_pairs;
     a.pt_kh = (int32_t)g.kh;
     a.pt_kw = (int32_t)g.kw;
     a.pt_cblk = (int32_t)(16 / io.in.es());
     a.pt_nblk = (int32_t)(g.cg * io.in.es() / 16);
     a.pt_bstat = pt_bstat_npt > 0 ? 1 : 0;
+    a.pt_ppst = pt_ppst;
+    a.pt_astg = pt_astg;
   }
   if (tma) {
     a.a_tma = 1;

@@ -867,11 +867,13 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int b_stage = p.n_rows * 128;
-  const int a_stage = 2 * p.pt_plane;
+  const int ppst = p.pt_ppst, AST = p.pt_astg;  // pairs per A stage, A ring depth
+  const int kbA = p.pt_kb;                        // A chunk width (swizzle span)
+  const int a_stage = ppst * p.pt_plane;           // pt_plane: one 1024-aligned chunk slab
   const bool bstat = p.pt_bstat != 0;
   const int SB = bstat ? p.num_kb : p.kb_per_split;  // resident B, or the B ring depth
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (((size_t)kPatchStages * a_stage + 1023) & ~(size_t)1023);  // SW128 B needs 1024-B atoms
+  uint8_t* sB = smem + (((size_t)AST * a_stage + 1023) & ~(size_t)1023);  // SW128 B needs 1024-B atoms
   uint64_t* a_full = (uint64_t*)(sB + (size_t)SB * b_stage);
   uint64_t* a_empty = a_full + kPatchStages;
   uint64_t* b_full = a_empty + kPatchStages;
@@ -901,7 +903,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
   }
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPatchStages; ++i) {
+    for (int i = 0; i < AST; ++i) {
       mbar_init(&a_full[i], 128);  // one cp.async arrival per producer thread
       mbar_init(&a_empty[i], 1);
     }
@@ -930,7 +932,9 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
     // reads one pixel's 32 contiguous bytes; thread 0 also moves B (once if resident).
     const int t = threadIdx.x;
     const int64_t y_tot = (p.m_total / ((int64_t)p.oh * p.ow)) * p.pt_hp;  // rows of the merged N*H_p grid
-    const int chunks = 2 * p.pt_rows * p.pt_wp;
+    const int nsub_sh = kbA == 128 ? 3 : (kbA == 64 ? 2 : 1);  // 16-byte sub-chunks per slab row: 8 / 4 / 2
+    const int items = (p.pt_rows * p.pt_wp) << nsub_sh;
+    const int ksteps_chunk = taps * (kbA >> 5);
     if (bstat && t == 0 && ct0 < ct_end) {
       const TileCoord c = tile_of(ct0, m_tiles, p.n_tiles);
       const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
@@ -945,21 +949,29 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
       const uint32_t y0 = P0 / (uint32_t)p.pt_wp;
       const uint8_t* btile = p.b + (int64_t)(c.g * p.n_tiles + c.nt) * p.num_kb * b_stage;
       int kb = 0;
-      for (int j = 0; j < p.pt_pairs; ++j, ++ia) {
-        const int s = (int)(ia % kPatchStages);
-        mbar_wait(&a_empty[s], ((ia / kPatchStages) & 1) ^ 1);
-        const int64_t cbyte = (int64_t)(c.g * p.pt_nblk + 2 * j) * 16;  // first block of the pair
-        uint8_t* dst = sA + (size_t)s * a_stage;
-        for (int i = t; i < chunks; i += 128) {
-          const uint32_t q = (uint32_t)i >> 1, b = (uint32_t)i & 1u;
-          const uint32_t dy = q / (uint32_t)p.pt_wp, x = q - dy * (uint32_t)p.pt_wp;
-          int64_t y = (int64_t)y0 + dy;
-          y = y < y_tot ? y : y_tot - 1;  // rows past the last image only feed discarded outputs
-          cp_async_16(dst + b * p.pt_plane + q * 16, p.a + y * p.a_row + (int64_t)x * p.a_pix + cbyte + b * 16);
+      for (int j0 = 0; j0 < p.pt_pairs; j0 += ppst, ++ia) {
+        const int s = (int)(ia % AST);
+        mbar_wait(&a_empty[s], ((ia / AST) & 1) ^ 1);
+        const int nch = min(ppst, p.pt_pairs - j0);
+        for (int jj = 0; jj < nch; ++jj) {
+          // slab row q = patch pixel q holds channel bytes [c0, c0 + kbA); its 16-byte
+          // sub-chunk j sits at j ^ swz(q): the absolute-address swizzle the UMMA reads, so
+          // a descriptor may start at any row (filter tap offset r * wp + s)
+          const int64_t cbyte = (int64_t)c.g * p.a_group + (int64_t)(j0 + jj) * kbA;
+          uint8_t* dst = sA + (size_t)s * a_stage + (size_t)jj * p.pt_plane;
+          for (int i = t; i < items; i += 128) {
+            const uint32_t q = (uint32_t)i >> nsub_sh, jc = (uint32_t)i & ((1u << nsub_sh) - 1u);
+            const uint32_t dy = q / (uint32_t)p.pt_wp, x = q - dy * (uint32_t)p.pt_wp;
+            int64_t y = (int64_t)y0 + dy;
+            y = y < y_tot ? y : y_tot - 1;  // rows past the last image only feed discarded outputs
+            const uint32_t swz = nsub_sh == 3 ? (q & 7u) : (nsub_sh == 2 ? ((q >> 1) & 3u) : ((q >> 2) & 1u));
+            cp_async_16(dst + (size_t)q * kbA + ((jc ^ swz) << 4),
+                        p.a + y * p.a_row + (int64_t)x * p.a_pix + cbyte + jc * 16);
+          }
         }
         cp_async_arrive_noinc(&a_full[s]);
         if (!bstat && t == 0) {
-          const int kb_end = ((j + 1) * taps + 3) / 4;
+          const int kb_end = ((j0 + nch) * ksteps_chunk + 3) / 4;
           for (; kb < kb_end && kb < p.num_kb; ++kb, ++ib) {
             const int sb = (int)(ib % SB);
             mbar_wait(&b_empty[sb], ((ib / SB) & 1) ^ 1);
@@ -989,43 +1001,49 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
         tc_fence_after();
         const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
         int k = 0;  // K step within the tile
-        for (int j = 0; j < p.pt_pairs; ++j, ++ia) {
-          const int s = (int)(ia % kPatchStages);
-          mbar_wait(&a_full[s], (ia / kPatchStages) & 1);
+        const int nk = kbA >> 5;  // K steps per (tap, chunk)
+        const uint32_t row_units = (uint32_t)(kbA >> 4);  // descriptor units per slab row
+        for (int j0 = 0; j0 < p.pt_pairs; j0 += ppst, ++ia) {
+          const int s = (int)(ia % AST);
+          mbar_wait(&a_full[s], (ia / AST) & 1);
           tc_fence_after();
-          const uint64_t ad0 = smem_desc_none(sA + (size_t)s * a_stage, (uint32_t)p.pt_plane, 128) + off0;
-          if (bstat) {
-            const uint64_t bd0 = smem_desc_sw128(sB);
-            if (elect_one()) {
-              int kk = k;
-              if (mma_on)
-                for (int r = 0; r < p.pt_kh; ++r)
-                  for (int t = 0; t < p.pt_kw; ++t, ++kk)
-                    umma<KIND>(dt, ad0 + (uint32_t)(r * wp + t), bd0 + (uint32_t)(kk >> 2) * b_units + 2 * (kk & 3),
-                               idesc, kk != 0);
-              tc_commit(&a_empty[s]);
-            }
-            __syncwarp();
-            k += p.pt_kh * p.pt_kw;
-          } else {
-            for (int r = 0; r < p.pt_kh; ++r)
-              for (int t = 0; t < p.pt_kw; ++t, ++k) {
-                const int sb = (int)(ib % SB);
-                if ((k & 3) == 0) {
-                  mbar_wait(&b_full[sb], (ib / SB) & 1);
-                  tc_fence_after();
-                }
-                const uint64_t bd = smem_desc_sw128(sB + (size_t)sb * b_stage) + 2 * (k & 3);
-                if (elect_one()) {
-                  if (mma_on) umma<KIND>(dt, ad0 + (uint32_t)(r * wp + t), bd, idesc, k != 0);
-                  if ((k & 3) == 3) tc_commit(&b_empty[sb]);
-                }
-                __syncwarp();
-                if ((k & 3) == 3) ++ib;
+          const int nch = min(ppst, p.pt_pairs - j0);
+          for (int jj = 0; jj < nch; ++jj) {
+            const uint64_t ad0 = smem_desc_sw(sA + (size_t)s * a_stage + (size_t)jj * p.pt_plane, kbA) + off0 * row_units;
+            if (bstat) {
+              const uint64_t bd0 = smem_desc_sw128(sB);
+              if (elect_one()) {
+                int kk = k;
+                if (mma_on)
+                  for (int r = 0; r < p.pt_kh; ++r)
+                    for (int t = 0; t < p.pt_kw; ++t)
+                      for (int q = 0; q < nk; ++q, ++kk)
+                        umma<KIND>(dt, ad0 + (uint32_t)(r * wp + t) * row_units + 2 * q,
+                                   bd0 + (uint32_t)(kk >> 2) * b_units + 2 * (kk & 3), idesc, kk != 0);
               }
-            if (elect_one()) tc_commit(&a_empty[s]);
-            __syncwarp();
+              __syncwarp();
+              k += p.pt_kh * p.pt_kw * nk;
+            } else {
+              for (int r = 0; r < p.pt_kh; ++r)
+                for (int t = 0; t < p.pt_kw; ++t)
+                  for (int q = 0; q < nk; ++q, ++k) {
+                    const int sb = (int)(ib % SB);
+                    if ((k & 3) == 0) {
+                      mbar_wait(&b_full[sb], (ib / SB) & 1);
+                      tc_fence_after();
+                    }
+                    const uint64_t bd = smem_desc_sw128(sB + (size_t)sb * b_stage) + 2 * (k & 3);
+                    if (elect_one()) {
+                      if (mma_on) umma<KIND>(dt, ad0 + (uint32_t)(r * wp + t) * row_units + 2 * q, bd, idesc, k != 0);
+                      if ((k & 3) == 3) tc_commit(&b_empty[sb]);
+                    }
+                    __syncwarp();
+                    if ((k & 3) == 3) ++ib;
+                  }
+            }
           }
+          if (elect_one()) tc_commit(&a_empty[s]);  // the whole A stage (all its chunks) consumed
+          __syncwarp();
         }
         if (!bstat && (k & 3)) {  // partially used last B stage
           if (elect_one()) tc_commit(&b_empty[(int)(ib % SB)]);
@@ -1048,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
 }
 
 static size_t igemm_patch_smem_bytes(const IgemmArgs& a, int sb) {
-  return 1024 + (((size_t)kPatchStages * 2 * a.pt_plane + 1023) & ~(size_t)1023) + (size_t)sb * a.n_rows * 128 +
+  return 1024 + (size_t)a.pt_astg * a.pt_ppst * a.pt_plane + (size_t)sb * a.n_rows * 128 +
          (2 * kPatchStages + 2 * kMaxStages + 4) * 8 + 16 + 256;
 }
 
@@ -1061,45 +1079,71 @@ bool igemm_patch_eligible(const IgemmGeometry& g, const ActLayout& in) {
   if (wp > 256 || g.kh > 32 || g.kw > 32) return false;
   const int64_t rows = (wp + kBM - 3 + g.kw) / wp + g.kh;
   if (rows > 256) return false;
-  const int64_t plane = round_up(rows * wp * 16, 128);
-  if (2 * kPatchStages * (plane + 64) > 120 * 1024) return false;
+  if (g.kind != KIND_I8) return false;  // unused chunk bytes meet zero weights; float garbage could be NaN
+  if (2 * round_up(rows * wp * 32, 1024) > 120 * 1024) return false;  // two stages of the narrowest chunk
   return true;
 }
 
-qnb_status igemm_plan_patch(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* pairs_out) {
-  const int64_t es = in.es();
-  const int64_t per_blk = 16 / es;                  // channels per 16-byte block
-  const int64_t nblk = (g.cg * es) / 16;
-  const int64_t pairs = (nblk + 1) / 2;
-  std::vector<int64_t> kmap;
-  for (int64_t j = 0; j < pairs; ++j)
+qnb_status igemm_plan_patch(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* chunks_out,
+                            int32_t* kb_out) {
+  const int64_t es = in.es(), cgb = g.cg * es;
+  // A chunk width: the swizzle span that wastes the fewest K bytes per tap (ties: wider)
+  int kb = 128;
+  int64_t best = ceil_div(cgb, 128) * 128;
+  for (int cand : {64, 32}) {
+    const int64_t w = ceil_div(cgb, cand) * cand;
+    if (w < best) {
+      best = w;
+      kb = cand;
+    }
+  }
+  const int64_t nchunk = ceil_div(cgb, kb);
+  std::vector<int64_t> kmap;  // K steps (chunk, r, s, 32-byte step), 32 bytes each
+  for (int64_t cc = 0; cc < nchunk; ++cc)
     for (int64_t r = 0; r < g.kh; ++r)
       for (int64_t s = 0; s < g.kw; ++s)
-        for (int64_t e = 0; e < 32 / es; ++e) {   // one K step: block 2j then block 2j+1
-          const int64_t blk = 2 * j + (e * es) / 16;
-          const int64_t c = blk * per_blk + (e * es % 16) / es;
+        for (int64_t b = 0; b < kb; b += es) {
+          const int64_t c = (cc * kb + b) / es;
           kmap.push_back(c < g.cg ? (c * g.kh + r) * g.kw + s : -1);
         }
   while (kmap.size() % (size_t)(128 / es) != 0) kmap.push_back(-1);
   pk->kmap = std::move(kmap);
   pk->num_kb = (int32_t)(pk->kmap.size() / (size_t)(128 / es));
   pk->chunk_off.assign((size_t)pk->num_kb * 8, 0);
-  pk->kbytes = 128;
-  *pairs_out = (int32_t)pairs;
+  pk->kbytes = 128;  // B stages stay 128-byte SW128 (4 K steps each)
+  *chunks_out = (int32_t)nchunk;
+  *kb_out = kb;
   return QNB_OK;
 }
 
-// Largest n-tile width (real output channels) whose whole B (num_kb stages of
-// round_up(npt + 1, 16) rows) fits in shared memory next to the patch ring; 0 = none.
-int igemm_patch_bstat_npt(const IgemmGeometry& g, int64_t num_kb, int32_t plane) {
-  const size_t a_bytes = ((size_t)kPatchStages * 2 * plane + 1023) & ~(size_t)1023;
+// Patch-mode configuration: the widest n-tile whose whole B can stay resident next
+// to an A ring of >= 2 stages, each stage holding as many channel-block pairs as fit
+// (ideally the whole tile patch, so one barrier round trip covers all its taps).
+// Returns false (streamed B) when no resident configuration fits.
+bool igemm_patch_config(const IgemmGeometry& g, int64_t num_kb, int32_t plane, int32_t pairs, int* npt_out,
+                        int* ppst_out, int* astg_out) {
+  const size_t budget = 214 * 1024;
   for (int npt : {240, 192, 128, 112, 96, 64, 48, 32}) {
     if (npt > round_up(g.og, 16) && npt != 32) continue;
-    const int64_t nrows = round_up(npt + 1, 16);
-    const size_t bytes = 1024 + a_bytes + (size_t)num_kb * nrows * 128 + 1024;
-    if (bytes <= 220 * 1024) return npt;
+    const size_t b = (size_t)num_kb * round_up(npt + 1, 16) * 128;
+    if (b + 4096 >= budget) continue;
+    const size_t room = budget - b - 4096;
+    const size_t pair_bytes = (size_t)plane;  // one channel-chunk slab
+    int ppst = (int)std::min<size_t>((size_t)pairs, room / (2 * pair_bytes));
+    if (ppst < 1) continue;
+    const int astg = (int)std::min<size_t>(4, room / (pair_bytes * ppst));
+    if (astg < 2) continue;
+    *npt_out = npt;
+    *ppst_out = ppst;
+    *astg_out = astg;
+    return true;
   }
-  return 0;
+  *npt_out = 0;
+  const size_t room = 120 * 1024;  // streamed B: A ring shares smem with the B ring
+  const int ppst = (int)std::max<size_t>(1, std::min<size_t>((size_t)pairs, room / (2 * (size_t)plane)));
+  *ppst_out = ppst;
+  *astg_out = (int)std::max<size_t>(2, std::min<size_t>(4, room / ((size_t)plane * ppst)));
+  return false;
 }
 
 static size_t igemm_hk_smem_bytes(const IgemmArgs& a) {

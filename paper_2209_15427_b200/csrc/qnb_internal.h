@@ -153,6 +153,8 @@ struct IgemmArgs {
   // pt_bstat = 1: the whole B of one (group, n-tile) stays resident in smem; each CTA
   // owns one such combination and walks its pixel tiles (weights leave L2 once per CTA).
   int32_t pt_bstat;
+  int32_t pt_ppst, pt_astg;  // channel chunks per A stage, A stages in the ring (<= 4)
+  int32_t pt_kb;             // channel-chunk width in bytes (128 / 64 / 32 = the A swizzle span)
 };
 // Row-Hankel mode: the input is image-pair interleaved with 1024-byte row slots, so
 // one tile (output row oy of images 2q and 2q+1) needs input rows
@@ -217,8 +219,10 @@ qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const u
 // Patch mode (see IgemmArgs::patch): eligibility and K map (K steps ordered
 // (channel-block pair, tap), 32 bytes each, 4 per 128-byte B stage).
 bool igemm_patch_eligible(const IgemmGeometry& g, const ActLayout& in);
-qnb_status igemm_plan_patch(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* pairs);
-int igemm_patch_bstat_npt(const IgemmGeometry& g, int64_t num_kb, int32_t plane);
+qnb_status igemm_plan_patch(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk, int32_t* chunks,
+                            int32_t* chunk_bytes);
+bool igemm_patch_config(const IgemmGeometry& g, int64_t num_kb, int32_t plane, int32_t pairs, int* npt, int* ppst,
+                        int* astg);
 
 // Row-Hankel eligibility (see IgemmArgs::hk) and its K map / stage count.
 bool hk_geometry_ok(const IgemmGeometry& g, const ActLayout& in);

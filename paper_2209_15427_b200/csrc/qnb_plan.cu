@@ -524,22 +524,28 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
   const bool patch = !hk && use_patch && igemm_patch_eligible(g, Lin);
   const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % 128 == 0;
-  int32_t pt_pairs = 0;
+  int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, Lin, &pk, &hk_kpr));
   else if (patch)
-    QNB_TRY(igemm_plan_patch(g, Lin, &pk, &pt_pairs));
+    QNB_TRY(igemm_plan_patch(g, Lin, &pk, &pt_pairs, &pt_kb));
   else if (tma)
     QNB_TRY(igemm_plan_tma(g, Lin, &pk));
   else
     QNB_TRY(igemm_plan_k(g, Lin, &pk));
   if (g.is_fc && !quant) pk.n_per_tile = 128;
   int32_t pt_bstat_npt = 0;
-  if (patch && g.kind == KIND_I8 && !std::getenv("QNB_NO_BSTAT")) {
+  int pt_ppst = 1, pt_astg = 2;
+  if (patch) {
     const int64_t wp = Lin.w + 2 * g.pw;
     const int64_t rows = (wp + 125 + g.kw) / wp + g.kh;
-    pt_bstat_npt = igemm_patch_bstat_npt(g, pk.num_kb, (int32_t)(round_up(rows * wp * 16, 128) + 64));
-    if (pt_bstat_npt > 0) pk.n_per_tile = pt_bstat_npt;
+    int npt = 0;
+    const bool bstat = igemm_patch_config(g, pk.num_kb, (int32_t)round_up(rows * wp * pt_kb, 1024), pt_pairs, &npt,
+                                          &pt_ppst, &pt_astg);
+    if (bstat && g.kind == KIND_I8 && !std::getenv("QNB_NO_BSTAT")) {
+      pt_bstat_npt = npt;
+      pk.n_per_tile = npt;
+    }
   }
   QNB_TRY(igemm_pack_b(g, l.weight, l.weight_dtype, &pk));
   IgemmArgs& a = st.ig;
@@ -562,13 +568,16 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     a.pt_wp = (int32_t)(Lin.w + 2 * g.pw);
     a.pt_hp = (int32_t)(Lin.h + 2 * g.ph);
     a.pt_rows = (int32_t)((a.pt_wp + 125 + g.kw) / a.pt_wp + g.kh);
-    a.pt_plane = (int32_t)(round_up((int64_t)a.pt_rows * a.pt_wp * 16, 128) + 64);  // +64: plane 1 on other banks
+    a.pt_plane = (int32_t)round_up((int64_t)a.pt_rows * a.pt_wp * pt_kb, 1024);  // one 1024-aligned chunk slab
+    a.pt_kb = pt_kb;
     a.pt_pairs = pt_pairs;
     a.pt_kh = (int32_t)g.kh;
     a.pt_kw = (int32_t)g.kw;
     a.pt_cblk = (int32_t)(16 / Lin.es());
     a.pt_nblk = (int32_t)(g.cg * Lin.es() / 16);
     a.pt_bstat = pt_bstat_npt > 0 ? 1 : 0;
+    a.pt_ppst = pt_ppst;
+    a.pt_astg = pt_astg;
   }
   if (tma) {
     a.a_tma = 1;
