@@ -176,6 +176,70 @@ __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, cons
   return (uint32_t)min(max(q + k.oz, k.omin), k.omax);
 }
 
+// Fused split-K fixup (serial reduction, CUTLASS "stream-K fixup" style): every CTA of a
+// tile writes its s32 partial to p.ws; the 256 epilogue threads then bump the tile's
+// arrival counter once, and the CTA that arrives last sums the ksplit partials (exact,
+// order-free integer adds, read back from L2) and applies the INT8 epilogue for the
+// tile, then resets the counter for the next forward.
+__device__ __noinline__ void splitk_fixup(const IgemmArgs& p, int64_t mt, int nt, const Q8Consts& k, int32_t* flag) {
+  const int et = threadIdx.x - 5 * 32;  // 0 .. 255 across the epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  int32_t* sema = p.tile_sema + mt * p.n_tiles + nt;
+  if (et == 0) {
+    __threadfence();
+    const int old = atomicAdd(sema, 1);
+    *flag = old == p.ksplit - 1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  if (!*flag) return;
+  __threadfence();
+  const int n0 = nt * p.n_per_tile;
+  const int n_here = min(p.n_per_tile, p.n_real - n0);
+  const int quads = (n_here + 3) >> 2;
+  const int64_t row_stride = (int64_t)p.n_tiles * p.n_rows;
+  const int64_t split_stride = p.m_total * row_stride;
+  const int64_t r0 = mt * kBM;
+  const int rows = (int)(p.m_total - r0 < kBM ? p.m_total - r0 : kBM);
+  for (int i = et; i < rows * quads; i += kEpiWarps * 32) {
+    const int rr = i / quads, j = (i - rr * quads) * 4;
+    const int64_t row = r0 + rr;
+    const int32_t* w = p.ws + row * row_stride + (int64_t)nt * p.n_rows;
+    int32_t d[4] = {0, 0, 0, 0};
+    int32_t rs = 0;
+    for (int ks = 0; ks < p.ksplit; ++ks) {
+      const int32_t* wsp = w + ks * split_stride;
+      const int4 v = __ldcg(reinterpret_cast<const int4*>(wsp + j));
+      d[0] += v.x;
+      d[1] += v.y;
+      d[2] += v.z;
+      d[3] += v.w;
+      rs += __ldcg(wsp + p.ones_col);
+    }
+    const int o0 = n0 + j;
+    uint8_t* dst = p.out + row * p.o_img + p.o_origin + o0;  // inner product: oh = ow = 1
+    uint32_t packed = 0;
+    const int cnt = min(4, p.n_real - o0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u >= cnt) break;
+      int64_t q;
+      if (p.fast_rq && p.chan_const32) {
+        q = q8_fast<false, 0>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, ReluFastK{});
+      } else {
+        q = requant_clamp((int64_t)d[u] + p.chan_const[o0 + u] - p.zw * (int64_t)rs, p.rq);
+      }
+      if (p.has_relu) q = p.relu_lut ? (int64_t)p.relu_lut[q] : relu_requant(q, p.relu);
+      packed |= ((uint32_t)q & 0xFFu) << (8 * u);
+    }
+    if (cnt == 4 && ((uintptr_t)dst & 3) == 0) {
+      *reinterpret_cast<uint32_t*>(dst) = packed;
+    } else {
+      for (int u = 0; u < cnt; ++u) dst[u] = (uint8_t)(packed >> (8 * u));
+    }
+  }
+  if (et == 0) *sema = 0;  // self-reset (graph replays reuse the counters)
+}
+
 template <int MODE, int F = 0>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
                                                uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
@@ -250,6 +314,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (p.tile_sema != nullptr) splitk_fixup(p, mt, c.nt, k, reinterpret_cast<int32_t*>(lut));
       continue;
     }
     if constexpr (MODE == EPIM_Q16) {

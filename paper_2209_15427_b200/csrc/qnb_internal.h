@@ -115,6 +115,10 @@ struct IgemmArgs {
   // igemm_finalize applies the epilogue.
   int32_t ksplit, kb_per_split;
   int32_t* ws;
+  // fused split-K fixup: per (m-tile, n-tile) arrival counters (zeroed, self-resetting);
+  // the last CTA of a tile to finish sums the partials and runs the INT8 epilogue, so no
+  // separate igemm_finalize launch is needed
+  int32_t* tile_sema;
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)

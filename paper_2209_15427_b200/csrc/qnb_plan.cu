@@ -669,6 +669,13 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
       void* ws = nullptr;
       QNB_TRY(dev_alloc(P, &ws, (size_t)a.ksplit * P.max_batch * pk.n_tiles * pk.n_rows * 4));
       a.ws = (int32_t*)ws;
+      if (std::getenv("QNB_FUSED_FIXUP")) {  // opt-in: serial last-CTA fixup (measured slower: 1 CTA reduces a tile)
+        const size_t n_sema = (size_t)ceil_div(P.max_batch, 128) * pk.n_tiles;
+        void* sema = nullptr;
+        QNB_TRY(dev_alloc(P, &sema, n_sema * 4));
+        QNB_CUDA(cudaMemset(sema, 0, n_sema * 4));
+        a.tile_sema = (int32_t*)sema;
+      }
     }
   }
   a.out = blob_ptr(P, op.out);
@@ -864,7 +871,7 @@ qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cuda
         case OP_IGEMM:
           QNB_TRY(igemm_launch(st.mma_kind, st.ig, st.groups, s));
           g_launches.fetch_sub(1);  // counted below with the others
-          if (st.ig.ksplit > 1) {
+          if (st.ig.ksplit > 1 && st.ig.tile_sema == nullptr) {
             QNB_TRY(igemm_finalize(st.ig, s));
             g_launches.fetch_sub(1);
           }
@@ -948,7 +955,7 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
   QNB_TRY(emit(*P));
   P->launches_per_forward = (int64_t)P->steps.size();
   for (const Step& st : P->steps)
-    if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1) ++P->launches_per_forward;
+    if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1 && st.ig.tile_sema == nullptr) ++P->launches_per_forward;
   QNB_CUDA(cudaDeviceSynchronize());
   // output description (reference layout)
   const Blob& sk = P->blobs[P->sink_blob];
