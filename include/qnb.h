@@ -172,10 +172,15 @@ qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, 
 /* Expert dispatch for PER_SAMPLE MoE (src/moe.cpp:220-251), device side.
  * qnb_moe_route: groups the batch*top_k (sample, expert) pairs of `idx` per expert
  * (stable: (sample, k) order inside an expert).  counts[n_experts]; pair_sample[p] =
- * sample of the p-th grouped pair; pair_slot[s*top_k + k] = its grouped position. */
-qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64_t n_experts, int64_t* counts,
-                         int64_t* pair_sample, int64_t* pair_slot, qnb_stream s);
-/* dst[i] = src[rows[i]] for n rows of row_bytes bytes (device pointers). */
+ * sample of the p-th grouped pair; pair_slot[s*top_k + k] = its grouped position.
+ * segment_pad = 0: segments are dense.  segment_pad >= batch: expert e's rows start at
+ * e*segment_pad (fixed addresses, so per-expert CUDA graphs replay) and its unused rows
+ * get pair_sample = -1; pair_sample then holds n_experts*segment_pad entries.
+ * qnb_gather_rows skips rows < 0. */
+qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64_t n_experts, int64_t segment_pad,
+                         int64_t* counts, int64_t* pair_sample, int64_t* pair_slot, qnb_stream s);
+/* dst[i] = src[rows[i]] for n rows of row_bytes bytes (device pointers); rows[i] < 0
+ * leaves dst row i untouched. */
 qnb_status qnb_gather_rows(const void* src, int64_t row_bytes, const int64_t* rows, int64_t n, void* dst,
                            qnb_stream s);
 /* Mixing loop of moe_forward (src/moe.cpp:240-249) over grouped expert output rows

@@ -266,7 +266,7 @@ __global__ void moe_combine_kernel(const float* __restrict__ eo, int64_t B, int6
 // expert runs on one contiguous sub-batch.  One CTA; thread e owns expert e, so the
 // order is deterministic without atomics.  B*K is small (1024 for AlexNet-MoE).
 constexpr int kRouteMaxExperts = 256;
-__global__ void moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, int64_t K, int64_t E,
+__global__ void moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, int64_t K, int64_t E, int64_t pad,
                                  int64_t* __restrict__ counts, int64_t* __restrict__ pair_sample,
                                  int64_t* __restrict__ pair_slot) {
   __shared__ int64_t cnt[kRouteMaxExperts], off[kRouteMaxExperts];
@@ -280,7 +280,7 @@ __global__ void moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, in
   if (e == 0) {
     int64_t o = 0;
     for (int64_t i = 0; i < E; ++i) {
-      off[i] = o;
+      off[i] = pad > 0 ? i * pad : o;  // pad > 0: fixed per-expert segments of `pad` rows
       o += cnt[i];
     }
   }
@@ -293,6 +293,8 @@ __global__ void moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, in
         pair_slot[p] = pos;
         ++pos;
       }
+    if (pad > 0)
+      for (int64_t q = pos; q < off[e] + pad; ++q) pair_sample[q] = -1;  // unused rows: the gather skips them
     counts[e] = cnt[e];
   }
 }
@@ -303,7 +305,8 @@ __global__ void gather_rows16_kernel(const uint4* __restrict__ src, int64_t row_
   const int64_t total = n * row_vec;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = o / row_vec, j = o - i * row_vec;
-    dst[o] = __ldg(src + __ldg(rows + i) * row_vec + j);
+    const int64_t r = __ldg(rows + i);
+    if (r >= 0) dst[o] = __ldg(src + r * row_vec + j);
   }
 }
 __global__ void gather_rows1_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
@@ -311,7 +314,7 @@ __global__ void gather_rows1_kernel(const uint8_t* __restrict__ src, int64_t row
   const int64_t total = n * row_bytes;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = o / row_bytes, j = o - i * row_bytes;
-    dst[o] = src[rows[i] * row_bytes + j];
+    if (rows[i] >= 0) dst[o] = src[rows[i] * row_bytes + j];
   }
 }
 
@@ -571,14 +574,15 @@ qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, 
   return QNB_OK;
 }
 
-qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64_t n_experts, int64_t* counts,
-                         int64_t* pair_sample, int64_t* pair_slot, qnb_stream s) {
+qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64_t n_experts, int64_t segment_pad,
+                         int64_t* counts, int64_t* pair_sample, int64_t* pair_slot, qnb_stream s) {
   QNB_TRY(ensure_device());
   if (n_experts < 1 || n_experts > kRouteMaxExperts) return fail(QNB_E_UNSUPPORTED, "1..256 experts supported");
   if (top_k < 1 || top_k > n_experts) return fail(QNB_E_ARG, "top_k out of range");
   if (batch < 0) return fail(QNB_E_SHAPE, "shape mismatch");
-  moe_route_kernel<<<1, kRouteMaxExperts, 0, as_stream(s)>>>(idx, batch * top_k, top_k, n_experts, counts,
-                                                             pair_sample, pair_slot);
+  if (segment_pad < 0 || (segment_pad > 0 && segment_pad < batch)) return fail(QNB_E_ARG, "segment_pad below batch");
+  moe_route_kernel<<<1, kRouteMaxExperts, 0, as_stream(s)>>>(idx, batch * top_k, top_k, n_experts, segment_pad,
+                                                             counts, pair_sample, pair_slot);
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;

@@ -127,6 +127,18 @@ struct qnb_plan {
   void* in_staging = nullptr;
   void* out_staging = nullptr;
   // captured graph
+  // graph cache: one instantiated forward per (input, output, batch, host flags); the MoE
+  // executor replays expert plans at a few bucketed batch sizes
+  struct GraphEntry {
+    const void* in;
+    void* out;
+    int64_t batch;
+    int32_t flags;
+    cudaGraphExec_t exec;
+    uint64_t last_use;
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t graph_clock = 0;
   cudaGraphExec_t exec = nullptr;
   const void* g_in = nullptr;
   void* g_out = nullptr;
@@ -1051,10 +1063,16 @@ qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32
   // pageable host buffers cannot be captured: run those forwards eagerly
   if (P->use_graph && (!input_on_host || pinned_in) && pinned_out) {
     const int32_t flags = (input_on_host ? 1 : 0) | (output_on_host ? 2 : 0);
-    if (!P->exec || P->g_in != input || P->g_out != output || P->g_batch != batch || P->g_flags != flags) {
-      if (P->exec) {
-        cudaGraphExecDestroy(P->exec);
-        P->exec = nullptr;
+    qnb_plan::GraphEntry* hit = nullptr;
+    for (auto& ge : P->graphs)
+      if (ge.in == input && ge.out == output && ge.batch == batch && ge.flags == flags) hit = &ge;
+    if (!hit) {
+      constexpr size_t kMaxGraphs = 16;
+      if (P->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+        auto lru = std::min_element(P->graphs.begin(), P->graphs.end(),
+                                    [](const qnb_plan::GraphEntry& a, const qnb_plan::GraphEntry& b) { return a.last_use < b.last_use; });
+        cudaGraphExecDestroy(lru->exec);
+        P->graphs.erase(lru);
       }
       cudaGraph_t graph;
       if (!P->capture_stream) QNB_CUDA(cudaStreamCreateWithFlags(&P->capture_stream, cudaStreamNonBlocking));
@@ -1064,14 +1082,15 @@ qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32
       cudaError_t e = cudaStreamEndCapture(P->capture_stream, &graph);
       if (st != QNB_OK) return st;
       if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-      e = cudaGraphInstantiate(&P->exec, graph, 0);
+      cudaGraphExec_t ex = nullptr;
+      e = cudaGraphInstantiate(&ex, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-      P->g_in = input;
-      P->g_out = output;
-      P->g_batch = batch;
-      P->g_flags = flags;
+      P->graphs.push_back(qnb_plan::GraphEntry{input, output, batch, flags, ex, 0});
+      hit = &P->graphs.back();
     }
+    hit->last_use = ++P->graph_clock;
+    P->exec = hit->exec;
     QNB_CUDA(cudaGraphLaunch(P->exec, s));
   } else {
     QNB_TRY(forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in, s));
@@ -1150,7 +1169,7 @@ qnb_status qnb_plan_profile(qnb_plan* P, const void* input, int64_t batch, void*
 
 qnb_status qnb_plan_destroy(qnb_plan* P) {
   if (!P) return QNB_OK;
-  if (P->exec) cudaGraphExecDestroy(P->exec);
+  for (auto& ge : P->graphs) cudaGraphExecDestroy(ge.exec);
   if (P->capture_stream) cudaStreamDestroy(P->capture_stream);
   if (P->copy_stream) cudaStreamDestroy(P->copy_stream);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);

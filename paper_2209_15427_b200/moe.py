@@ -132,6 +132,8 @@ class ExpertExchange:
 class MoeNet:
     """qnet::Net surface for a graph with one MOE layer, backed by B200 plans."""
 
+    BUCKET = 32
+
     def __init__(self, graph: dict, rank: int = 0, world: int = 1):
         self.graph = G.normalized(graph)
         trunk, moe, tail = split_moe_graph(self.graph)
@@ -217,7 +219,8 @@ class MoeNet:
             "trunk": self.trunk.compile(B),
             "gating": self.gating.compile(B),
             "tail": self.tail.compile(B),
-            "experts": {e: self.experts[e].compile(cap, use_cuda_graph=False)
+            # expert plans replay CUDA graphs at bucketed batch sizes (multiples of 32)
+            "experts": {e: self.experts[e].compile(cap, use_cuda_graph=True)
                         for e in range(self.rank * self.per_rank, (self.rank + 1) * self.per_rank)},
             "D": D, "per": per, "row_elems": row_elems, "in_shape": in_shape,
             "in_dtype": G.DTYPE_CODE[self.moe_layer["bottom_data_type"]],
@@ -234,11 +237,14 @@ class MoeNet:
             "idx": torch.empty(P, dtype=torch.int64, device=dev),
             "w": torch.empty(P, dtype=torch.float32, device=dev),
             "counts": torch.empty(self.n_experts, dtype=torch.int64, device=dev),
-            "pair_sample": torch.empty(P, dtype=torch.int64, device=dev),
+            "pair_sample": torch.empty(max(P, self.n_experts * (cap + self.BUCKET)), dtype=torch.int64, device=dev),
             "pair_slot": torch.empty(P, dtype=torch.int64, device=dev),
-            "S": torch.empty((P, row_elems * es), dtype=torch.uint8, device=dev),
-            "X": torch.empty(cap * self.per_rank * row_elems, dtype=torch.float32, device=dev),
-            "Y": torch.empty((cap * self.per_rank, per), dtype=torch.float32, device=dev),
+            "S": torch.empty((max(P, self.n_experts * (cap + self.BUCKET)), row_elems * es), dtype=torch.uint8,
+                             device=dev),
+            # + kBucket rows: an expert's bucketed batch may run past its segment (read-only
+            # spill into the next expert's rows, whose outputs are written after it)
+            "X": torch.empty((self.per_rank * (cap + self.BUCKET)) * row_elems, dtype=torch.float32, device=dev),
+            "Y": torch.empty((self.per_rank * (cap + self.BUCKET), per), dtype=torch.float32, device=dev),
             "M": torch.empty(B * per * NP_OF[p["top_dtype"]]().itemsize, dtype=torch.uint8, device=dev),
             "wa": torch.from_numpy(self.gates["gate_a"]).to(dev),
             "wb": torch.from_numpy(self.gates["gate_b"]).to(dev),
@@ -277,9 +283,13 @@ class MoeNet:
         check(lib.qnb_moe_gate(b["feats"].data_ptr(), B, p["D"], b["wa"].data_ptr(), b["wb"].data_ptr(),
                                b["wc"].data_ptr(), self.n_experts, self.top_k, 1 if self.noise else 0,
                                C.c_uint64(self.seed), b["idx"].data_ptr(), b["w"].data_ptr(), sp))
-        check(lib.qnb_moe_route(b["idx"].data_ptr(), B, self.top_k, self.n_experts, b["counts"].data_ptr(),
+        # one rank: fixed per-expert segments (stride B + BUCKET rows) -> every expert's plan
+        # replays a cached CUDA graph at a bucketed batch size, concurrently on its own
+        # stream; N ranks: dense rows (the all-to-all splits count real pairs)
+        stride = B + self.BUCKET if self.world == 1 else 0
+        check(lib.qnb_moe_route(b["idx"].data_ptr(), B, self.top_k, self.n_experts, stride, b["counts"].data_ptr(),
                                 b["pair_sample"].data_ptr(), b["pair_slot"].data_ptr(), sp))
-        P = B * self.top_k
+        P = self.n_experts * stride if stride else B * self.top_k
         es = b["S"].shape[1] // p["row_elems"]
         check(lib.qnb_gather_rows(b["T"].data_ptr(), p["row_elems"] * es, b["pair_sample"].data_ptr(), P,
                                   b["S"].data_ptr(), sp))
@@ -288,20 +298,47 @@ class MoeNet:
             rows, local_counts = p["xchg"].dispatch(b["S"], counts)
         else:
             rows, local_counts = b["S"], counts
-        nrows = int(local_counts.sum())
-        if p["qv_in"] is not None:
-            check(lib.qnb_dequantize(rows.data_ptr(), nrows * p["row_elems"], p["in_dtype"], C.byref(p["qv_in"]),
-                                     b["X"].data_ptr(), sp))
-        else:
-            check(lib.qnb_cast_float(rows.data_ptr(), nrows * p["row_elems"], p["in_dtype"], L.FP32,
-                                     b["X"].data_ptr(), sp))
+        nrows = int(local_counts.sum()) if not stride else self.n_experts * stride
+
+        def to_f32(src_ptr, dst_ptr, n_rows, st):
+            ne = n_rows * p["row_elems"]
+            if p["qv_in"] is not None:
+                check(lib.qnb_dequantize(src_ptr, ne, p["in_dtype"], C.byref(p["qv_in"]), dst_ptr, C.c_void_p(st)))
+            else:
+                check(lib.qnb_cast_float(src_ptr, ne, p["in_dtype"], L.FP32, dst_ptr, C.c_void_p(st)))
+
+        if not stride:
+            to_f32(rows.data_ptr(), b["X"].data_ptr(), nrows, s)
         off = 0
+        cap = p["experts"][next(iter(p["experts"]))].max_batch
+        main = torch.cuda.current_stream()
+        if "streams" not in p:
+            p["streams"] = [torch.cuda.Stream() for _ in range(4)]
+            p["events"] = [torch.cuda.Event() for _ in range(5)]
+        ready = p["events"][4]
+        ready.record(main)
+        used = []
         for j, e in enumerate(sorted(p["experts"])):
             c = int(local_counts[j])
             if c:
+                if stride:
+                    # fixed segment, bucketed batch (graph cache hit), concurrent stream
+                    bk = min(cap, -(-c // self.BUCKET) * self.BUCKET)
+                    st = p["streams"][len(used) % len(p["streams"])]
+                    st.wait_event(ready)
+                    used.append(st)
+                    ss = st.cuda_stream
+                    to_f32(b["S"].data_ptr() + off * p["row_elems"] * es, b["X"].data_ptr() + off * p["row_elems"] * 4,
+                           c, ss)
+                else:
+                    bk, ss = c, s
                 p["experts"][e].forward_device(b["X"].data_ptr() + off * p["row_elems"] * 4,
-                                               b["Y"].data_ptr() + off * p["per"] * 4, c, s)
-            off += c
+                                               b["Y"].data_ptr() + off * p["per"] * 4, bk, ss)
+            off += stride if stride else c
+        for i, st in enumerate({id(x): x for x in used}.values()):
+            ev = p["events"][i]
+            ev.record(st)
+            main.wait_event(ev)
         y = b["Y"][:nrows]
         if self.world > 1:
             y = p["xchg"].combine(y)
