@@ -510,37 +510,48 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
   const int qi = threadIdx.x % quads, pl = threadIdx.x / quads, pstride = kLrnThreads / quads;
   if (pl >= pstride) return;
   const int c4 = qi * 4;
-  const int32_t oz = (int32_t)a.out_q.zero, omin = (int32_t)a.out_q.i_min, omax = (int32_t)a.out_q.i_max;
+  const float zf = (float)a.out_q.zero, lo = (float)a.out_q.i_min, hi = (float)a.out_q.i_max;
   for (int pi = pl; pi < np; pi += pstride) {
     const float* row = lrn_smem + pi * C;
-    float sq[12];  // squares of channels c4-4 .. c4+7 (0 outside [0, C))
+    // squares of channels c4-4 .. c4+7 (0 outside [0, C)): three float4 smem loads
+    float sq[12], xs[4];
+    {
+      const float4 mid = *reinterpret_cast<const float4*>(row + c4);
+      const float4 lo4 = c4 >= 4 ? *reinterpret_cast<const float4*>(row + c4 - 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 hi4 = c4 + 4 < C ? *reinterpret_cast<const float4*>(row + c4 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float v[12] = {lo4.x, lo4.y, lo4.z, lo4.w, mid.x, mid.y, mid.z, mid.w, hi4.x, hi4.y, hi4.z, hi4.w};
 #pragma unroll
-    for (int u = 0; u < 12; ++u) {
-      const int c = c4 - 4 + u;
-      const float x = (c >= 0 && c < C) ? row[c] : 0.0f;
-      sq[u] = __fmul_rn(x, x);
+      for (int u = 0; u < 12; ++u) sq[u] = __fmul_rn(v[u], v[u]);
+      xs[0] = mid.x;
+      xs[1] = mid.y;
+      xs[2] = mid.z;
+      xs[3] = mid.w;
     }
-    uint32_t packed = 0;
+    uint32_t packed = 0, slow = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int c = c4 + u;
       float sf = 0.0f;
 #pragma unroll
       for (int d = -2; d <= 2; ++d)
         if (d >= -half && d <= half) sf = __fadd_rn(sf, sq[4 + u + d]);
-      const float x = row[c];
-      const float base = __fadd_rn(fk, __fmul_rn(fa_n, sf));
+      const float x = xs[u];
+      const float base = __fmaf_rn(fa_n, sf, fk);
       const float rden = ex2_approx(-__fmul_rn(fbeta, __log2f(base)));
       const float t = __fmul_rn(__fmul_rn(x, rden), finv);
-      const float fl = floorf(t);
-      int32_t qv;
-      if (fabsf(t) < 1e6f && fabsf(t - fl - 0.5f) > __fmaf_rn(3e-6f, fabsf(t), 1e-6f) && half <= 2) {
-        const int32_t v = (int32_t)rintf(t) + oz;
-        qv = v < omin ? omin : (v > omax ? omax : v);
-      } else {
-        qv = (int32_t)lrn_exact_q(row, max(0, c - half), min(C - 1, c + half), x, a.k, a.a_n, a.beta, a.out_q);
+      const float r = rintf(t);
+      // decided unless within the float path's error bound of a tie (NaN/huge: exact path)
+      slow |= (fabsf(__fsub_rn(t, r)) < __fsub_rn(0.5f, __fmaf_rn(3e-6f, fabsf(t), 1e-6f)) ? 0u : 1u) << u;
+      const uint32_t qv = (uint32_t)(int)fminf(fmaxf(r + zf, lo), hi);
+      packed |= (qv & 0xFFu) << (8 * u);
+    }
+    if (slow != 0 || half > 2) {  // rare: the reference's exact double arithmetic
+      for (int u = 0; u < 4; ++u) {
+        if (half <= 2 && !((slow >> u) & 1u)) continue;
+        const int c = c4 + u;
+        const uint32_t qv =
+            (uint32_t)lrn_exact_q(row, max(0, c - half), min(C - 1, c + half), row[c], a.k, a.a_n, a.beta, a.out_q);
+        packed = (packed & ~(0xFFu << (8 * u))) | ((qv & 0xFFu) << (8 * u));
       }
-      packed |= ((uint32_t)qv & 0xFFu) << (8 * u);
     }
     *reinterpret_cast<uint32_t*>(dbase + out_off[pi] + c4) = packed;
   }
