@@ -369,7 +369,19 @@ def run_qnb(a):
             roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "kernel": f"{kind} {names[li]}", "algorithmic_bytes": by, "launch_ms": t}
         roof["frac"] = roof["achieved"] / roof["peak"]
+        # measured DRAM traffic of that launch (dram__bytes_read + write, one ncu --set full
+        # capture of this workload, committed under profiles/ncu/)
         roof["traffic"] = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu", f"traffic_{a.model}_{a.precision}.json")) as f:
+                tr = json.load(f)["per_launch"].get(names[li])
+            if tr:
+                roof["traffic"] = tr["dram_bytes"]
+                roof["traffic_source"] = f"profiles/ncu/traffic_{a.model}_{a.precision}.json"
+                alg = roof.get("algorithmic_bytes") or by
+                roof["algorithmic_bytes"] = alg
+        except Exception:
+            pass
         roof["peak_source"] = (f"{peak_src}: 2 x bf16_tflops {peaks['bf16_tflops']} (dense int8 = 2x bf16)"
                                if kind == "igemm" else f"{peak_src}: hbm_gbs")
         conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
