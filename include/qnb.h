@@ -238,8 +238,11 @@ typedef struct {
 typedef struct {
   int64_t max_batch;      /* batch the plan's buffers and CUDA graph are sized for */
   int32_t use_cuda_graph; /* capture the whole forward once and replay it */
-  int32_t reserved;
+  int32_t flags;          /* QNB_PLAN_* bits */
 } qnb_plan_opts;
+
+/* Keep every layer's top blob in memory (no CONV/IP+RELU fusion): calibration plans. */
+#define QNB_PLAN_OBSERVE 1
 
 typedef struct qnb_plan qnb_plan;
 
@@ -275,6 +278,14 @@ qnb_status qnb_plan_step_info(const qnb_plan* plan, int32_t step, int32_t* layer
  * (device pointers) and writes the mean milliseconds of every step. */
 qnb_status qnb_plan_profile(qnb_plan* plan, const void* input, int64_t batch, void* output,
                             int32_t reps, qnb_stream s, float* ms_per_step);
+/* OBSERVE-mode calibration on the device (Net::forward in OBSERVE, src/net.cpp:305-330 +
+ * observe(), src/quantizer.cpp:58-68): runs the plan on `input` (device, the INPUT
+ * layer's NCHW dtype) and writes, per blob id, the min / max over every element of the
+ * blob (NaN where the plan does not materialise it, e.g. values fused away).  Build the
+ * plan from the FP32 view of the graph with QNB_PLAN_OBSERVE so that every top that
+ * Net::forward would observe exists. */
+qnb_status qnb_plan_observe(qnb_plan* plan, const void* input, int64_t batch, double* mins, double* maxs,
+                            qnb_stream s);
 qnb_status qnb_plan_destroy(qnb_plan* plan);
 
 #if defined(__GNUC__)

@@ -81,7 +81,7 @@ class LayerDesc(C.Structure):
 
 
 class PlanOpts(C.Structure):
-    _fields_ = [("max_batch", C.c_int64), ("use_cuda_graph", C.c_int32), ("reserved", C.c_int32)]
+    _fields_ = [("max_batch", C.c_int64), ("use_cuda_graph", C.c_int32), ("flags", C.c_int32)]
 
 
 _PLAN_SIGS = {
@@ -94,6 +94,8 @@ _PLAN_SIGS = {
     "qnb_plan_blob_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "qnb_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                  C.POINTER(C.c_int64)]),
+    "qnb_plan_observe": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.c_void_p]),
     "qnb_plan_destroy": (C.c_int, [C.c_void_p]),
     "qnb_plan_step_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),

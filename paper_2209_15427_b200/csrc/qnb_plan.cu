@@ -116,6 +116,8 @@ struct qnb_plan {
   std::vector<qnb::Step> steps;
   int64_t max_batch = 0;
   bool use_graph = true;
+  int32_t flags = 0;
+  int32_t n_user_blobs = 0;  // blob ids the caller numbered (lowering may append internal ones)
   int input_blob = -1, sink_blob = -1;
   int out_dtype = QNB_FP32, out_ndim = 2;
   int64_t out_shape[4] = {0, 0, 0, 0};
@@ -369,7 +371,7 @@ qnb_status lower(qnb_plan& P) {
       case QNB_LAYER_CONV:
       case QNB_LAYER_INNER_PRODUCT: {
         op.kind = OP_IGEMM;
-        const int j = sole_consumer(P, l.top);
+        const int j = (P.flags & QNB_PLAN_OBSERVE) ? -1 : sole_consumer(P, l.top);
         if (j >= 0 && P.layers[j].kind == QNB_LAYER_RELU && P.layers[j].d_type == l.mo_type &&
             P.layers[j].mo_type == l.mo_type) {
           done[j] = true;
@@ -941,8 +943,10 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
   auto P = std::make_unique<qnb_plan>();
   P->layers.assign(layers, layers + n_layers);
   P->blobs.resize((size_t)n_blobs);
+  P->n_user_blobs = n_blobs;
   P->max_batch = opts && opts->max_batch > 0 ? opts->max_batch : 1;
   P->use_graph = opts ? opts->use_cuda_graph != 0 : true;
+  P->flags = opts ? opts->flags : 0;
   QNB_CUDA(cudaGetDevice(&P->device));
   QNB_TRY(build_blob_table(*P));
   QNB_TRY(lower(*P));
@@ -1164,6 +1168,106 @@ qnb_status qnb_plan_profile(qnb_plan* P, const void* input, int64_t batch, void*
   }
   for (size_t i = 0; i < n; ++i) ms_per_step[i] = (float)(acc[i] / (reps > 0 ? reps : 1));
   for (auto& e : ev) cudaEventDestroy(e);
+  return QNB_OK;
+}
+
+}  // extern "C"
+
+namespace qnb {
+namespace {
+// Per-block min/max over the interior, real channels of an NHWC blob (or a dense
+// NCHW buffer when L.c_phys == 0 is passed with n*c*h*w elements); partials to part[2*b].
+__global__ void minmax_kernel(const uint8_t* __restrict__ base, DevLayout L, int dtype, int64_t dense_n,
+                              float* __restrict__ part) {
+  float lo = INFINITY, hi = -INFINITY;
+  const int64_t total = dense_n > 0 ? dense_n : L.n * L.h * L.w * L.c;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float v;
+    if (dense_n > 0) {
+      v = dtype == QNB_FP32 ? reinterpret_cast<const float*>(base)[i]
+                            : __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(base)[i]));
+    } else {
+      const int64_t c = i % L.c, px = i / L.c;
+      const int64_t x = px % L.w, y = (px / L.w) % L.h, n = px / (L.w * L.h);
+      const uint8_t* p = base + n * L.img + y * L.row + x * L.pix + L.origin + c * L.es;
+      v = dtype == QNB_FP32 ? *reinterpret_cast<const float*>(p)
+                            : __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(p)));
+    }
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+  }
+  __shared__ float slo[256], shi[256];
+  slo[threadIdx.x] = lo;
+  shi[threadIdx.x] = hi;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) {
+      slo[threadIdx.x] = fminf(slo[threadIdx.x], slo[threadIdx.x + st]);
+      shi[threadIdx.x] = fmaxf(shi[threadIdx.x], shi[threadIdx.x + st]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = slo[0];
+    part[2 * blockIdx.x + 1] = shi[0];
+  }
+}
+
+qnb_status minmax(const uint8_t* base, const DevLayout& L, int dtype, int64_t dense_n, cudaStream_t s, double* lo,
+                  double* hi) {
+  constexpr int kBlocks = 592;
+  float* part = nullptr;
+  QNB_CUDA(cudaMallocAsync(&part, kBlocks * 2 * sizeof(float), s));
+  minmax_kernel<<<kBlocks, 256, 0, s>>>(base, L, dtype, dense_n, part);
+  count_launch();
+  std::vector<float> h(kBlocks * 2);
+  QNB_CUDA(cudaMemcpyAsync(h.data(), part, h.size() * sizeof(float), cudaMemcpyDeviceToHost, s));
+  QNB_CUDA(cudaStreamSynchronize(s));
+  QNB_CUDA(cudaFreeAsync(part, s));
+  float l = INFINITY, u = -INFINITY;
+  for (int b = 0; b < kBlocks; ++b) {
+    l = std::min(l, h[2 * b]);
+    u = std::max(u, h[2 * b + 1]);
+  }
+  *lo = l;
+  *hi = u;
+  return QNB_OK;
+}
+}  // namespace
+}  // namespace qnb
+
+extern "C" {
+
+qnb_status qnb_plan_observe(qnb_plan* P, const void* input, int64_t batch, double* mins, double* maxs, qnb_stream s_) {
+  if (!P || !mins || !maxs) return fail(QNB_E_ARG, "null argument");
+  if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
+  cudaStream_t s = as_stream(s_);
+  void* out = nullptr;
+  QNB_CUDA(cudaMallocAsync(&out, (size_t)(P->out_bytes_per_sample * batch), s));
+  QNB_TRY(launch_steps(*P, batch, input, out, s));
+  count_launch((uint64_t)P->launches_per_forward);
+  const double nan = std::nan("");
+  for (int b = 0; b < P->n_user_blobs; ++b) {
+    mins[b] = maxs[b] = nan;
+    const Blob& bl = P->blobs[b];
+    if (!bl.defined || (bl.dtype != QNB_FP32 && bl.dtype != QNB_FP16)) continue;
+    const int r = root_of(*P, (int)b);
+    const Blob& rb = P->blobs[r];
+    if (b == P->input_blob || rb.external) {
+      QNB_TRY(minmax((const uint8_t*)input, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+    } else if (r == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) {
+      QNB_TRY(minmax((const uint8_t*)out, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+    } else if (rb.needs_buffer) {
+      DevLayout L = dev_layout(rb.L);
+      if (L.pslot != 0) return fail(QNB_E_UNSUPPORTED, "observe on a pair-interleaved blob");
+      L.n = batch;
+      QNB_TRY(minmax(P->arena + rb.off, L, bl.dtype, 0, s, &mins[b], &maxs[b]));
+    } else if (r == P->sink_blob) {
+      QNB_TRY(minmax((const uint8_t*)out, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+    }
+  }
+  QNB_CUDA(cudaFreeAsync(out, s));
+  QNB_CUDA(cudaStreamSynchronize(s));
   return QNB_OK;
 }
 

@@ -13,6 +13,7 @@ reference.  Weight quantization during finalize runs on the GPU (qnb_quantize).
 """
 from __future__ import annotations
 
+import copy
 import ctypes as C
 
 import numpy as np
@@ -38,12 +39,15 @@ NP_OF = {0: np.float32, 1: np.uint16, 2: np.uint8, 3: np.uint16}
 class Plan:
     """A compiled device plan (qnb_plan) for one calibrated chain graph."""
 
-    def __init__(self, descs, n_blobs, keep_alive, max_batch, use_cuda_graph=True, blob_ids=None):
+    OBSERVE = 1  # QNB_PLAN_OBSERVE: keep every top (no CONV/IP+RELU fusion)
+
+    def __init__(self, descs, n_blobs, keep_alive, max_batch, use_cuda_graph=True, blob_ids=None, flags=0):
         self._keep = keep_alive
         self.max_batch = max_batch
         self.blob_ids = blob_ids or {}
+        self.n_blobs = n_blobs
         arr = (LayerDesc * len(descs))(*descs)
-        opts = PlanOpts(max_batch, 1 if use_cuda_graph else 0, 0)
+        opts = PlanOpts(max_batch, 1 if use_cuda_graph else 0, flags)
         self.h = C.c_void_p()
         lib = _plan_lib()
         check(lib.qnb_plan_create(arr, len(descs), n_blobs, C.byref(opts), C.byref(self.h)))
@@ -96,6 +100,24 @@ class Plan:
         """Raw pointers (device by default), stream-ordered, no synchronisation."""
         check(_plan_lib().qnb_plan_forward(self.h, C.c_void_p(in_ptr), batch, 1 if in_host else 0,
                                            C.c_void_p(out_ptr), 1 if out_host else 0, C.c_void_p(stream)))
+
+    def observe_host(self, x: np.ndarray):
+        """qnb_plan_observe on a host batch: (output, {blob id: (min, max)})."""
+        x = np.ascontiguousarray(x)
+        b = x.shape[0]
+        lib = L.lib()
+        d = C.c_void_p()
+        check(lib.qnb_malloc(C.byref(d), x.nbytes))
+        try:
+            check(lib.qnb_memcpy_h2d(d, x.ctypes.data_as(C.c_void_p), x.nbytes, None))
+            lo = (C.c_double * self.n_blobs)()
+            hi = (C.c_double * self.n_blobs)()
+            check(_plan_lib().qnb_plan_observe(self.h, d, b, lo, hi, None))
+            out = self.forward_host(x)
+        finally:
+            lib.qnb_free(d)
+        seen = {i: (lo[i], hi[i]) for i in range(self.n_blobs) if lo[i] == lo[i]}
+        return out, seen
 
     def blob(self, name: str, shape=None):
         """Reads a materialised blob's interior back (NHWC -> reference NCHW)."""
@@ -264,11 +286,64 @@ class Net:
             self._plans[batch] = self.compile(batch)
         return self._plans[batch]
 
+    def observe_graph(self) -> dict:
+        """The float execution Net::forward runs in OBSERVE mode (src/net.cpp:332-376): every
+        layer in FP32, QUANTIZER / DROPOUT layers numeric no-ops.  QUANTIZER layers are dropped
+        and their consumers rewired to the quantizer's bottom; the dropped tops share their
+        bottom's range key (graph range_aliases), so the recorded ranges are the same."""
+        g = copy.deepcopy(self.graph)
+        ren, layers = {}, []
+        for l in g["layers"]:
+            if l.get("bottom"):
+                l["bottom"] = [ren.get(b, b) for b in l["bottom"]]
+            if l["kind"] == "quantizer":
+                ren[l["top"][0]] = l["bottom"][0]
+                continue
+            l["bottom_data_type"] = l["compute_data_type"] = l["top_data_type"] = G.FP32
+            layers.append(l)
+        g["layers"] = layers
+        return g
+
+    def observe(self, x: np.ndarray) -> np.ndarray:
+        """Net::forward in OBSERVE mode on the device: FP32 (TF32 tensor-core) execution and a
+        min / max reduction per blob (observe(), src/quantizer.cpp:58-68); the ranges widen the
+        ones already recorded (src/net.cpp:206-209)."""
+        if x.dtype.kind not in "f":
+            raise QnbError(10, "OBSERVE on the device takes float inputs")
+        x = x.astype(np.float32)
+        og = self.observe_graph()
+        saved = self.graph
+        self.graph = og
+        try:
+            params = {}
+            for l in og["layers"]:
+                if l["kind"] in ("conv", "inner_product"):
+                    w = self.params.get(l["name"] + ".weight")
+                    if w is not None and w[1] != 0:  # param_float(): finalized weights dequantize
+                        params[l["name"] + ".weight"] = w
+                        self.params[l["name"] + ".weight"] = (ops.dequantize(w[0], w[1], w[2]), 0, None)
+            try:
+                descs, n_blobs, keep, ids = self.layer_descs()
+            finally:
+                self.params.update(params)
+        finally:
+            self.graph = saved
+        plan = Plan(descs, n_blobs, keep, x.shape[0], False, ids, flags=Plan.OBSERVE)
+        out, seen = plan.observe_host(x)
+        for name, i in ids.items():
+            if i not in seen:
+                continue
+            lo, hi = seen[i]
+            key = G.range_key(self.aliases, name)
+            if key in self.ranges:
+                plo, phi = self.ranges[key]
+                lo, hi = min(lo, plo), max(hi, phi)
+            self.ranges[key] = (float(lo), float(hi))
+        self._plans.clear()
+        return out
+
     def forward(self, inputs: dict) -> dict:
         """src/net.cpp:305-330: returns {sink: tensor} in the reference layout."""
-        if self.mode == QUANTIZED or all(
-                self.blobs[b]["dtype"] in G.FLOAT for b in self.blobs):
-            pass
         name = G.input_name(self.graph)
         if name not in inputs:
             raise QnbError(1, "missing input: " + name)
@@ -276,5 +351,7 @@ class Net:
         want = next(l for l in self.graph["layers"] if l["kind"] == "input")["input_shape"]
         if x.ndim != len(want) or list(x.shape[1:]) != list(want[1:]):
             raise QnbError(2, "shape mismatch")
+        if self.mode == OBSERVE:
+            return {G.sinks(self.graph)[-1]: self.observe(x)}
         out = self.plan(x.shape[0]).forward_host(x)
         return {G.sinks(self.graph)[-1]: out}
