@@ -233,6 +233,8 @@ typedef struct {
   const float* bias;                  /* FP32, OC / OUT entries, or NULL */
   int32_t top_has_qv;                 /* quantized tops: Net::blob_qvals(top) */
   qnb_qvals top_qv;
+  int32_t inspect_top;                /* top is in Graph::inspect (include/qnet/graph.hpp:96):
+                                         never fused away, readable via qnb_plan_blob_info */
 } qnb_layer_desc;
 
 typedef struct {
@@ -241,7 +243,7 @@ typedef struct {
   int32_t flags;          /* QNB_PLAN_* bits */
 } qnb_plan_opts;
 
-/* Keep every layer's top blob in memory (no CONV/IP+RELU fusion): calibration plans. */
+/* Every layer's top blob is materialised, as if all were inspected: calibration plans. */
 #define QNB_PLAN_OBSERVE 1
 
 typedef struct qnb_plan qnb_plan;

@@ -17,6 +17,7 @@
 #ifndef QNB_QNET_HPP_
 #define QNB_QNET_HPP_
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -104,6 +105,7 @@ class Executor {
       d.mo_type = (int32_t)l.mo_type;
       d.bottom = l.bottoms.empty() ? -1 : id_of(l.bottoms[0]);
       d.top = id_of(l.tops.at(0));
+      d.inspect_top = std::find(g.inspect.begin(), g.inspect.end(), l.tops[0]) != g.inspect.end() ? 1 : 0;
       switch (l.kind) {
         case qnet::LayerKind::INPUT:
           d.input_ndim = (int32_t)l.input_shape.size();

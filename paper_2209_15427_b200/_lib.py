@@ -77,6 +77,7 @@ class LayerDesc(C.Structure):
         ("negative_slope", C.c_float), ("num_output", C.c_int64), ("bias_term", C.c_int32),
         ("weight", C.c_void_p), ("weight_dtype", C.c_int32), ("weight_has_qv", C.c_int32),
         ("weight_qv", QVals), ("bias", C.c_void_p), ("top_has_qv", C.c_int32), ("top_qv", QVals),
+        ("inspect_top", C.c_int32),
     ]
 
 

@@ -57,6 +57,7 @@ struct Blob {
   bool external = false; // the user's NCHW input
   bool needs_buffer = false;
   bool layout_set = false;
+  bool inspect = false;  // Graph::inspect or an OBSERVE plan: never fused away
   ActLayout L;
   size_t off = 0;
 };
@@ -246,6 +247,7 @@ qnb_status build_blob_table(qnb_plan& P) {
     if (t.defined) return fail(QNB_E_ARG, "blob produced twice");
     t.defined = true;
     t.dtype = l.mo_type;
+    t.inspect = l.inspect_top != 0 || (P.flags & QNB_PLAN_OBSERVE) != 0;
     if (l.kind == QNB_LAYER_INPUT) {
       if (P.input_blob >= 0) return fail(QNB_E_UNSUPPORTED, "graphs with several INPUT layers");
       P.input_blob = l.top;
@@ -322,9 +324,15 @@ qnb_status build_blob_table(qnb_plan& P) {
   return QNB_OK;
 }
 
-int sole_consumer(const qnb_plan& P, int blob) {
+int only_consumer(const qnb_plan& P, int blob) {
   const Blob& b = P.blobs[blob];
   return b.consumers.size() == 1 ? b.consumers[0] : -1;
+}
+
+// The layer that may be fused into the producer of `blob` (every fusion goes through
+// here): none when the blob must stay materialised.
+int sole_consumer(const qnb_plan& P, int blob) {
+  return P.blobs[blob].inspect ? -1 : only_consumer(P, blob);
 }
 
 bool is_q2f(const qnb_layer_desc& l) {
@@ -346,12 +354,12 @@ qnb_status lower(qnb_plan& P) {
     op.out = l.top;
     switch (l.kind) {
       case QNB_LAYER_INPUT: {
-        const int j = sole_consumer(P, l.top);
+        const int j = only_consumer(P, l.top);
         if (j < 0) return fail(QNB_E_UNSUPPORTED, "input without consumer");
         const qnb_layer_desc& q = P.layers[j];
         op.kind = OP_PACK;
         op.in = l.top;
-        if (q.kind == QNB_LAYER_QUANTIZER) {
+        if (q.kind == QNB_LAYER_QUANTIZER && !P.blobs[q.top].inspect) {
           done[j] = true;
           op.out = q.top;
           op.pack_op = is_quant(q.mo_type) ? PACK_QUANTIZE : (q.mo_type == l.mo_type ? PACK_COPY : PACK_CAST);
@@ -371,7 +379,7 @@ qnb_status lower(qnb_plan& P) {
       case QNB_LAYER_CONV:
       case QNB_LAYER_INNER_PRODUCT: {
         op.kind = OP_IGEMM;
-        const int j = (P.flags & QNB_PLAN_OBSERVE) ? -1 : sole_consumer(P, l.top);
+        const int j = sole_consumer(P, l.top);
         if (j >= 0 && P.layers[j].kind == QNB_LAYER_RELU && P.layers[j].d_type == l.mo_type &&
             P.layers[j].mo_type == l.mo_type) {
           done[j] = true;

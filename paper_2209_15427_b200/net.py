@@ -268,6 +268,7 @@ class Net:
                     keep.append(barr)
                     d.bias = barr.ctypes.data
             top = l["top"][0]
+            d.inspect_top = 1 if top in self.graph.get("inspect", ()) else 0
             if l["top_data_type"] in G.QUANT:
                 qv = self.blob_qv.get(top)
                 if qv is None:

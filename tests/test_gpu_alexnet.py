@@ -135,3 +135,36 @@ def test_host_buffer_pipeline_matches_device_forward(setup):
         assert np.array_equal(op.numpy(), want)
     got = plan.forward_host(x)  # pageable numpy buffers
     assert np.array_equal(got, want)
+
+
+def test_inspect_blobs_stay_addressable(setup):
+    """Graph::inspect (include/qnet/graph.hpp:96): inspected blobs are never fused away.
+    conv1 (normally fused with relu1), pool1 (normally inside the pool+LRN kernel) and
+    fc8__fp32 (normally inside the softmax) get their own buffers; their contents equal
+    the reference's blob and the network output is unchanged."""
+    ref, g, params, ranges, ours = setup
+    batch = 2
+    x = graphs.synth_images(batch, (3, 227, 227), offset=3)
+    gi = G.override_precision(g, "int8")
+    gi["inspect"] = ["conv1", "pool1", "fc8__fp32"]
+    net = Net(gi)
+    for k, (arr, dt, qv) in ours.params.items():
+        net.set_param(k, arr, dt, qv)
+    net.blob_qv = dict(ours.blob_qv)
+    net.set_quant_mode(QUANTIZED)
+    out = net.forward({"data": x})["prob"]
+    assert np.array_equal(out, ours.forward({"data": x})["prob"])
+    plan = net.plan(batch)
+    assert plan.stats()["kernels_per_forward"] > ours.plan(batch).stats()["kernels_per_forward"]
+    names = [l["name"] for l in g["layers"]]
+    for ck in ("conv1", "pool1"):
+        prefix = {"name": "alexnet_prefix", "layers": g["layers"][: names.index(ck) + 1]}
+        pr = {k: v for k, v in params.items() if k.split(".")[0] in names[: names.index(ck) + 1]}
+        (arr, dt, qv), = ref_net(ref, prefix, "int8", pr, ranges).forward("data", x).values()
+        raw, lay = plan.blob(ck)
+        mine = nhwc_interior_to_nchw(raw, lay, np.uint8)[..., : arr.shape[1]]
+        assert np.array_equal(mine, np.transpose(arr, (0, 2, 3, 1))), ck
+    raw, lay = plan.blob("fc8__fp32")
+    fc8 = nhwc_interior_to_nchw(raw, lay, np.float32).reshape(batch, -1)[:, :1000]
+    e = np.exp(fc8.astype(np.float64) - fc8.max(axis=1, keepdims=True))
+    assert np.allclose(e / e.sum(axis=1, keepdims=True), out, rtol=1e-5, atol=1e-9)
