@@ -231,7 +231,9 @@ typedef struct {
   int32_t weight_has_qv;
   qnb_qvals weight_qv;
   const float* bias;                  /* FP32, OC / OUT entries, or NULL */
-  int32_t top_has_qv;                 /* quantized tops: Net::blob_qvals(top) */
+  int32_t top_has_qv;                 /* quantized tops: Net::blob_qvals(top); PSEUDO
+                                         QUANTIZER layers (FP32 bottom/top, quantized d_type):
+                                         the grid the values are fake-quantized onto */
   qnb_qvals top_qv;
   int32_t inspect_top;                /* top is in Graph::inspect (include/qnet/graph.hpp:96):
                                          never fused away, readable via qnb_plan_blob_info */
@@ -245,6 +247,10 @@ typedef struct {
 
 /* Every layer's top blob is materialised, as if all were inspected: calibration plans. */
 #define QNB_PLAN_OBSERVE 1
+/* FP32 conv / inner product in the reference's exact arithmetic (sequential sum of
+ * separately rounded products, src/ops.cpp:273-297, 405-420) on CUDA cores instead of
+ * TF32 tensor cores: bit-identical float layers for OBSERVE / PSEUDO calibration. */
+#define QNB_PLAN_EXACT_FLOAT 2
 
 typedef struct qnb_plan qnb_plan;
 

@@ -42,7 +42,7 @@ int default_shift_bits(int dtype);
 
 namespace {
 
-enum OpKind { OP_PACK, OP_IGEMM, OP_POOL, OP_POOL_LRN, OP_CONVERT, OP_SOFTMAX, OP_ALIAS };
+enum OpKind { OP_PACK, OP_IGEMM, OP_POOL, OP_POOL_LRN, OP_CONVERT, OP_SOFTMAX, OP_ALIAS, OP_FEXACT };
 
 struct Blob {
   bool defined = false;
@@ -86,6 +86,7 @@ struct Step {
   int64_t groups = 1;
   int64_t rows_per_img = 0;  // igemm: oh*ow
   PackArgs pack;
+  FExactArgs fx;
   PoolArgs pool;
   PoolLrnArgs plrn;
   ConvertArgs cvt;
@@ -338,6 +339,10 @@ int sole_consumer(const qnb_plan& P, int blob) {
 bool is_q2f(const qnb_layer_desc& l) {
   return l.kind == QNB_LAYER_QUANTIZER && l.mo_type == QNB_FP32 && l.mi_type != QNB_FP32;
 }
+// PSEUDO fake-quant: FP32 in and out, the declared type as compute type.
+bool is_pseudo(const qnb_layer_desc& l) {
+  return l.kind == QNB_LAYER_QUANTIZER && l.mi_type == QNB_FP32 && l.mo_type == QNB_FP32 && l.d_type != QNB_FP32;
+}
 bool is_f2x(const qnb_layer_desc& l) {
   return l.kind == QNB_LAYER_QUANTIZER && l.mi_type == QNB_FP32 && l.mo_type != QNB_FP32;
 }
@@ -359,7 +364,7 @@ qnb_status lower(qnb_plan& P) {
         const qnb_layer_desc& q = P.layers[j];
         op.kind = OP_PACK;
         op.in = l.top;
-        if (q.kind == QNB_LAYER_QUANTIZER && !P.blobs[q.top].inspect) {
+        if (q.kind == QNB_LAYER_QUANTIZER && !is_pseudo(q) && !P.blobs[q.top].inspect) {
           done[j] = true;
           op.out = q.top;
           op.pack_op = is_quant(q.mo_type) ? PACK_QUANTIZE : (q.mo_type == l.mo_type ? PACK_COPY : PACK_CAST);
@@ -379,6 +384,11 @@ qnb_status lower(qnb_plan& P) {
       case QNB_LAYER_CONV:
       case QNB_LAYER_INNER_PRODUCT: {
         op.kind = OP_IGEMM;
+        if ((P.flags & QNB_PLAN_EXACT_FLOAT) && l.mi_type == QNB_FP32 && l.d_type == QNB_FP32 &&
+            l.mo_type == QNB_FP32) {
+          op.kind = OP_FEXACT;
+          break;
+        }
         const int j = sole_consumer(P, l.top);
         if (j >= 0 && P.layers[j].kind == QNB_LAYER_RELU && P.layers[j].d_type == l.mo_type &&
             P.layers[j].mo_type == l.mo_type) {
@@ -449,6 +459,11 @@ qnb_status lower(qnb_plan& P) {
           op.in_dtype = l.mi_type;
           op.out_dtype = l.mo_type;
           op.conv_op = (is_quant(l.mi_type) && is_quant(l.mo_type)) ? CVT_REQUANT : CVT_CONVERT;
+          if (is_pseudo(l)) {
+            if (is_quant(l.d_type) && !l.top_has_qv)
+              return fail(QNB_E_QVALS, "quantizer not finalized: blob " + std::to_string(l.top));
+            op.conv_op = CVT_PSEUDO;
+          }
           break;
         }
         return fail(QNB_E_ARG, "unreachable lowering state");
@@ -765,6 +780,51 @@ qnb_status emit(qnb_plan& P) {
       case OP_IGEMM:
         QNB_TRY(emit_igemm(P, op, st));
         break;
+      case OP_FEXACT: {
+        const qnb_layer_desc& l = P.layers[op.layer];
+        const Blob& bi = P.blobs[op.in];
+        const Blob& bo = P.blobs[op.out];
+        if (l.weight_dtype != QNB_FP32) return fail(QNB_E_DTYPE, "exact float layers take FP32 weights");
+        FExactArgs& a = st.fx;
+        std::memset(&a, 0, sizeof(a));
+        a.src = blob_ptr(P, op.in);
+        a.S = dev_layout(blob_layout(P, op.in));
+        a.dst = blob_ptr(P, op.out);
+        a.D = dev_layout(blob_layout(P, op.out));
+        int64_t nw = 0;
+        if (l.kind == QNB_LAYER_CONV) {
+          const auto& cp = l.conv;
+          a.cg = bi.c / cp.groups;
+          a.og = cp.out_channels / cp.groups;
+          a.kh = cp.kernel_h;
+          a.kw = cp.kernel_w;
+          a.sh = cp.stride_h;
+          a.sw = cp.stride_w;
+          a.ph = cp.pad_h;
+          a.pw = cp.pad_w;
+          nw = cp.out_channels * a.cg * a.kh * a.kw;
+          st.ops = 2.0 * P.max_batch * bo.h * bo.w * bo.c * (double)(a.cg * a.kh * a.kw);
+        } else {
+          a.is_fc = 1;
+          a.in_c = bi.c;
+          a.in_h = bi.h;
+          a.in_w = bi.w;
+          a.out = l.num_output;
+          nw = bi.c * bi.h * bi.w * l.num_output;
+          st.ops = 2.0 * P.max_batch * (double)nw;
+        }
+        std::vector<float> w((const float*)l.weight, (const float*)l.weight + nw);
+        float* wd = nullptr;
+        QNB_TRY(upload(P, w, &wd));
+        a.w = wd;
+        if (l.bias_term && l.bias) {
+          std::vector<float> b(l.bias, l.bias + (a.is_fc ? l.num_output : l.conv.out_channels));
+          float* bd = nullptr;
+          QNB_TRY(upload(P, b, &bd));
+          a.bias = bd;
+        }
+        break;
+      }
       case OP_POOL: {
         const qnb_layer_desc& l = P.layers[op.layer];
         st.pool.src = blob_ptr(P, op.in);
@@ -827,6 +887,10 @@ qnb_status emit(qnb_plan& P) {
           a.relu = to_dev_relu(rq, l.d_type);
         }
         a.slope = l.negative_slope;
+        if (op.conv_op == CVT_PSEUDO) {
+          a.pseudo_dtype = l.d_type;
+          if (is_quant(l.d_type)) a.out_q = dev_q(l.top_qv);
+        }
         break;
       }
       case OP_SOFTMAX: {
@@ -872,6 +936,7 @@ Step with_batch(const Step& s0, int64_t b, const void* in, void* out) {
   s.ig.m_total = b * s.rows_per_img;
   s.pack.N = b;
   s.pack.L.n = b;
+  s.fx.S.n = s.fx.D.n = b;
   s.pool.S.n = s.pool.D.n = b;
   s.plrn.S.n = s.plrn.D.n = b;
   s.cvt.S.n = s.cvt.D.n = b;
@@ -897,6 +962,9 @@ qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cuda
             QNB_TRY(igemm_finalize(st.ig, s));
             g_launches.fetch_sub(1);
           }
+          break;
+        case OP_FEXACT:
+          launch_fexact(st.fx, s);
           break;
         case OP_POOL:
           launch_pool(st.pool, s);
@@ -928,7 +996,8 @@ int step_kind_code(const Step& st) {
   if (st.unpack) return 6;
   switch (st.kind) {
     case OP_PACK: return 0;
-    case OP_IGEMM: return 1;
+    case OP_IGEMM:
+    case OP_FEXACT: return 1;
     case OP_POOL: return 2;
     case OP_POOL_LRN: return 3;
     case OP_CONVERT: return 4;

@@ -591,6 +591,14 @@ __global__ void convert_kernel(ConvertArgs a) {
         store_from_float(d, a.out_dtype, r, a.out_q);
         break;
       }
+      case CVT_PSEUDO: {  // Net::apply_pseudo (src/net.cpp:379-389): FP32 -> grid -> FP32
+        const float v = *reinterpret_cast<const float*>(s);
+        float r;
+        if (a.pseudo_dtype == QNB_FP16) r = h2f_bits(f2h_bits(v));
+        else r = dq(qz(v, a.out_q), a.out_q);  // pseudo_quantize, src/quantizer.cpp:141-153
+        *reinterpret_cast<float*>(d) = r;
+        break;
+      }
       default: {  // CVT_CONVERT: dequantize / quantize / cast / copy
         if ((a.in_dtype == QNB_FP16 && a.out_dtype == QNB_FP16) ||
             ((a.in_dtype == QNB_INT8Q || a.in_dtype == QNB_INT16Q) && a.in_dtype == a.out_dtype)) {
@@ -737,6 +745,72 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
   } else {
     pool_lrn_kernel<<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
   }
+}
+
+// ------------------------------------------------------------ exact FP32 contractions
+// One thread per output pixel and OCT output channels of one group.  Out-of-image taps
+// are skipped: the reference adds w * 0.0f there, which leaves a sum that can never be
+// -0 unchanged (finite weights).
+template <int OCT>
+__global__ void fconv_exact_kernel(FExactArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t npix = a.D.n * a.D.h * a.D.w;
+  if (p >= npix) return;
+  const int64_t ox = p % a.D.w, oy = (p / a.D.w) % a.D.h, n = p / (a.D.w * a.D.h);
+  const int64_t oc0 = (int64_t)blockIdx.y * OCT;
+  const int64_t grp = oc0 / a.og;
+  const int64_t patch = a.cg * a.kh * a.kw;
+  float acc[OCT];
+#pragma unroll
+  for (int o = 0; o < OCT; ++o) acc[o] = 0.0f;
+  const float* wb = a.w + oc0 * patch;
+  for (int64_t c = 0; c < a.cg; ++c) {
+    for (int64_t ki = 0; ki < a.kh; ++ki) {
+      const int64_t iy = oy * a.sh - a.ph + ki;
+      if (iy < 0 || iy >= a.S.h) continue;
+      for (int64_t kj = 0; kj < a.kw; ++kj) {
+        const int64_t ix = ox * a.sw - a.pw + kj;
+        if (ix < 0 || ix >= a.S.w) continue;
+        const float x = *reinterpret_cast<const float*>(at(a.src, a.S, n, iy, ix) + (grp * a.cg + c) * 4);
+        const int64_t k = (c * a.kh + ki) * a.kw + kj;
+#pragma unroll
+        for (int o = 0; o < OCT; ++o) acc[o] = __fadd_rn(acc[o], __fmul_rn(__ldg(wb + o * patch + k), x));
+      }
+    }
+  }
+  float* d = reinterpret_cast<float*>(at(a.dst, a.D, n, oy, ox)) + oc0;
+#pragma unroll
+  for (int o = 0; o < OCT; ++o) d[o] = __fadd_rn(acc[o], a.bias ? a.bias[oc0 + o] : 0.0f);
+}
+
+__global__ void fip_exact_kernel(FExactArgs a) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = blockIdx.y;
+  if (o >= a.out) return;
+  float acc = 0.0f;
+  for (int64_t c = 0; c < a.in_c; ++c)
+    for (int64_t h = 0; h < a.in_h; ++h)
+      for (int64_t w = 0; w < a.in_w; ++w) {
+        const float x = *reinterpret_cast<const float*>(at(a.src, a.S, n, h, w) + c * 4);
+        const int64_t k = (c * a.in_h + h) * a.in_w + w;
+        acc = __fadd_rn(acc, __fmul_rn(x, __ldg(a.w + k * a.out + o)));
+      }
+  if (a.bias) acc = __fadd_rn(acc, a.bias[o]);
+  *(reinterpret_cast<float*>(at(a.dst, a.D, n, 0, 0)) + o) = acc;
+}
+
+void launch_fexact(const FExactArgs& a, cudaStream_t s) {
+  if (a.is_fc) {
+    fip_exact_kernel<<<dim3((unsigned)((a.out + 127) / 128), (unsigned)a.D.n), 128, 0, s>>>(a);
+    return;
+  }
+  const int64_t npix = a.D.n * a.D.h * a.D.w;
+  const unsigned bx = (unsigned)((npix + 127) / 128);
+  const int64_t oc = a.D.c;
+  if (a.og % 8 == 0) fconv_exact_kernel<8><<<dim3(bx, (unsigned)(oc / 8)), 128, 0, s>>>(a);
+  else if (a.og % 4 == 0) fconv_exact_kernel<4><<<dim3(bx, (unsigned)(oc / 4)), 128, 0, s>>>(a);
+  else if (a.og % 2 == 0) fconv_exact_kernel<2><<<dim3(bx, (unsigned)(oc / 2)), 128, 0, s>>>(a);
+  else fconv_exact_kernel<1><<<dim3(bx, (unsigned)oc), 128, 0, s>>>(a);
 }
 
 void launch_convert(const ConvertArgs& a, cudaStream_t s) {

@@ -75,7 +75,7 @@ struct PoolLrnArgs {
   double a_n, beta, k;
 };
 
-enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3 };
+enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3, CVT_PSEUDO = 4 };
 
 struct ConvertArgs {
   const uint8_t* src;
@@ -88,9 +88,26 @@ struct ConvertArgs {
   int64_t in_zero;
   ReluRequant relu;
   float slope;
+  int pseudo_dtype;  // CVT_PSEUDO: the declared type whose grid out_q is
+};
+
+// FP32 conv / inner product in the reference's exact arithmetic (src/ops.cpp:273-297,
+// 405-420): per output a sequential sum of separately rounded products in the
+// reference's k order, then the bias.  Used by calibration plans (QNB_PLAN_EXACT_FLOAT).
+struct FExactArgs {
+  const uint8_t* src;
+  DevLayout S;
+  uint8_t* dst;
+  DevLayout D;
+  const float* w;     // reference layout: conv OC x Cg x KH x KW, IP K x OUT
+  const float* bias;  // or null
+  int is_fc;
+  int64_t cg, og, kh, kw, sh, sw, ph, pw;  // conv
+  int64_t in_c, in_h, in_w, out;           // IP: K = in_c * in_h * in_w in NCHW order
 };
 
 void launch_pack_input(const PackArgs& p, cudaStream_t s);
+void launch_fexact(const FExactArgs& a, cudaStream_t s);
 void launch_pool(const PoolArgs& p, cudaStream_t s);
 void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s);
 void launch_convert(const ConvertArgs& a, cudaStream_t s);

@@ -39,7 +39,8 @@ NP_OF = {0: np.float32, 1: np.uint16, 2: np.uint8, 3: np.uint16}
 class Plan:
     """A compiled device plan (qnb_plan) for one calibrated chain graph."""
 
-    OBSERVE = 1  # QNB_PLAN_OBSERVE: keep every top (no CONV/IP+RELU fusion)
+    OBSERVE = 1      # QNB_PLAN_OBSERVE: every top materialised (no fusion)
+    EXACT_FLOAT = 2  # QNB_PLAN_EXACT_FLOAT: FP32 conv / IP in the reference's exact arithmetic
 
     def __init__(self, descs, n_blobs, keep_alive, max_batch, use_cuda_graph=True, blob_ids=None, flags=0):
         self._keep = keep_alive
@@ -269,6 +270,9 @@ class Net:
                     d.bias = barr.ctypes.data
             top = l["top"][0]
             d.inspect_top = 1 if top in self.graph.get("inspect", ()) else 0
+            if l.get("pseudo_qv") is not None:
+                d.top_has_qv = 1
+                d.top_qv = QVals(*l["pseudo_qv"].as_tuple())
             if l["top_data_type"] in G.QUANT:
                 qv = self.blob_qv.get(top)
                 if qv is None:
@@ -305,33 +309,73 @@ class Net:
         g["layers"] = layers
         return g
 
+    def pseudo_graph(self) -> dict:
+        """The execution Net::forward runs in PSEUDO mode (src/net.cpp:305-330, 379-389):
+        the float execution of observe_graph() with every top fake-quantized onto its
+        declared type (pseudo_quantize, src/quantizer.cpp:141-153; FP16 tops round through
+        half).  Each fake-quant is a QUANTIZER layer with FP32 bottom/top and the declared
+        type as compute type, carrying the blob's grid; a dropped QUANTIZER's fake-quant
+        lands on its bottom's value, which only it consumes (chain graphs)."""
+        g = copy.deepcopy(self.graph)
+        ren, layers = {}, []
+
+        def fake(blob, cur):
+            dt = self.blobs[blob]["dtype"]
+            if dt == G.FP32:
+                return cur
+            qv = None
+            if dt in G.QUANT:
+                qv = self.blob_qv.get(blob)
+                if qv is None:
+                    raise QnbError(5, "quantizer not finalized: " + G.range_key(self.aliases, blob))
+            top = blob + "__pseudo"
+            layers.append({"name": top, "kind": "quantizer", "bottom": [cur], "top": [top],
+                           "bottom_data_type": G.FP32, "compute_data_type": dt, "top_data_type": G.FP32,
+                           "pseudo_qv": qv})
+            return top
+
+        for l in g["layers"]:
+            if l.get("bottom"):
+                l["bottom"] = [ren.get(b, b) for b in l["bottom"]]
+            top = l["top"][0]
+            if l["kind"] == "quantizer":
+                ren[top] = fake(top, l["bottom"][0])
+                continue
+            l["bottom_data_type"] = l["compute_data_type"] = l["top_data_type"] = G.FP32
+            layers.append(l)
+            ren[top] = fake(top, top)
+        g["layers"] = layers
+        sink = G.sinks(self.graph)[-1]
+        return g, ren.get(sink, sink)
+
+    def _float_plan(self, graph: dict, batch: int, flags: int = 0) -> Plan:
+        """A plan over an all-FP32 execution graph with param_float() weights
+        (src/net.cpp:183-196: finalized weights dequantize)."""
+        saved, stash = self.graph, {}
+        self.graph = graph
+        try:
+            for l in graph["layers"]:
+                if l["kind"] in ("conv", "inner_product"):
+                    w = self.params.get(l["name"] + ".weight")
+                    if w is not None and w[1] != 0:
+                        stash[l["name"] + ".weight"] = w
+                        self.params[l["name"] + ".weight"] = (ops.dequantize(w[0], w[1], w[2]), 0, None)
+            descs, n_blobs, keep, ids = self.layer_descs()
+        finally:
+            self.params.update(stash)
+            self.graph = saved
+        return Plan(descs, n_blobs, keep, batch, False, ids, flags=flags)
+
     def observe(self, x: np.ndarray) -> np.ndarray:
-        """Net::forward in OBSERVE mode on the device: FP32 (TF32 tensor-core) execution and a
+        """Net::forward in OBSERVE mode on the device: FP32 execution (exact reference arithmetic) and a
         min / max reduction per blob (observe(), src/quantizer.cpp:58-68); the ranges widen the
         ones already recorded (src/net.cpp:206-209)."""
         if x.dtype.kind not in "f":
             raise QnbError(10, "OBSERVE on the device takes float inputs")
         x = x.astype(np.float32)
-        og = self.observe_graph()
-        saved = self.graph
-        self.graph = og
-        try:
-            params = {}
-            for l in og["layers"]:
-                if l["kind"] in ("conv", "inner_product"):
-                    w = self.params.get(l["name"] + ".weight")
-                    if w is not None and w[1] != 0:  # param_float(): finalized weights dequantize
-                        params[l["name"] + ".weight"] = w
-                        self.params[l["name"] + ".weight"] = (ops.dequantize(w[0], w[1], w[2]), 0, None)
-            try:
-                descs, n_blobs, keep, ids = self.layer_descs()
-            finally:
-                self.params.update(params)
-        finally:
-            self.graph = saved
-        plan = Plan(descs, n_blobs, keep, x.shape[0], False, ids, flags=Plan.OBSERVE)
+        plan = self._float_plan(self.observe_graph(), x.shape[0], Plan.OBSERVE | Plan.EXACT_FLOAT)
         out, seen = plan.observe_host(x)
-        for name, i in ids.items():
+        for name, i in plan.blob_ids.items():
             if i not in seen:
                 continue
             lo, hi = seen[i]
@@ -342,6 +386,17 @@ class Net:
             self.ranges[key] = (float(lo), float(hi))
         self._plans.clear()
         return out
+
+    def pseudo(self, x: np.ndarray) -> np.ndarray:
+        """Net::forward in PSEUDO mode on the device (fake-quant accuracy studies)."""
+        if x.dtype.kind not in "f":
+            raise QnbError(10, "PSEUDO on the device takes float inputs")
+        x = x.astype(np.float32)
+        key = ("pseudo", x.shape[0])
+        if key not in self._plans:
+            g, _ = self.pseudo_graph()
+            self._plans[key] = self._float_plan(g, x.shape[0], Plan.EXACT_FLOAT)
+        return self._plans[key].forward_host(x)
 
     def forward(self, inputs: dict) -> dict:
         """src/net.cpp:305-330: returns {sink: tensor} in the reference layout."""
@@ -354,5 +409,7 @@ class Net:
             raise QnbError(2, "shape mismatch")
         if self.mode == OBSERVE:
             return {G.sinks(self.graph)[-1]: self.observe(x)}
+        if self.mode == PSEUDO:
+            return {G.sinks(self.graph)[-1]: self.pseudo(x)}
         out = self.plan(x.shape[0]).forward_host(x)
         return {G.sinks(self.graph)[-1]: out}
