@@ -60,7 +60,8 @@ typedef enum {
   QNB_E_RATIO = 7,       /* "invalid rescale ratio" / "shift_bits out of range" */
   QNB_E_CUDA = 8,        /* CUDA runtime/driver error or no sm_100 device */
   QNB_E_OOM = 9,         /* device allocation failed */
-  QNB_E_UNSUPPORTED = 10 /* valid for the reference but not implemented here */
+  QNB_E_UNSUPPORTED = 10, /* valid for the reference but not implemented here */
+  QNB_E_IO = 11           /* std::runtime_error: "not a model file", "truncated model file", "cannot read: ..." */
 } qnb_status;
 
 /* qnet::QuantizerValues (include/qnet/quantizer_values.hpp:32-42). */
@@ -295,6 +296,35 @@ qnb_status qnb_plan_profile(qnb_plan* plan, const void* input, int64_t batch, vo
 qnb_status qnb_plan_observe(qnb_plan* plan, const void* input, int64_t batch, double* mins, double* maxs,
                             qnb_stream s);
 qnb_status qnb_plan_destroy(qnb_plan* plan);
+
+/* ---------------------------------------------------------------- QCNM model store
+ * The reference's binary model file (QCNM v1, src/model_store.cpp:123-206;
+ * include/qnet/model_store.hpp:29-60).  qnb_model_open maps the file and validates
+ * every record without copying: each record's payload pointer points into the mapping,
+ * so a plan built from it (qnb_layer_desc.weight = payload) packs the weights from the
+ * file bytes straight into device tiles with no host tensor in between. */
+typedef struct qnb_model qnb_model;
+
+typedef struct {
+  const char* name;    /* NUL-terminated copy of the record name ("<layer>.<slot>" or "blob:<key>") */
+  int32_t dtype;       /* qnb_dtype */
+  int32_t rank;
+  int64_t extents[8];
+  float f_min, f_max, scale, zero, one; /* calibration fields; calibrated when scale > 0 */
+  const void* payload; /* rank>0: prod(extents) * byte_width(dtype) bytes, inside the mapping */
+  int64_t payload_bytes;
+} qnb_record;
+
+/* load_model (src/model_store.cpp:177-206): QNB_E_IO with the reference's messages on
+ * a missing file, bad magic/version/dtype tag ("not a model file") or short payload
+ * ("truncated model file"); QNB_E_UNSUPPORTED for ranks above 8. */
+qnb_status qnb_model_open(const char* path, qnb_model** out);
+qnb_status qnb_model_count(const qnb_model* m, int64_t* n_records);
+qnb_status qnb_model_record(const qnb_model* m, int64_t i, qnb_record* out);
+qnb_status qnb_model_close(qnb_model* m);
+/* save_model (src/model_store.cpp:123-175): writes `<path>.tmp`, then renames it into
+ * place; QNB_E_ARG "record name too long: <name>" / "payload size mismatch: <name>". */
+qnb_status qnb_model_save(const char* path, const qnb_record* records, int64_t n_records);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -46,6 +46,8 @@ inline void throw_on(qnb_status st) {
     case QNB_E_DTYPE:
     case QNB_E_RATIO:
       throw std::invalid_argument(msg);
+    case QNB_E_IO:
+      throw std::runtime_error(msg);
     default:
       throw std::runtime_error("qnb: " + msg);
   }

@@ -337,7 +337,7 @@ class Reference(_Base):
         L.ref_net_output_names.argtypes = [C.c_void_p]
         L.ref_load_balance_loss.restype = C.c_double
         for fn in ("ref_net_set_param", "ref_net_param_info", "ref_net_param_data", "ref_net_set_range",
-                   "ref_net_get_range", "ref_net_finalize", "ref_net_set_mode", "ref_net_blob_qvals",
+                   "ref_net_get_range", "ref_net_finalize", "ref_net_save", "ref_net_load", "ref_net_set_mode", "ref_net_blob_qvals",
                    "ref_net_forward", "ref_net_output_info", "ref_net_output_data", "ref_net_forward_mt"):
             getattr(L, fn).argtypes = None
         L.ref_net_set_range.argtypes = [C.c_void_p, C.c_char_p, C.c_double, C.c_double]
@@ -439,6 +439,14 @@ class RefNet:
 
     def finalize(self):
         self.ref._check(self.L.ref_net_finalize(self.h))
+
+    def save(self, path: str):
+        """save_model(net.to_model(), path) (src/model_store.cpp:123-175)."""
+        self.ref._check(self.L.ref_net_save(self.h, path.encode()))
+
+    def load(self, path: str):
+        """net.load_weights(load_model(path)) (src/net.cpp:605-619)."""
+        self.ref._check(self.L.ref_net_load(self.h, path.encode()))
 
     def set_mode(self, mode: int):
         """0 PASSIVE, 1 OBSERVE, 2 PSEUDO, 3 QUANTIZED."""

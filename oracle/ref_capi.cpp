@@ -25,6 +25,7 @@
 #include "qnet/graph_json.hpp"
 #include "qnet/half.hpp"
 #include "qnet/memory_plan.hpp"
+#include "qnet/model_store.hpp"
 #include "qnet/moe.hpp"
 #include "qnet/net.hpp"
 #include "qnet/ops.hpp"
@@ -513,6 +514,13 @@ int ref_net_get_range(void* h, const char* key, double* lo, double* hi) {
 }
 int ref_net_finalize(void* h) {
   return guard([&] { static_cast<NetHandle*>(h)->net->finalize_quantizers(); });
+}
+// QCNM model store (src/model_store.cpp, Net::to_model / load_weights src/net.cpp:546-619).
+int ref_net_save(void* h, const char* path) {
+  return guard([&] { save_model(static_cast<NetHandle*>(h)->net->to_model(), path); });
+}
+int ref_net_load(void* h, const char* path) {
+  return guard([&] { static_cast<NetHandle*>(h)->net->load_weights(load_model(path)); });
 }
 int ref_net_set_mode(void* h, int mode) {
   return guard([&] { static_cast<NetHandle*>(h)->net->set_quant_mode(static_cast<QuantMode>(mode)); });

@@ -19,7 +19,7 @@ DTYPE_BY_NAME = {"fp32": FP32, "float": FP32, "fp16": FP16, "half": FP16, "int8"
 STATUS_NAMES = {
     0: "QNB_OK", 1: "QNB_E_ARG", 2: "QNB_E_SHAPE", 3: "QNB_E_GROUPS", 4: "QNB_E_EXTENT",
     5: "QNB_E_QVALS", 6: "QNB_E_DTYPE", 7: "QNB_E_RATIO", 8: "QNB_E_CUDA", 9: "QNB_E_OOM",
-    10: "QNB_E_UNSUPPORTED",
+    10: "QNB_E_UNSUPPORTED", 11: "QNB_E_IO",
 }
 
 
@@ -81,6 +81,14 @@ class LayerDesc(C.Structure):
     ]
 
 
+class Record(C.Structure):
+    """qnb_record (include/qnb.h): one QCNM record."""
+
+    _fields_ = [("name", C.c_char_p), ("dtype", C.c_int32), ("rank", C.c_int32), ("extents", C.c_int64 * 8),
+                ("f_min", C.c_float), ("f_max", C.c_float), ("scale", C.c_float), ("zero", C.c_float),
+                ("one", C.c_float), ("payload", C.c_void_p), ("payload_bytes", C.c_int64)]
+
+
 class PlanOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int64), ("use_cuda_graph", C.c_int32), ("flags", C.c_int32)]
 
@@ -98,6 +106,11 @@ _PLAN_SIGS = {
     "qnb_plan_observe": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.c_void_p]),
     "qnb_plan_destroy": (C.c_int, [C.c_void_p]),
+    "qnb_model_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "qnb_model_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "qnb_model_record": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Record)]),
+    "qnb_model_close": (C.c_int, [C.c_void_p]),
+    "qnb_model_save": (C.c_int, [C.c_char_p, C.POINTER(Record), C.c_int64]),
     "qnb_plan_step_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "qnb_plan_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,

@@ -208,6 +208,48 @@ class Net:
                         raise QnbError(5, "quantizer not finalized: " + l["name"] + ".weight")
         self.mode = mode
 
+    # ---- model store (src/net.cpp:546-619)
+    def to_model(self):
+        """Net::to_model: parameter records in layer order (FP16 layers' FP32 weights
+        narrowed), then one "blob:<key>" record per recorded range, keys sorted."""
+        from .model_store import Model, ParamRecord, set_record_qvals
+        recs = []
+        for l in self.graph["layers"]:
+            if l["kind"] not in ("conv", "inner_product"):
+                continue
+            bias = (l["conv"].get("bias_term", True) if l["kind"] == "conv" else l.get("bias_term", True))
+            for name in [l["name"] + ".weight"] + ([l["name"] + ".bias"] if bias else []):
+                p = self.params.get(name)
+                if p is None:
+                    continue
+                arr, dt, qv = p
+                is_weight = name.endswith(".weight")
+                if is_weight and l["compute_data_type"] in G.QUANT and dt != G.DTYPE_CODE[l["compute_data_type"]]:
+                    raise QnbError(5, "quantizer not finalized: " + name)
+                if is_weight and l["compute_data_type"] == G.FP16 and dt == 0:
+                    arr, dt = ops.cast_float(np.ascontiguousarray(arr, np.float32), 0, 1), 1
+                arr = np.ascontiguousarray(arr, NP_OF[dt])
+                r = ParamRecord(name, dt, tuple(arr.shape), payload=arr.view(np.uint8).reshape(-1))
+                if qv is not None:
+                    set_record_qvals(r, qv)
+                recs.append(r)
+        for key in sorted(self.ranges):
+            lo, hi = self.ranges[key]
+            recs.append(ParamRecord("blob:" + key, 0, (0,), float(np.float32(lo)), float(np.float32(hi))))
+        return Model(recs)
+
+    def load_weights(self, model) -> None:
+        """Net::load_weights: "blob:" records set ranges, the others set parameters (with
+        their quantizer values when the record is calibrated).  Parameter arrays are views
+        into the model's file mapping."""
+        from .model_store import record_qvals
+        for r in model.records:
+            if r.name.startswith("blob:"):
+                self.set_range(r.name[5:], r.f_min, r.f_max)
+                continue
+            self.set_param(r.name, r.array(), r.dtype, record_qvals(r) if r.scale > 0 else None)
+        self._model_keepalive = model
+
     def blob_qvals(self, blob):
         return self.blob_qv.get(blob)
 
