@@ -1494,14 +1494,34 @@ __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
     const int32_t* w = p.ws + row * row_stride + (int64_t)nt * p.n_rows;
     int32_t d[4] = {0, 0, 0, 0};
     int32_t rs = 0;
-    for (int ks = 0; ks < p.ksplit; ++ks) {
+    int ks = 0;
+    // 4 splits per round: 8 independent L2 loads in flight per thread
+    for (; ks + 4 <= p.ksplit; ks += 4) {
+      int4 v[4];
+      int32_t r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t* ws = w + (ks + u) * split_stride;
+        v[u] = __ldcg(reinterpret_cast<const int4*>(ws + j));  // n_per_tile % 16 == 0
+        r[u] = __ldcg(ws + p.ones_col);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        d[0] += v[u].x;
+        d[1] += v[u].y;
+        d[2] += v[u].z;
+        d[3] += v[u].w;
+        rs += r[u];
+      }
+    }
+    for (; ks < p.ksplit; ++ks) {
       const int32_t* ws = w + ks * split_stride;
-      const int4 v = *reinterpret_cast<const int4*>(ws + j);  // n_per_tile % 16 == 0
+      const int4 v = __ldcg(reinterpret_cast<const int4*>(ws + j));
       d[0] += v.x;
       d[1] += v.y;
       d[2] += v.z;
       d[3] += v.w;
-      rs += ws[p.ones_col];
+      rs += __ldcg(ws + p.ones_col);
     }
     uint8_t* dst = p.out + row * p.o_img + p.o_origin + o0;  // inner product: oh = ow = 1
     uint32_t packed = 0;

@@ -698,6 +698,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     const int64_t tiles = m_tiles * pk.n_tiles;
     int64_t ks = 148 / std::max<int64_t>(tiles, 1);
     ks = std::max<int64_t>(1, std::min<int64_t>(ks, pk.num_kb / 2));
+    if (const char* e = std::getenv("QNB_FC_KS_MAX")) ks = std::max<int64_t>(1, std::min<int64_t>(ks, atoi(e)));
     a.cluster = 1;
     if (ks > 1) {
       a.ksplit = (int32_t)ks;

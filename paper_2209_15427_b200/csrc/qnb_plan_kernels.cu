@@ -10,6 +10,7 @@
 //   softmax_rows   [dequant ->] softmax over rows (src/ops.cpp:445-467)
 //   unpack         NHWC -> NCHW for sinks
 #include <cuda_fp16.h>
+#include <cstdlib>
 
 #include "qnb_device.cuh"
 #include "qnb_internal.h"
@@ -228,6 +229,63 @@ __global__ void __launch_bounds__(256) pack_rgb_u8_kernel(const float* __restric
   }
 }
 
+// C-channel specialisation of pack_rgb_u8: the fast bins of all 4 x C values are
+// computed branch-free, the values near a bin edge (or NaN / huge) are collected in a
+// mask and redone by the exact path afterwards, so the common case carries no
+// divergent branches.
+template <int C>
+__global__ void __launch_bounds__(256) pack_rgb_c_kernel(const float* __restrict__ src, int H, int W,
+                                                         uint8_t* __restrict__ dst, DevLayout L, DevQ q,
+                                                         uint32_t fill) {
+  const int ry = threadIdx.x / kPackLanes, l = threadIdx.x % kPackLanes;
+  const int y = blockIdx.x * (256 / kPackLanes) + ry;
+  if (y >= H) return;
+  const int64_t n = blockIdx.y;
+  const int64_t plane = (int64_t)H * W;
+  const float* rowp = src + n * C * plane + (int64_t)y * W;
+  uint32_t* orow = reinterpret_cast<uint32_t*>(at(dst, L, n, y, 0));
+  const float invf = (float)q.inv, zf = (float)q.zero, lo = (float)q.i_min, hi = (float)q.i_max;
+  uint32_t fillw = 0;
+#pragma unroll
+  for (int c = C; c < 4; ++c) fillw |= (fill & 0xFFu) << (8 * c);
+  for (int xb = 0; xb < W; xb += 4 * kPackLanes) {
+    float v[4][C];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = xb + l + kPackLanes * i;
+#pragma unroll
+      for (int c = 0; c < C; ++c) v[i][c] = x < W ? __ldg(rowp + c * plane + x) : 0.0f;
+    }
+    uint32_t word[4], slow = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t w = fillw;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const float yf = __fmul_rn(v[i][c], invf);
+        const float r = rintf(yf);
+        const float d = fabsf(__fsub_rn(yf, r));
+        slow |= (d < __fsub_rn(0.5f, __fmaf_rn(4e-7f, fabsf(yf), 1e-6f)) ? 0u : 1u) << (i * C + c);
+        w |= ((uint32_t)(int)fminf(fmaxf(r + zf, lo), hi) & 0xFFu) << (8 * c);
+      }
+      word[i] = w;
+    }
+    if (slow) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+          if ((slow >> (i * C + c)) & 1u)
+            word[i] = (word[i] & ~(0xFFu << (8 * c))) | (((uint32_t)qz_slow(v[i][c], q) & 0xFFu) << (8 * c));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = xb + l + kPackLanes * i;
+      if (x < W) orow[x] = word[i];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ pool
 // Max over k x k windows (no padding).  Integer types compare raw values; float
 // types keep the first element unless a later one is strictly greater.
@@ -439,21 +497,55 @@ __device__ __noinline__ int64_t lrn_exact_q(const float* row, int c0, int c1, fl
   return qz(__double2float_rn(__ddiv_rn((double)x, pow(b, beta))), q);
 }
 
+// u8x4 max through the native 16-bit SIMD max (VIMNMX.U16x2; __vmaxu4 is a 7-op
+// emulation): the high byte of a u16 lane decides the u16 comparison, so the max over
+// raw words is right in bytes 1 and 3 and the max over words shifted left by 8 is right
+// in bytes 0 and 2 (as its bytes 1 and 3).
+struct MaxU8x4 {
+  uint32_t odd, even;
+  __device__ __forceinline__ void init(uint32_t w) {
+    odd = w;
+    even = w << 8;
+  }
+  __device__ __forceinline__ void add(uint32_t w) {
+    odd = __vmaxu2(odd, w);
+    even = __vmaxu2(even, w << 8);
+  }
+  __device__ __forceinline__ uint32_t get() const { return __byte_perm(odd, even, 0x3715); }
+};
+
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t sat_u8(float x) {  // integral x: clamp to [0, 255]
+  uint32_t q;
+  asm("cvt.rzi.sat.u8.f32 %0, %1;" : "=r"(q) : "f"(x));
+  return q;
+}
+
 // INT8 -> INT8 specialisation of pool_lrn (the AlexNet norm layers).  A block owns P
 // output pixels of one image.  Stage 1: thread (pixel, 16-channel chunk) loads the
-// PK x PK window of 16-byte vectors in one unrolled batch, pools with __vmaxu4 and
-// dequantises through a 256-entry table into smem.  Stage 2: thread (pixel, 4
-// channels) forms the 5-channel square sums from 8 cached values, evaluates the LRN in
+// PK x PK window of 16-byte vectors in one unrolled batch, pools with 16-bit SIMD max
+// and dequantises through a 256-entry table into smem.  Stage 2: thread (pixel, 4
+// channels) forms the 5-channel square sums from 12 cached values, evaluates the LRN in
 // float (MUFU log2/exp2, relative error < 1.1e-6) and keeps that integer unless the
 // value sits within 3e-6 relative of a rounding boundary, where the exact double
-// reference formula decides.  Work assignment is fixed per thread (no divisions).
-template <int PK>
+// reference formula decides.  HALF2: local_size 5 (no window predicates).  Work
+// assignment is fixed per thread (no divisions).
+template <int PK, bool HALF2>
 __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a) {
   extern __shared__ float lrn_smem[];
   __shared__ float lut[256];
   __shared__ int32_t in_off[256], out_off[256];
   const int C = (int)a.D.c;
-  const int P = lrn_pixels(C);
+  const int P = a.pix;
   const int pix_per_img = (int)(a.D.h * a.D.w);
   const int tiles_per_img = (pix_per_img + P - 1) / P;
   const int64_t n = blockIdx.x / tiles_per_img;
@@ -473,27 +565,39 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
   {
     const int chunks = C >> 4;
     const int ch = threadIdx.x % chunks, pl = threadIdx.x / chunks, pstride = kLrnThreads / chunks;
+    const int srow = (int)a.S.row, spix = (int)a.S.pix;
     if (pl < pstride) {
       for (int pi = pl; pi < np; pi += pstride) {
         const uint8_t* wp = sbase + in_off[pi] + ch * 16;
-        uint4 v[PK > 0 ? PK * PK : 1];
+        uint32_t w4[4];
         if constexpr (PK > 0) {
+          uint4 v[PK * PK];
 #pragma unroll
           for (int ky = 0; ky < PK; ++ky)
 #pragma unroll
             for (int kx = 0; kx < PK; ++kx)
-              v[ky * PK + kx] = __ldg(reinterpret_cast<const uint4*>(wp + ky * a.S.row + kx * a.S.pix));
+              v[ky * PK + kx] = __ldg(reinterpret_cast<const uint4*>(wp + ky * srow + kx * spix));
+          MaxU8x4 m[4];
+          m[0].init(v[0].x);
+          m[1].init(v[0].y);
+          m[2].init(v[0].z);
+          m[3].init(v[0].w);
 #pragma unroll
           for (int i = 1; i < PK * PK; ++i) {
-            v[0].x = __vmaxu4(v[0].x, v[i].x);
-            v[0].y = __vmaxu4(v[0].y, v[i].y);
-            v[0].z = __vmaxu4(v[0].z, v[i].z);
-            v[0].w = __vmaxu4(v[0].w, v[i].w);
+            m[0].add(v[i].x);
+            m[1].add(v[i].y);
+            m[2].add(v[i].z);
+            m[3].add(v[i].w);
           }
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) w4[qd] = m[qd].get();
         } else {
-          v[0] = __ldg(reinterpret_cast<const uint4*>(wp));
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(wp));
+          w4[0] = v.x;
+          w4[1] = v.y;
+          w4[2] = v.z;
+          w4[3] = v.w;
         }
-        const uint32_t w4[4] = {v[0].x, v[0].y, v[0].z, v[0].w};
         float4* row = reinterpret_cast<float4*>(lrn_smem + pi * C + ch * 16);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd)
@@ -505,20 +609,21 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
   __syncthreads();
   // ---- stage 2
   const float fa_n = (float)a.a_n, fbeta = (float)a.beta, fk = (float)a.k, finv = (float)(1.0 / a.out_q.scale);
-  const int half = (int)a.half;
+  const int half = HALF2 ? 2 : (int)a.half;
   const int quads = C >> 2;
   const int qi = threadIdx.x % quads, pl = threadIdx.x / quads, pstride = kLrnThreads / quads;
   if (pl >= pstride) return;
   const int c4 = qi * 4;
-  const float zf = (float)a.out_q.zero, lo = (float)a.out_q.i_min, hi = (float)a.out_q.i_max;
+  const float zf = (float)a.out_q.zero;
+  const bool has_lo = c4 >= 4, has_hi = c4 + 4 < C;
   for (int pi = pl; pi < np; pi += pstride) {
     const float* row = lrn_smem + pi * C;
     // squares of channels c4-4 .. c4+7 (0 outside [0, C)): three float4 smem loads
     float sq[12], xs[4];
     {
       const float4 mid = *reinterpret_cast<const float4*>(row + c4);
-      const float4 lo4 = c4 >= 4 ? *reinterpret_cast<const float4*>(row + c4 - 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 hi4 = c4 + 4 < C ? *reinterpret_cast<const float4*>(row + c4 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 lo4 = has_lo ? *reinterpret_cast<const float4*>(row + c4 - 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 hi4 = has_hi ? *reinterpret_cast<const float4*>(row + c4 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float v[12] = {lo4.x, lo4.y, lo4.z, lo4.w, mid.x, mid.y, mid.z, mid.w, hi4.x, hi4.y, hi4.z, hi4.w};
 #pragma unroll
       for (int u = 0; u < 12; ++u) sq[u] = __fmul_rn(v[u], v[u]);
@@ -527,26 +632,25 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
       xs[2] = mid.z;
       xs[3] = mid.w;
     }
-    uint32_t packed = 0, slow = 0;
+    uint32_t q[4], slow = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float sf = 0.0f;
 #pragma unroll
       for (int d = -2; d <= 2; ++d)
-        if (d >= -half && d <= half) sf = __fadd_rn(sf, sq[4 + u + d]);
-      const float x = xs[u];
+        if (HALF2 || (d >= -half && d <= half)) sf = __fadd_rn(sf, sq[4 + u + d]);
       const float base = __fmaf_rn(fa_n, sf, fk);
-      const float rden = ex2_approx(-__fmul_rn(fbeta, __log2f(base)));
-      const float t = __fmul_rn(__fmul_rn(x, rden), finv);
+      const float rden = ex2_ftz(-__fmul_rn(fbeta, lg2_ftz(base)));
+      const float t = __fmul_rn(__fmul_rn(xs[u], rden), finv);
       const float r = rintf(t);
       // decided unless within the float path's error bound of a tie (NaN/huge: exact path)
       slow |= (fabsf(__fsub_rn(t, r)) < __fsub_rn(0.5f, __fmaf_rn(3e-6f, fabsf(t), 1e-6f)) ? 0u : 1u) << u;
-      const uint32_t qv = (uint32_t)(int)fminf(fmaxf(r + zf, lo), hi);
-      packed |= (qv & 0xFFu) << (8 * u);
+      q[u] = sat_u8(r + zf);  // INT8Q grid: i_min 0, i_max 255
     }
-    if (slow != 0 || half > 2) {  // rare: the reference's exact double arithmetic
+    uint32_t packed = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
+    if (slow != 0 || (!HALF2 && half > 2)) {  // rare: the reference's exact double arithmetic
       for (int u = 0; u < 4; ++u) {
-        if (half <= 2 && !((slow >> u) & 1u)) continue;
+        if ((HALF2 || half <= 2) && !((slow >> u) & 1u)) continue;
         const int c = c4 + u;
         const uint32_t qv =
             (uint32_t)lrn_exact_q(row, max(0, c - half), min(C - 1, c + half), row[c], a.k, a.a_n, a.beta, a.out_q);
@@ -685,6 +789,11 @@ void launch_pack_input(const PackArgs& p, cudaStream_t s) {
   if (p.src_dtype == QNB_FP32 && p.dst_dtype == QNB_INT8Q && p.op == PACK_QUANTIZE && p.L.c_phys == 4 &&
       p.C <= 4 && p.L.pix == 4 && p.L.origin % 4 == 0 && p.L.row % 4 == 0 && p.L.img % 4 == 0) {
     dim3 grid((unsigned)ceil_div(p.H, 256 / kPackLanes), (unsigned)p.N);
+    if (p.C == 3 && !std::getenv("QNB_PACK_GENERIC")) {
+      pack_rgb_c_kernel<3><<<grid, 256, 0, s>>>((const float*)p.src, (int)p.H, (int)p.W, p.dst, p.L, p.q,
+                                                (uint32_t)(int64_t)p.fill);
+      return;
+    }
     pack_rgb_u8_kernel<<<grid, 256, 0, s>>>((const float*)p.src, (int)p.C, (int)p.H, (int)p.W, p.dst, p.L, p.q,
                                             (uint32_t)(int64_t)p.fill, 1);
     return;
@@ -707,6 +816,16 @@ void launch_pool(const PoolArgs& p, cudaStream_t s) {
   }
 }
 
+template <int PK, bool H2>
+static void launch_plq8(const PoolLrnArgs& b, int64_t blocks, size_t sm, cudaStream_t s) {
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(pool_lrn_q8_kernel<PK, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    set = true;
+  }
+  pool_lrn_q8_kernel<PK, H2><<<(unsigned)blocks, kLrnThreads, sm, s>>>(b);
+}
+
 void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -721,27 +840,20 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
                   a.S.origin % 16 == 0 && a.D.pix % 4 == 0 && a.D.row % 4 == 0 && a.D.img % 4 == 0 &&
                   a.D.origin % 4 == 0;
   // windows never leave the input: (out-1)*s + k <= in for floor-mode pooling
-  if (q8 && a.pool_k == 3) {
-    static bool at3 = false;
-    if (!at3) {
-      cudaFuncSetAttribute(pool_lrn_q8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      at3 = true;
-    }
-    pool_lrn_q8_kernel<3><<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
-  } else if (q8 && a.pool_k == 2) {
-    static bool at2 = false;
-    if (!at2) {
-      cudaFuncSetAttribute(pool_lrn_q8_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      at2 = true;
-    }
-    pool_lrn_q8_kernel<2><<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
-  } else if (q8 && a.pool_k == 0) {
-    static bool at0 = false;
-    if (!at0) {
-      cudaFuncSetAttribute(pool_lrn_q8_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      at0 = true;
-    }
-    pool_lrn_q8_kernel<0><<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
+  if (q8 && (a.pool_k == 3 || a.pool_k == 2 || a.pool_k == 0)) {
+    static int env_pix = [] {
+      const char* e = std::getenv("QNB_LRN_PIX");
+      return e ? atoi(e) : 0;
+    }();
+    PoolLrnArgs b = a;
+    b.pix = std::min(64, lrn_pixels(a.D.c));  // 64 pixels: more resident blocks (measured best)
+    if (env_pix > 0) b.pix = std::min(env_pix, lrn_pixels(a.D.c));
+    const int64_t qblocks = a.D.n * ceil_div(a.D.h * a.D.w, b.pix);
+    const size_t qsm = (size_t)b.pix * a.D.c * 4;
+    const bool h2 = a.half == 2;
+    if (a.pool_k == 3) h2 ? launch_plq8<3, true>(b, qblocks, qsm, s) : launch_plq8<3, false>(b, qblocks, qsm, s);
+    else if (a.pool_k == 2) h2 ? launch_plq8<2, true>(b, qblocks, qsm, s) : launch_plq8<2, false>(b, qblocks, qsm, s);
+    else h2 ? launch_plq8<0, true>(b, qblocks, qsm, s) : launch_plq8<0, false>(b, qblocks, qsm, s);
   } else {
     pool_lrn_kernel<<<(unsigned)blocks, kLrnThreads, sm, s>>>(a);
   }

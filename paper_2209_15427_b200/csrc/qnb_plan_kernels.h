@@ -73,6 +73,7 @@ struct PoolLrnArgs {
   int64_t pool_k, pool_s;  // pool_k = 0: no pooling stage
   int64_t half;
   double a_n, beta, k;
+  int32_t pix;  // output pixels per block (pool_lrn_q8); set by launch_pool_lrn
 };
 
 enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3, CVT_PSEUDO = 4 };
