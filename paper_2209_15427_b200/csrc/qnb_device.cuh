@@ -44,10 +44,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Wait on a barrier that also receives arrivals from the peer CTA.  The default
+// (acquire.cta) form, as CUTLASS's 2-SM pipelines use: the operands it guards are read
+// by the tensor core, and cluster-scope acquire costs an L1 invalidate per poll.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 
 // ------------------------------------------------------------ async copies
 __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gmem_src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src)
+               : "memory");
+}
+// L1-allocating variant: neighbouring im2col rows re-read the same input bytes.
+__device__ __forceinline__ void cp_async_16_ca(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                "l"(gmem_src)
                : "memory");
 }
@@ -146,6 +156,50 @@ __device__ __forceinline__ void tc_commit_multicast(uint64_t* bar, uint16_t mask
           smem_u32(bar)),
       "h"(mask)
       : "memory");
+}
+
+// ------------------------------------------------- CTA pairs (cta_group::2)
+// The two CTAs of a cluster of 2 run one M = 256 MMA: each holds 128 rows of A and half
+// of B's N rows at the same smem offsets; only rank 0 issues.
+__device__ __forceinline__ void tmem_alloc2(uint32_t* smem_result, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
+               "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish2() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// Pair MMA completion -> arrive on the mbarrier at `bar`'s offset in every CTA of `mask`.
+__device__ __forceinline__ void tc_commit2_multicast(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// Arrive (relaxed) on the mbarrier at `bar`'s offset in CTA `rank`: for hand-backs
+// ordered by tcgen05.fence::before_thread_sync (no memory to publish).
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+// Arrive (default release.cta semantics, as CUTLASS's umma_arrive_2x1SM_sm0) on the
+// mbarrier at `bar`'s offset in CTA `rank`; release.cluster would emit MEMBAR.ALL.GPU.
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void umma2_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 // One lane of a converged warp (elect.sync): lets a whole warp run the MMA-issue loop

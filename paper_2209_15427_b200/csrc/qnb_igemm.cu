@@ -240,6 +240,12 @@ __device__ __noinline__ void splitk_fixup(const IgemmArgs& p, int64_t mt, int nt
   if (et == 0) *sema = 0;  // self-reset (graph replays reuse the counters)
 }
 
+// Hands an accumulator buffer back to the MMA issuer (rank 0's barrier in pair mode).
+__device__ __forceinline__ void epi_release(const IgemmArgs& p, uint64_t* bar) {
+  if (p.pair) mbar_arrive_cluster_relaxed(bar, 0);
+  else mbar_arrive(bar);
+}
+
 template <int MODE, int F = 0>
 __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem, uint64_t* acc_full,
                                                uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
@@ -269,7 +275,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     if (p.dbg & 1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) epi_release(p, &acc_empty[buf]);
       continue;
     }
     const uint32_t trow = tmem + buf * (uint32_t)tcols + ((uint32_t)(32 * quarter) << 16);
@@ -313,7 +319,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) epi_release(p, &acc_empty[buf]);
       if (p.tile_sema != nullptr) splitk_fixup(p, mt, c.nt, k, reinterpret_cast<int32_t*>(lut));
       continue;
     }
@@ -348,7 +354,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) epi_release(p, &acc_empty[buf]);
       continue;
     }
     int64_t rowsum = 0;
@@ -402,7 +408,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        if (lane == 0) epi_release(p, &acc_empty[buf]);
         continue;
       }
     }
@@ -481,7 +487,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    if (lane == 0) epi_release(p, &acc_empty[buf]);
   }
 }
 
@@ -661,10 +667,18 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         }
         const int32_t off = chunk_tab[kb * 8 + jc];
         uint8_t* dst = sA + (size_t)s * a_stage;
+        if (p.dbg & 16) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = warp * 32 + rr + 4 * i;
-          if (valid & (1u << i)) cp_async_16(dst + row * 128 + ((jc ^ (row & 7)) << 4), base[i] + off);
+          for (int i = 0; i < 8; ++i) {
+            const int row = warp * 32 + rr + 4 * i;
+            if (valid & (1u << i)) cp_async_16_ca(dst + row * 128 + ((jc ^ (row & 7)) << 4), base[i] + off);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int row = warp * 32 + rr + 4 * i;
+            if (valid & (1u << i)) cp_async_16(dst + row * 128 + ((jc ^ (row & 7)) << 4), base[i] + off);
+          }
         }
         cp_async_arrive_noinc(&full[s]);
       }
@@ -717,6 +731,206 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     tc_fence_after();
     tmem_dealloc(tmem, (uint32_t)(2 * p.tmem_cols));
   }
+}
+
+
+// ---------------------------------------------------------------- CTA-pair kernel
+// cta_group::2 variant of the gather kernel for layers whose B tile (one group, all N
+// rows) fits in two SMs' shared memory: the cluster pair runs M = 256 tiles (128 A
+// rows per CTA), each CTA keeps HALF of B's N rows resident for the whole launch, so
+// the A gather is the only operand stream (the stock kernel re-streams all of B with
+// every tile, about half of its L2->SM traffic on AlexNet conv2).  A pair serves one
+// group.  Synchronisation:
+//   full[s]      rank 0: 128 local cp.async arrivals + 1 forwarded by rank 1's warp 4
+//                once rank 1's stage s has landed; rank 1: its 128 arrivals
+//   empty[s]     one multicast pair-commit per stage (both CTAs)
+//   acc_full     one multicast pair-commit per tile (both CTAs)
+//   acc_empty    rank 0: 8 local + 8 remote epilogue-warp arrivals
+//   bfull        each CTA's resident B half (expect_tx); bpeer on rank 0: rank 1's B
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_constant__ IgemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int nb2 = p.n_rows >> 1;                 // B rows held by this CTA
+  const int bh = nb2 * 128;                      // bytes of one K block of the B half
+  const int S = p.pair;                          // A stages (host-chosen)
+  constexpr int a_stage = kBM * 128;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)S * a_stage;
+  uint64_t* full = (uint64_t*)(sB + (size_t)p.num_kb * bh);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* acc_full = empty + kMaxStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bfull = acc_empty + 2;
+  uint64_t* bpeer = bfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(bpeer + 1);
+  int64_t* rowoff = (int64_t*)(tmem_slot + 4);   // [2][128]
+  int32_t* chunk_s = (int32_t*)(rowoff + 256);
+  const int n_chunks = p.num_kb * 8;
+  const bool chunks_in_smem = n_chunks <= kMaxChunkSmem;
+  if (chunks_in_smem)
+    for (int i = threadIdx.x; i < n_chunks; i += blockDim.x) chunk_s[i] = __ldg(p.chunk_off + i);
+  const int32_t* chunk_tab = chunks_in_smem ? chunk_s : p.chunk_off;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int64_t m_tiles = (p.m_total + kBM - 1) / kBM;
+  const int64_t m_pairs = (m_tiles + 1) / 2;
+  // pairs are split evenly over the groups; each pair streams only its group's tiles
+  const int64_t pid = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int64_t ppg = npairs / p.groups;
+  const int64_t g = pid / ppg;
+  const bool idle = g >= p.groups;
+  const int64_t cid = idle ? 0 : g * m_pairs + (pid - g * ppg);
+  const int64_t ncl = ppg;
+  const int64_t total = idle ? 0 : (g + 1) * m_pairs;
+  const int64_t pix_per_img = (int64_t)p.oh * p.ow;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], (rank == 0 && !(p.dbg & 32)) ? 129u : 128u);  // dbg 32: timing probe, no coupling
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 2 * kEpiWarps);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bpeer, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc2(tmem_slot, (uint32_t)(2 * p.tmem_cols));
+    tmem_relinquish2();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------------------------------------------------------- producers
+    const int t = threadIdx.x;
+    const int jc = lane & 7, rr = lane >> 3;
+    uint32_t it = 0, par = 0;
+    for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
+      const TileCoord c = tile_of(ct, m_pairs, 1);
+      const int64_t mt = c.mt * 2 + rank;
+      {
+        const int64_t row = mt * kBM + t;
+        int64_t off = -1;
+        if (row < p.m_total) {
+          const uint32_t img = (uint32_t)row / (uint32_t)pix_per_img;
+          const uint32_t rem = (uint32_t)row - img * (uint32_t)pix_per_img;
+          const uint32_t oy = rem / (uint32_t)p.ow, ox = rem - oy * (uint32_t)p.ow;
+          off = img * p.a_img + (int64_t)oy * p.stride_h * p.a_row + (int64_t)ox * p.stride_w * p.a_pix +
+                (int64_t)c.g * p.a_group + p.a_origin;
+        }
+        rowoff[par * 128 + t] = off;
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      const uint8_t* base[8];
+      uint32_t valid = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t off = rowoff[par * 128 + warp * 32 + rr + 4 * i];
+        base[i] = p.a + (off < 0 ? 0 : off);
+        valid |= (off >= 0 ? 1u : 0u) << i;
+      }
+      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+        const int s = (int)(it % S);
+        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+        const int32_t off = chunk_tab[kb * 8 + jc];
+        uint8_t* dst = sA + (size_t)s * a_stage;
+        if (p.dbg & 16) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int row = warp * 32 + rr + 4 * i;
+            if (valid & (1u << i)) cp_async_16_ca(dst + row * 128 + ((jc ^ (row & 7)) << 4), base[i] + off);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int row = warp * 32 + rr + 4 * i;
+            if (valid & (1u << i)) cp_async_16(dst + row * 128 + ((jc ^ (row & 7)) << 4), base[i] + off);
+          }
+        }
+        cp_async_arrive_noinc(&full[s]);
+      }
+    }
+  } else if (warp == 4) {
+    // resident B half: rows [rank * nb2, rank * nb2 + nb2) of every K block of the group
+    if (!idle && elect_one()) {
+      mbar_arrive_expect_tx(bfull, (uint32_t)(p.num_kb * bh));
+      const uint8_t* bg = p.b + (int64_t)g * p.num_kb * (p.n_rows * 128);
+      for (int kb = 0; kb < p.num_kb; ++kb)
+        bulk_g2s(sB + (size_t)kb * bh, bg + (int64_t)kb * p.n_rows * 128 + (int64_t)rank * bh, (uint32_t)bh, bfull);
+    }
+    __syncwarp();
+    if (!idle) mbar_wait(bfull, 0);
+    if (rank == 1) {
+      // ------------------------------------------------------- forwarder (rank 1)
+      if (!idle && elect_one()) mbar_arrive_cluster(bpeer, 0);
+      __syncwarp();
+      uint32_t it = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl)
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = (int)(it % S);
+          mbar_wait(&full[s], (it / S) & 1);
+          if (elect_one() && !(p.dbg & 32)) {
+            fence_proxy_async_smem();
+            mbar_arrive_cluster(&full[s], 0);
+          }
+          __syncwarp();
+        }
+    } else {
+      // ------------------------------------------------------- MMA issuer (rank 0)
+      if (!idle) mbar_wait_cluster(bpeer, 0);
+      uint32_t idesc = make_idesc<KIND>(p.n_rows);
+      idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24);  // M = 256 (pair)
+      const bool mma_on = !(p.dbg & 2);
+      uint32_t it = 0, j = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
+        const uint32_t buf = j & 1;
+        mbar_wait_cluster(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = (int)(it % S);
+          mbar_wait_cluster(&full[s], (it / S) & 1);
+          tc_fence_after();
+          const uint64_t ad = smem_desc_sw(sA + (size_t)s * a_stage, 128);
+          const uint64_t bd = smem_desc_sw(sB + (size_t)kb * bh, 128);
+          if (elect_one()) {
+            if (mma_on)
+              for (int k = 0; k < 4; ++k) umma2_i8(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            tc_commit2_multicast(&empty[s], 3);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) tc_commit2_multicast(&acc_full[buf], 3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    run_epilogue(p, tmem, acc_full, acc_empty, m_pairs, total, cid, ncl, 2, rank, warp, lane, nullptr, (warp - 5) >> 2,
+                 2);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, (uint32_t)(2 * p.tmem_cols));
+  }
+}
+
+static size_t igemm_pair_smem_bytes(int n_rows, int num_kb, int stages) {
+  return 1024 + (size_t)stages * kBM * 128 + (size_t)num_kb * (n_rows / 2) * 128 + (2 * kMaxStages + 6) * 8 + 16 +
+         2 * 128 * 8 + kMaxChunkSmem * 4;
 }
 
 
@@ -1667,6 +1881,39 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     return fail(QNB_E_ARG, "row-Hankel mode is INT8 only");
   }
   const int64_t m_tiles = ceil_div(a.m_total, kBM);
+  if constexpr (KIND == KIND_I8) {
+    // CTA-pair path: one group's B split over the pair's smem, resident for the launch
+    static const bool no_pair = std::getenv("QNB_NO_PAIR") != nullptr;
+    const int64_t npairs = (num_sms() / 2 / std::max<int64_t>(groups, 1)) * groups;
+    const size_t fixed = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0);
+    const size_t cap = 227 * 1024;
+    const int stages = fixed < cap ? (int)std::min<size_t>(kMaxStages, (cap - fixed) / (kBM * 128)) : 0;
+    if (!no_pair && !a.a_tma && a.ksplit == 1 && a.n_tiles == 1 && a.kbytes == 128 && a.n_rows % 16 == 0 &&
+        a.n_rows <= 256 && 2 * a.tmem_cols <= 512 && m_tiles >= 2 && npairs >= groups && stages >= 4 &&
+        a.epi_mode != EPIM_RAW32) {
+      a.pair = stages;
+      a.cluster = 2;
+      const size_t smem = igemm_pair_smem_bytes(a.n_rows, a.num_kb, stages);
+      QNB_CUDA(cudaFuncSetAttribute(igemm_pair_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(2 * npairs));
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_pair_kernel<KIND>, a));
+      count_launch();
+      QNB_CUDA(cudaGetLastError());
+      return QNB_OK;
+    }
+  }
+  a.pair = 0;
   a.cluster = (m_tiles >= 2 && a.cluster != 1) ? 2 : 1;
   const int64_t ctiles = ceil_div(m_tiles, a.cluster) * a.n_tiles * a.ksplit * groups;
   const int64_t nclusters = std::min<int64_t>(ctiles, num_sms() / a.cluster);

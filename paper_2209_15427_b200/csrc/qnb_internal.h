@@ -119,6 +119,9 @@ struct IgemmArgs {
   // the last CTA of a tile to finish sums the partials and runs the INT8 epilogue, so no
   // separate igemm_finalize launch is needed
   int32_t* tile_sema;
+  // CTA-pair mode (igemm_pair_kernel): cta_group::2 MMAs with M = 256 and each CTA's
+  // half of B resident in smem for the whole launch.
+  int32_t pair;
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)

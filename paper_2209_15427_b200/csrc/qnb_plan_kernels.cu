@@ -287,30 +287,58 @@ __global__ void __launch_bounds__(256) pack_rgb_c_kernel(const float* __restrict
 }
 
 // ------------------------------------------------------------------ pool
+// u8x4 max through the native 16-bit SIMD max (VIMNMX.U16x2; __vmaxu4 is a 7-op
+// emulation): the high byte of a u16 lane decides the u16 comparison, so the max over
+// raw words is right in bytes 1 and 3 and the max over words shifted left by 8 is right
+// in bytes 0 and 2 (as its bytes 1 and 3).
+struct MaxU8x4 {
+  uint32_t odd, even;
+  __device__ __forceinline__ void init(uint32_t w) {
+    odd = w;
+    even = w << 8;
+  }
+  __device__ __forceinline__ void add(uint32_t w) {
+    odd = __vmaxu2(odd, w);
+    even = __vmaxu2(even, w << 8);
+  }
+  __device__ __forceinline__ uint32_t get() const { return __byte_perm(odd, even, 0x3715); }
+};
+
 // Max over k x k windows (no padding).  Integer types compare raw values; float
 // types keep the first element unless a later one is strictly greater.
 __global__ void pool_u8_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst, DevLayout D,
                                int64_t k, int64_t st) {
-  const int64_t chunks = S.c_phys / 16;
-  const int64_t total = D.n * D.h * D.w * chunks;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ch = i % chunks, pix = i / chunks;
-    const int64_t ox = pix % D.w, oy = (pix / D.w) % D.h, n = pix / (D.w * D.h);
-    uint4 m = make_uint4(0, 0, 0, 0);
-    for (int64_t ky = 0; ky < k; ++ky) {
-      const int64_t iy = oy * st + ky;
-      if (iy >= S.h) continue;
-      for (int64_t kx = 0; kx < k; ++kx) {
-        const int64_t ix = ox * st + kx;
-        if (ix >= S.w) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(at(src, S, n, iy, ix) + ch * 16);
-        m.x = __vmaxu4(m.x, v.x);
-        m.y = __vmaxu4(m.y, v.y);
-        m.z = __vmaxu4(m.z, v.z);
-        m.w = __vmaxu4(m.w, v.w);
+  const int chunks = (int)(S.c_phys / 16);
+  const int total = (int)(D.n * D.h * D.w * chunks);  // host checks < 2^31
+  const int Dw = (int)D.w, Dh = (int)D.h, Sw = (int)S.w, Sh = (int)S.h, K = (int)k, ST = (int)st;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int ch = i % chunks, pix = i / chunks;
+    const int ox = pix % Dw, oy = (pix / Dw) % Dh, n = pix / (Dw * Dh);
+    MaxU8x4 m[4];
+    bool first = true;
+    for (int ky = 0; ky < K; ++ky) {
+      const int iy = oy * ST + ky;
+      if (iy >= Sh) continue;
+      for (int kx = 0; kx < K; ++kx) {
+        const int ix = ox * ST + kx;
+        if (ix >= Sw) continue;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(at(src, S, n, iy, ix) + ch * 16));
+        if (first) {
+          m[0].init(v.x);
+          m[1].init(v.y);
+          m[2].init(v.z);
+          m[3].init(v.w);
+          first = false;
+        } else {
+          m[0].add(v.x);
+          m[1].add(v.y);
+          m[2].add(v.z);
+          m[3].add(v.w);
+        }
       }
     }
-    *reinterpret_cast<uint4*>(at(dst, D, n, oy, ox) + ch * 16) = m;
+    *reinterpret_cast<uint4*>(at(dst, D, n, oy, ox) + ch * 16) =
+        make_uint4(m[0].get(), m[1].get(), m[2].get(), m[3].get());
   }
 }
 
@@ -496,23 +524,6 @@ __device__ __noinline__ int64_t lrn_exact_q(const float* row, int c0, int c1, fl
   const double b = __dadd_rn(k, __dmul_rn(a_n, sum));
   return qz(__double2float_rn(__ddiv_rn((double)x, pow(b, beta))), q);
 }
-
-// u8x4 max through the native 16-bit SIMD max (VIMNMX.U16x2; __vmaxu4 is a 7-op
-// emulation): the high byte of a u16 lane decides the u16 comparison, so the max over
-// raw words is right in bytes 1 and 3 and the max over words shifted left by 8 is right
-// in bytes 0 and 2 (as its bytes 1 and 3).
-struct MaxU8x4 {
-  uint32_t odd, even;
-  __device__ __forceinline__ void init(uint32_t w) {
-    odd = w;
-    even = w << 8;
-  }
-  __device__ __forceinline__ void add(uint32_t w) {
-    odd = __vmaxu2(odd, w);
-    even = __vmaxu2(even, w << 8);
-  }
-  __device__ __forceinline__ uint32_t get() const { return __byte_perm(odd, even, 0x3715); }
-};
 
 __device__ __forceinline__ float lg2_ftz(float x) {
   float y;
@@ -807,7 +818,7 @@ void launch_pack_input(const PackArgs& p, cudaStream_t s) {
 void launch_pool(const PoolArgs& p, cudaStream_t s) {
   if (p.dtype == QNB_INT8Q && p.S.c_phys % 16 == 0 && p.D.c_phys == p.S.c_phys && p.S.c == p.S.c_phys &&
       p.S.pix % 16 == 0 && p.D.pix % 16 == 0 && p.S.origin % 16 == 0 && p.D.origin % 16 == 0 && p.S.row % 16 == 0 &&
-      p.D.row % 16 == 0) {
+      p.D.row % 16 == 0 && p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16) < (int64_t(1) << 31)) {
     pool_u8_kernel<<<blocks_for(p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16), 256), 256, 0, s>>>(p.src, p.S, p.dst, p.D,
                                                                                             p.k, p.s);
   } else {
