@@ -754,10 +754,11 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   const int nb2 = p.n_rows >> 1;                 // B rows held by this CTA
   const int bh = nb2 * 128;                      // bytes of one K block of the B half
   const int S = p.pair;                          // A stages (host-chosen)
+  const bool stream = p.pair_stream != 0;        // B half streamed per stage (else resident)
   constexpr int a_stage = kBM * 128;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)S * a_stage;
-  uint64_t* full = (uint64_t*)(sB + (size_t)p.num_kb * bh);
+  uint64_t* full = (uint64_t*)(sB + (size_t)(stream ? S : p.num_kb) * bh);
   uint64_t* empty = full + kMaxStages;
   uint64_t* acc_full = empty + kMaxStages;
   uint64_t* acc_empty = acc_full + 2;
@@ -776,19 +777,27 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   const int rank = (int)cluster_ctarank();
   const int64_t m_tiles = (p.m_total + kBM - 1) / kBM;
   const int64_t m_pairs = (m_tiles + 1) / 2;
-  // pairs are split evenly over the groups; each pair streams only its group's tiles
+  const int ntk = p.n_tiles * p.ksplit;
   const int64_t pid = blockIdx.x / 2, npairs = gridDim.x / 2;
-  const int64_t ppg = npairs / p.groups;
-  const int64_t g = pid / ppg;
-  const bool idle = g >= p.groups;
-  const int64_t cid = idle ? 0 : g * m_pairs + (pid - g * ppg);
-  const int64_t ncl = ppg;
-  const int64_t total = idle ? 0 : (g + 1) * m_pairs;
+  int64_t g = 0, cid, ncl, total;
+  bool idle = false;
+  if (stream) {  // all pairs walk all (m-pair, n-tile, k-split, group) tiles
+    cid = pid;
+    ncl = npairs;
+    total = m_pairs * ntk * p.groups;
+  } else {  // resident B: pairs split evenly over the groups, each serves one group
+    const int64_t ppg = npairs / p.groups;
+    g = pid / ppg;
+    idle = g >= p.groups;
+    cid = idle ? 0 : g * m_pairs + (pid - g * ppg);
+    ncl = ppg;
+    total = idle ? 0 : (g + 1) * m_pairs;
+  }
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], (rank == 0 && !(p.dbg & 32)) ? 129u : 128u);  // dbg 32: timing probe, no coupling
+      mbar_init(&full[i], 128u + (stream ? 1u : 0u) + (rank == 0 ? 1u : 0u));
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -813,10 +822,14 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
     // ---------------------------------------------------------------- producers
     const int t = threadIdx.x;
     const int jc = lane & 7, rr = lane >> 3;
-    uint32_t it = 0, par = 0;
+    uint32_t par = 0, st_ph = 0;
+    int st_s = 0;
     for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
-      const TileCoord c = tile_of(ct, m_pairs, 1);
+      const TileCoord c = tile_of(ct, m_pairs, ntk);
       const int64_t mt = c.mt * 2 + rank;
+      const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
+      const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+      const uint8_t* bsrc = p.b + ((int64_t)(c.g * p.n_tiles + ntile) * p.num_kb) * (p.n_rows * 128) + (int64_t)rank * bh;
       {
         const int64_t row = mt * kBM + t;
         int64_t off = -1;
@@ -838,10 +851,18 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
         base[i] = p.a + (off < 0 ? 0 : off);
         valid |= (off >= 0 ? 1u : 0u) << i;
       }
-      for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-        const int s = (int)(it % S);
-        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-        const int32_t off = chunk_tab[kb * 8 + jc];
+      for (int kb = kb0; kb < kb1; ++kb) {
+        const int s = st_s;
+        mbar_wait(&empty[s], st_ph ^ 1);
+        if (++st_s == S) {
+          st_s = 0;
+          st_ph ^= 1;
+        }
+        if (stream && t == 0) {
+          mbar_arrive_expect_tx(&full[s], (uint32_t)bh);
+          bulk_g2s(sB + (size_t)s * bh, bsrc + (int64_t)kb * p.n_rows * 128, (uint32_t)bh, &full[s]);
+        }
+        const int32_t off = chunks_in_smem ? chunk_s[kb * 8 + jc] : __ldg(p.chunk_off + kb * 8 + jc);
         uint8_t* dst = sA + (size_t)s * a_stage;
         if (p.dbg & 16) {
 #pragma unroll
@@ -861,50 +882,67 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
     }
   } else if (warp == 4) {
     // resident B half: rows [rank * nb2, rank * nb2 + nb2) of every K block of the group
-    if (!idle && elect_one()) {
+    if (!stream && !idle && elect_one()) {
       mbar_arrive_expect_tx(bfull, (uint32_t)(p.num_kb * bh));
       const uint8_t* bg = p.b + (int64_t)g * p.num_kb * (p.n_rows * 128);
       for (int kb = 0; kb < p.num_kb; ++kb)
         bulk_g2s(sB + (size_t)kb * bh, bg + (int64_t)kb * p.n_rows * 128 + (int64_t)rank * bh, (uint32_t)bh, bfull);
     }
     __syncwarp();
-    if (!idle) mbar_wait(bfull, 0);
+    if (!stream && !idle) mbar_wait(bfull, 0);
     if (rank == 1) {
       // ------------------------------------------------------- forwarder (rank 1)
-      if (!idle && elect_one()) mbar_arrive_cluster(bpeer, 0);
+      if (!stream && !idle && elect_one()) mbar_arrive_cluster(bpeer, 0);
       __syncwarp();
-      uint32_t it = 0;
-      for (int64_t ct = cid; ct < total; ct += ncl)
-        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-          const int s = (int)(it % S);
-          mbar_wait(&full[s], (it / S) & 1);
-          if (elect_one() && !(p.dbg & 32)) {
+      int st_s = 0;
+      uint32_t st_ph = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        const TileCoord c = tile_of(ct, m_pairs, ntk);
+        const int ks = c.nt % p.ksplit;
+        const int nkb = min(p.num_kb, (ks + 1) * p.kb_per_split) - ks * p.kb_per_split;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int s = st_s;
+          mbar_wait(&full[s], st_ph);
+          if (++st_s == S) {
+            st_s = 0;
+            st_ph ^= 1;
+          }
+          if (elect_one()) {
             fence_proxy_async_smem();
             mbar_arrive_cluster(&full[s], 0);
           }
           __syncwarp();
         }
+      }
     } else {
       // ------------------------------------------------------- MMA issuer (rank 0)
-      if (!idle) mbar_wait_cluster(bpeer, 0);
+      if (!stream && !idle) mbar_wait_cluster(bpeer, 0);
       uint32_t idesc = make_idesc<KIND>(p.n_rows);
       idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24);  // M = 256 (pair)
       const bool mma_on = !(p.dbg & 2);
-      uint32_t it = 0, j = 0;
+      uint32_t j = 0, st_ph = 0;
+      int st_s = 0;
       for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
         const uint32_t buf = j & 1;
         mbar_wait_cluster(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
-        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-          const int s = (int)(it % S);
-          mbar_wait_cluster(&full[s], (it / S) & 1);
+        const TileCoord c = tile_of(ct, m_pairs, ntk);
+        const int ks = c.nt % p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int s = st_s;
+          mbar_wait_cluster(&full[s], st_ph);
+          if (++st_s == S) {
+            st_s = 0;
+            st_ph ^= 1;
+          }
           tc_fence_after();
           const uint64_t ad = smem_desc_sw(sA + (size_t)s * a_stage, 128);
-          const uint64_t bd = smem_desc_sw(sB + (size_t)kb * bh, 128);
+          const uint64_t bd = smem_desc_sw(sB + (size_t)(stream ? s : kb) * bh, 128);
           if (elect_one()) {
             if (mma_on)
-              for (int k = 0; k < 4; ++k) umma2_i8(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k) umma2_i8(dt, ad + 2 * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
             tc_commit2_multicast(&empty[s], 3);
           }
           __syncwarp();
@@ -931,6 +969,10 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
 static size_t igemm_pair_smem_bytes(int n_rows, int num_kb, int stages) {
   return 1024 + (size_t)stages * kBM * 128 + (size_t)num_kb * (n_rows / 2) * 128 + (2 * kMaxStages + 6) * 8 + 16 +
          2 * 128 * 8 + kMaxChunkSmem * 4;
+}
+static size_t igemm_pair_stream_smem_bytes(int n_rows, int stages) {
+  return 1024 + (size_t)stages * (kBM + n_rows / 2) * 128 + (2 * kMaxStages + 6) * 8 + 16 + 2 * 128 * 8 +
+         kMaxChunkSmem * 4;
 }
 
 
@@ -1887,16 +1929,32 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     const int64_t npairs = (num_sms() / 2 / std::max<int64_t>(groups, 1)) * groups;
     const size_t fixed = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0);
     const size_t cap = 227 * 1024;
-    const int stages = fixed < cap ? (int)std::min<size_t>(kMaxStages, (cap - fixed) / (kBM * 128)) : 0;
-    if (!no_pair && !a.a_tma && a.ksplit == 1 && a.n_tiles == 1 && a.kbytes == 128 && a.n_rows % 16 == 0 &&
-        a.n_rows <= 256 && 2 * a.tmem_cols <= 512 && m_tiles >= 2 && npairs >= groups && stages >= 4 &&
-        a.epi_mode != EPIM_RAW32) {
-      a.pair = stages;
+    int stages = fixed < cap ? (int)std::min<size_t>(kMaxStages, (cap - fixed) / (kBM * 128)) : 0;
+    static const int env_st = [] {
+      const char* e = std::getenv("QNB_PAIR_STAGES");
+      return e ? atoi(e) : 0;
+    }();
+    if (env_st >= 2 && env_st < stages) stages = env_st;
+    const bool shape_ok = !no_pair && !a.a_tma && a.kbytes == 128 && a.n_rows % 16 == 0 && a.n_rows <= 256 &&
+                          2 * a.tmem_cols <= 512 && m_tiles >= 2;
+    const bool resident = shape_ok && a.ksplit == 1 && a.n_tiles == 1 && npairs >= groups && stages >= 4 &&
+                          a.epi_mode != EPIM_RAW32;
+    static const bool no_stream = std::getenv("QNB_NO_PAIR_STREAM") != nullptr;
+    int sstages = (int)std::min<size_t>(kMaxStages, (cap - igemm_pair_stream_smem_bytes(a.n_rows, 0)) /
+                                                        ((size_t)(kBM + a.n_rows / 2) * 128));
+    if (sstages > 6) sstages = 6;
+    const bool streamed = shape_ok && !resident && !no_stream && sstages >= 4;
+    if (resident || streamed) {
+      a.pair = resident ? stages : sstages;
+      a.pair_stream = resident ? 0 : 1;
       a.cluster = 2;
-      const size_t smem = igemm_pair_smem_bytes(a.n_rows, a.num_kb, stages);
+      const size_t smem = resident ? igemm_pair_smem_bytes(a.n_rows, a.num_kb, stages)
+                                   : igemm_pair_stream_smem_bytes(a.n_rows, sstages);
+      const int64_t ptiles = ceil_div(m_tiles, 2) * a.n_tiles * a.ksplit * groups;
+      const int64_t np = resident ? npairs : std::min<int64_t>(num_sms() / 2, ptiles);
       QNB_CUDA(cudaFuncSetAttribute(igemm_pair_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(2 * npairs));
+      cfg.gridDim = dim3((unsigned)(2 * np));
       cfg.blockDim = dim3(kThreads);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
