@@ -144,7 +144,8 @@ __device__ __forceinline__ uint64_t mulwide_u32(uint32_t a, uint32_t b) {
   return r;
 }
 // RN32: n >= 32 (the product's high word alone holds the quotient)
-template <bool RN32>
+// FREE: the host proved zout + t within [omin, omax] for every d (no clamp).
+template <bool RN32, bool FREE = false>
 __device__ __forceinline__ uint32_t relu_tail(int32_t q, const ReluFastK& r) {
   const uint32_t d = (uint32_t)max(min(q + r.zdiff, r.dmax), r.dmin);
   const uint64_t P = mulwide_u32(d, r.mult);
@@ -152,10 +153,11 @@ __device__ __forceinline__ uint32_t relu_tail(int32_t q, const ReluFastK& r) {
   if constexpr (RN32) t = (uint32_t)(P >> 32) >> (r.n - 32);
   else t = __funnelshift_r((uint32_t)P, (uint32_t)(P >> 32), (uint32_t)r.n);
   t &= r.mask;
+  if constexpr (FREE) return t + (uint32_t)r.zout;
   return (uint32_t)min(max((int32_t)t + r.zout, r.omin), r.omax);
 }
 
-// F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32.
+// F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32; bit 2: clamp-free ReLU tail.
 template <bool RELU, int F>
 __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk) {
   int32_t q;  // RNE quotient (before the output zero point)
@@ -172,7 +174,7 @@ __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, cons
     qq = qq < -lim ? -lim : (qq > lim ? lim : qq);
     q = (int32_t)max(min(qq, (int64_t)INT32_MAX / 2), (int64_t)INT32_MIN / 2);
   }
-  if constexpr (RELU) return relu_tail<(F & 2) != 0>(q, rk);
+  if constexpr (RELU) return relu_tail<(F & 2) != 0, (F & 4) != 0>(q, rk);
   return (uint32_t)min(max(q + k.oz, k.omin), k.omax);
 }
 
@@ -364,7 +366,8 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       tmem_ld_wait();
       rowsum = (int64_t)(int32_t)v;
     }
-    const int32_t rowterm32 = (int32_t)(-zw * rowsum);
+    int32_t rowterm32 = (int32_t)(-zw * rowsum);
+    asm volatile("" : "+r"(rowterm32));  // keep it in a register (one IADD3 per output, no re-multiply)
     const int n0 = c.nt * npt;
     const int n_here = min(npt, n_real - n0);
     const int ch0 = c.g * n_real + n0;
@@ -500,11 +503,15 @@ __device__ __forceinline__ void run_epilogue(const IgemmArgs& p, uint32_t tmem, 
   const int f = (p.rq.s >= 32 ? 1 : 0) | (p.relu.shift_bits + p.relu.shift >= 32 ? 2 : 0);
   switch (p.epi_mode) {
     case EPIM_Q8_FAST_RELU:
-      switch (f) {
+      switch (f | (p.relu_free ? 4 : 0)) {
         case 0: QNB_EPI(EPIM_Q8_FAST_RELU, 0); break;
         case 1: QNB_EPI(EPIM_Q8_FAST_RELU, 1); break;
         case 2: QNB_EPI(EPIM_Q8_FAST_RELU, 2); break;
-        default: QNB_EPI(EPIM_Q8_FAST_RELU, 3);
+        case 3: QNB_EPI(EPIM_Q8_FAST_RELU, 3); break;
+        case 4: QNB_EPI(EPIM_Q8_FAST_RELU, 4); break;
+        case 5: QNB_EPI(EPIM_Q8_FAST_RELU, 5); break;
+        case 6: QNB_EPI(EPIM_Q8_FAST_RELU, 6); break;
+        default: QNB_EPI(EPIM_Q8_FAST_RELU, 7);
       }
       break;
     case EPIM_Q8_FAST:
@@ -1840,6 +1847,21 @@ static bool relu_fast_ok(const ReluRequant& r) {
   return t2 + az < (int64_t(1) << 31) && r.out_min >= INT32_MIN && r.out_max <= INT32_MAX;
 }
 
+// The truncating ReLU tail needs no final clamp when zout + t stays inside
+// [omin, omax] for the whole d range (t is monotone in d; the mask only lowers it).
+static bool relu_clamp_free(const ReluRequant& r, const Requant& rq) {
+  const int n = r.shift_bits + r.shift;
+  if (n < 0 || n > 63) return false;
+  const int64_t zin = r.in_zero;
+  const int64_t dmax = rq.out_max - zin, dmin = std::max<int64_t>(rq.out_min - zin, 0);
+  if (dmax < dmin || dmin < 0 || dmax > 0xFFFFFFFFLL) return false;
+  const int ls = r.shift < 0 ? -r.shift : 0;
+  const uint64_t mask = ~((uint64_t(1) << ls) - 1);
+  const int64_t tmin = (int64_t)((uint64_t)(((unsigned __int128)dmin * (uint64_t)r.mult) >> n) & mask);
+  const int64_t tmax = (int64_t)(((unsigned __int128)dmax * (uint64_t)r.mult) >> n);
+  return r.out_zero + tmin >= r.out_min && r.out_zero + tmax <= r.out_max;
+}
+
 template <int KIND>
 static qnb_status launch_hk(const IgemmArgs& a, cudaStream_t s) {
   static bool attr_set = false;
@@ -1914,6 +1936,8 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     const bool fast = a.fast_rq && a.chan_const32 != nullptr;
     a.epi_mode = fast ? (a.has_relu ? (relu_fast_ok(a.relu) ? EPIM_Q8_FAST_RELU : EPIM_Q8_EXACT) : EPIM_Q8_FAST)
                       : EPIM_Q8_EXACT;
+    static const bool no_free = std::getenv("QNB_NO_RELU_FREE") != nullptr;
+    a.relu_free = (a.epi_mode == EPIM_Q8_FAST_RELU && !no_free && relu_clamp_free(a.relu, a.rq)) ? 1 : 0;
   } else {
     a.epi_mode = a.epi == EPI_F16 ? EPIM_F16 : EPIM_F32;
   }

@@ -122,7 +122,8 @@ struct IgemmArgs {
   // CTA-pair mode (igemm_pair_kernel): cta_group::2 MMAs with M = 256 and each CTA's
   // half of B resident in smem for the whole launch.
   int32_t pair;
-  int32_t pair_stream;  // pair mode with B streamed per stage (each CTA its half) instead of resident
+  int32_t pair_stream;
+  int32_t relu_free;  // fused ReLU tail provably needs no mask / clamp (host-checked)  // pair mode with B streamed per stage (each CTA its half) instead of resident
   // epilogue
   int32_t epi;
   const int64_t* chan_const;  // [G * n_real] (quantized)
