@@ -935,6 +935,7 @@ Step with_batch(const Step& s0, int64_t b, const void* in, void* out) {
     s.up_dst = (uint8_t*)out;
   }
   s.ig.m_total = b * s.rows_per_img;
+  if (s.ig.hk) s.ig.hk_pairs = (int32_t)((b + 1) / 2);  // row-Hankel tiles cover only this batch's image pairs
   s.pack.N = b;
   s.pack.L.n = b;
   s.fx.S.n = s.fx.D.n = b;
@@ -1066,15 +1067,42 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
   return QNB_OK;
 }
 
-// Host-buffer forwards are pipelined: the batch is cut into chunks (>= 32 images,
-// at most 8), chunk i's H2D copy runs on the plan's copy stream while chunk i-1 runs
-// through the network on the compute stream, and each chunk's result is copied back
-// as soon as it is done.  Sub-batches reuse the activation arena in order (the
-// compute stream serialises them), so no extra device memory is needed.
-static int64_t pipeline_chunks(int64_t batch) {
-  if (batch < 64) return 1;
-  return std::min<int64_t>(8, batch / 32);
+// Host-buffer forwards are pipelined: the batch is cut into at most 8 chunks, chunk
+// i's H2D copy runs on the plan's copy stream while chunk i-1 runs through the network
+// on the compute stream, and each chunk's result is copied back as soon as it is done.
+// Chunks are equal, >= 32 images (QNB_E2E_CHUNKS=n forces n equal chunks; -1 selects a
+// tapered 64, 64, 48, 32, 24, 16, 8 split, which measured slower).  Sub-batches reuse
+// the activation arena in order (the compute stream serialises them), so no extra
+// device memory is needed.
+static std::vector<int64_t> pipeline_split(int64_t batch) {
+  static const int mode = [] {
+    const char* e = std::getenv("QNB_E2E_CHUNKS");
+    return e ? atoi(e) : 0;
+  }();
+  std::vector<int64_t> v;
+  if (batch < 64) {
+    v.push_back(batch);
+    return v;
+  }
+  if (mode >= 0) {  // equal chunks
+    const int64_t n = mode > 0 ? std::min<int64_t>(std::min<int64_t>(8, mode), batch / 8)
+                               : std::min<int64_t>(8, batch / 32);
+    const int64_t per = (batch + n - 1) / n;
+    for (int64_t b0 = 0; b0 < batch; b0 += per) v.push_back(std::min(per, batch - b0));
+    return v;
+  }
+  static const int w[7] = {8, 8, 6, 4, 3, 2, 1};  // 32ths of the batch
+  int64_t done = 0;
+  for (int i = 0; i < 7 && done < batch; ++i) {
+    int64_t c = i == 6 ? batch - done : std::max<int64_t>(1, (batch * w[i] + 16) / 32);
+    c = std::min(c, batch - done);
+    v.push_back(c);
+    done += c;
+  }
+  if (done < batch) v.back() += batch - done;
+  return v;
 }
+static int64_t pipeline_chunks(int64_t batch) { return (int64_t)pipeline_split(batch).size(); }
 
 static qnb_status forward_body(qnb_plan& P, int64_t batch, const void* input, bool in_host, void* output,
                                bool out_host, bool pinned_in, cudaStream_t s) {
@@ -1085,24 +1113,25 @@ static qnb_status forward_body(qnb_plan& P, int64_t batch, const void* input, bo
       QNB_CUDA(cudaMemcpyAsync(output, out_dev, (size_t)(P.out_bytes_per_sample * batch), cudaMemcpyDeviceToHost, s));
     return QNB_OK;
   }
-  const int64_t nch = pipeline_chunks(batch), per = ceil_div(batch, nch);
+  const std::vector<int64_t> split = pipeline_split(batch);
   const size_t ib = (size_t)P.in_bytes_per_sample, ob = (size_t)P.out_bytes_per_sample;
   uint8_t* stage = (uint8_t*)P.in_staging;
   if (pinned_in) {
     // all copies queued on the copy stream up front; each chunk's compute waits for its copy
     QNB_CUDA(cudaEventRecord(P.ev_fork, s));
     QNB_CUDA(cudaStreamWaitEvent(P.copy_stream, P.ev_fork, 0));
-    for (int64_t i = 0, b0 = 0; b0 < batch; ++i, b0 += per) {
-      const int64_t b = std::min(per, batch - b0);
-      QNB_CUDA(cudaMemcpyAsync(stage + b0 * ib, (const uint8_t*)input + b0 * ib, b * ib, cudaMemcpyHostToDevice,
-                               P.copy_stream));
-      QNB_CUDA(cudaEventRecord(P.ev_copy[(size_t)i], P.copy_stream));
+    int64_t b0 = 0;
+    for (size_t i = 0; i < split.size(); b0 += split[i], ++i) {
+      QNB_CUDA(cudaMemcpyAsync(stage + b0 * ib, (const uint8_t*)input + b0 * ib, split[i] * ib,
+                               cudaMemcpyHostToDevice, P.copy_stream));
+      QNB_CUDA(cudaEventRecord(P.ev_copy[i], P.copy_stream));
     }
   }
-  for (int64_t i = 0, b0 = 0; b0 < batch; ++i, b0 += per) {
-    const int64_t b = std::min(per, batch - b0);
+  int64_t b0 = 0;
+  for (size_t i = 0; i < split.size(); b0 += split[i], ++i) {
+    const int64_t b = split[i];
     if (pinned_in) {
-      QNB_CUDA(cudaStreamWaitEvent(s, P.ev_copy[(size_t)i], 0));
+      QNB_CUDA(cudaStreamWaitEvent(s, P.ev_copy[i], 0));
     } else {
       // pageable source: the copy call itself blocks the host, so issue it right before
       // its chunk; the device keeps computing the previous chunk meanwhile
