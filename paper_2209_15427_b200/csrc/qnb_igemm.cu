@@ -398,6 +398,38 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
           *reinterpret_cast<uint4*>(obase + (int64_t)(ch0 + cb)) = make_uint4(w[0], w[1], w[2], w[3]);
         };
         int cb = half * 16;
+        if (cb + cstep < n_here && cb + 2 * cstep >= n_here) {
+          // exactly two blocks for this warp (row-Hankel conv1: 96 channels, 3 warps per
+          // lane quarter): both TMEM loads in flight, one wait, and the two blocks'
+          // requant chains interleaved for ILP
+          const int cb1 = cb + cstep;
+          issue(cb, r0, c0);
+          issue(cb1, r1, c1);
+          tmem_ld_wait(r0);
+          tmem_ld_wait(r1);
+          if (ok) {
+            uint32_t w0[4], w1[4];
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) {
+              const uint32_t a0 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 0] + c0[qd].x + rowterm32, k, lut_s);
+              const uint32_t b0 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 0] + c1[qd].x + rowterm32, k, lut_s);
+              const uint32_t a1 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 1] + c0[qd].y + rowterm32, k, lut_s);
+              const uint32_t b1 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 1] + c1[qd].y + rowterm32, k, lut_s);
+              const uint32_t a2 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 2] + c0[qd].z + rowterm32, k, lut_s);
+              const uint32_t b2 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 2] + c1[qd].z + rowterm32, k, lut_s);
+              const uint32_t a3 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 3] + c0[qd].w + rowterm32, k, lut_s);
+              const uint32_t b3 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 3] + c1[qd].w + rowterm32, k, lut_s);
+              w0[qd] = a0 | (a1 << 8) | (a2 << 16) | (a3 << 24);
+              w1[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+            }
+            *reinterpret_cast<uint4*>(obase + (int64_t)(ch0 + cb)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+            *reinterpret_cast<uint4*>(obase + (int64_t)(ch0 + cb1)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) epi_release(p, &acc_empty[buf]);
+          continue;
+        }
         if (cb < n_here) issue(cb, r0, c0);
         for (; cb < n_here; cb += 2 * cstep) {
           const int cb1 = cb + cstep;
