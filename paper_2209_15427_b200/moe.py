@@ -263,9 +263,12 @@ class MoeNet:
         self._pipes[B] = p
         return p
 
-    def forward_device(self, x_ptr: int, out_ptr: int, B: int) -> dict:
-        """One MoE forward on device buffers (stream: torch's current stream).  Returns
-        routing statistics (per-expert counts) for load-balance reporting."""
+    def forward_device(self, x_ptr: int, out_ptr: int, B: int, in_host: bool = False,
+                       out_host: bool = False) -> dict:
+        """One MoE forward (stream: torch's current stream) on device buffers, or on pinned
+        host buffers: the trunk plan then pipelines the input's H2D copy chunk by chunk
+        under its own compute, and the tail plan copies the result back.  Returns routing
+        statistics (per-expert counts) for load-balance reporting."""
         import torch
         p = self._pipe(B)
         b = p["bufs"]
@@ -273,7 +276,7 @@ class MoeNet:
         s = torch.cuda.current_stream().cuda_stream
         sp = C.c_void_p(s)
         n = B * p["row_elems"]
-        p["trunk"].forward_device(x_ptr, b["T"].data_ptr(), B, s)
+        p["trunk"].forward_device(x_ptr, b["T"].data_ptr(), B, s, in_host=in_host)
         if p["qv_in"] is not None:
             check(lib.qnb_dequantize(b["T"].data_ptr(), n, p["in_dtype"], C.byref(p["qv_in"]), b["F"].data_ptr(),
                                      sp))
@@ -345,7 +348,7 @@ class MoeNet:
         qv = C.byref(p["qv_top"]) if p["qv_top"] is not None else None
         check(lib.qnb_moe_combine_rows(y.data_ptr(), p["per"], b["pair_slot"].data_ptr(), b["w"].data_ptr(), B,
                                        self.top_k, p["top_dtype"], qv, b["M"].data_ptr(), sp))
-        p["tail"].forward_device(b["M"].data_ptr(), out_ptr, B, s)
+        p["tail"].forward_device(b["M"].data_ptr(), out_ptr, B, s, out_host=out_host)
         self.last_stats = {"counts": counts}
         return self.last_stats
 

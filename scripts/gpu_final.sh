@@ -7,7 +7,7 @@ echo "tests rc=$?" >> gpurun_out/${TAG}_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.log
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
-timeout 900 python bench.py --model alexnet_moe --steps 10 --warmup 3 > gpurun_out/${TAG}_moe.json 2> gpurun_out/${TAG}_moe.err
+timeout 900 python bench.py --model alexnet_moe --steps 30 --warmup 5 > gpurun_out/${TAG}_moe.json 2> gpurun_out/${TAG}_moe.err
 timeout 900 python bench.py --model vgg16 --batch 128 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_vgg.json 2> gpurun_out/${TAG}_vgg.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --profile-reps 1 > /dev/null 2> gpurun_out/${TAG}_ncu.err

@@ -76,3 +76,26 @@ def test_alexnet_moe_int8_matches_reference(reference, setup):
     m_ours = p["bufs"]["M"].cpu().numpy()[: m_ref.size].reshape(m_ref.shape)
     assert np.array_equal(m_ours, m_ref), int((m_ours != m_ref).sum())
     torch.cuda.synchronize()
+
+
+def test_alexnet_moe_host_buffers_match_device_path(setup):
+    """forward_device with pinned host input / output (the trunk plan pipelines the H2D
+    copy chunk by chunk, the tail plan copies the result back) gives the device-buffer
+    result bit for bit, at a batch large enough to be split into several chunks."""
+    import torch
+    g, params, ranges = setup
+    batch = 96
+    x = graphs.synth_images(batch, (3, 227, 227), offset=300)
+    ours = our_net(g, params, ranges)
+    xd = torch.from_numpy(x).cuda()
+    od = torch.empty((batch, 1000), dtype=torch.float32, device="cuda")
+    ours.forward_device(xd.data_ptr(), od.data_ptr(), batch)
+    torch.cuda.synchronize()
+    want = od.cpu().numpy()
+    xp = torch.from_numpy(x).pin_memory()
+    op = torch.empty((batch, 1000), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        op.zero_()
+        ours.forward_device(xp.data_ptr(), op.data_ptr(), batch, in_host=True, out_host=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(op.numpy(), want)
