@@ -203,7 +203,8 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   // is used where a tap's channels fill whole 128-byte stages (measured faster there).
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
   const bool patch = !hk && use_patch && igemm_patch_eligible(g, io.in);
-  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, io.in) && (g.cg * io.in.es()) % 128 == 0;
+  static const int tma_align = std::getenv("QNB_TMA64") ? 64 : 128;
+  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, io.in) && (g.cg * io.in.es()) % tma_align == 0;
   int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, io.in, &pk, &hk_kpr));

@@ -560,7 +560,8 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   // is used where a tap's channels fill whole 128-byte stages (measured faster there).
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
   const bool patch = !hk && use_patch && igemm_patch_eligible(g, Lin);
-  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % 128 == 0;
+  static const int tma_align = std::getenv("QNB_TMA64") ? 64 : 128;  // A/B: 64-byte (SW64) im2col stages
+  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % tma_align == 0;
   int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, Lin, &pk, &hk_kpr));
