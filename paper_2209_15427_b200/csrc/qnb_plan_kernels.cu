@@ -757,8 +757,53 @@ __global__ void softmax_rows_kernel(const uint8_t* __restrict__ src, DevLayout S
   }
   __syncthreads();
   const double md = smax;
-  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) ex[f] = exp(__dsub_rn((double)xv[f], md));
+  // Certified parallel sum: every summation order of F positive terms is within
+  // (F-1) u of the exact sum, so the reference's sequential sum and this tree sum differ
+  // by < 2F u relative.  An output keeps the tree-sum quotient unless that quotient lies
+  // within (2F + 8) u of a float rounding midpoint; then (rare: ~F * 1e-8 of the rows)
+  // thread 0 redoes the reference's sequential sum for the row.
+  double part = 0.0;
+  for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
+    const double e = exp(__dsub_rn((double)xv[f], md));
+    ex[f] = e;
+    part = __dadd_rn(part, e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+  __shared__ double wsum[32];
+  __shared__ int unsafe;
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = part;
+  if (threadIdx.x == 0) unsafe = 0;
   __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = __dadd_rn(t, wsum[w]);
+    ssum = t;
+    if (!(t >= 1.0 && t < 1e300)) unsafe = 1;  // NaN / inf inputs: exact path
+  }
+  __syncthreads();
+  const double tol = (double)(2 * F + 8) * 1.1102230246251565e-16;
+  {
+    const double tsum = ssum;
+    bool bad = false;
+    for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
+      const double y = __ddiv_rn(ex[f], tsum);
+      const float r = __double2float_rn(y);
+      if (y != 0.0) {
+        const double up = (double)nextafterf(r, INFINITY), dn = (double)nextafterf(r, 0.0f);
+        const double mhi = 0.5 * ((double)r + up), mlo = 0.5 * ((double)r + dn);
+        const double dist = fmin(fabs(y - mlo), fabs(mhi - y));
+        bad |= !(dist > tol * fabs(y));
+      }
+      xv[f] = r;
+    }
+    if (bad) unsafe = 1;
+  }
+  __syncthreads();
+  if (!unsafe) {
+    for (int64_t f = threadIdx.x; f < F; f += blockDim.x) out[n * F + f] = xv[f];
+    return;
+  }
   if (threadIdx.x == 0) {  // the reference's sequential double sum, loads batched for ILP
     double s = 0.0;
     int64_t f = 0;
