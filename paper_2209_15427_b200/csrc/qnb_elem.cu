@@ -555,8 +555,11 @@ qnb_status qnb_softmax(const float* in, int64_t rows, int64_t cols, float* out, 
   if (rows <= 0 || cols <= 0) return QNB_OK;
   const size_t sm = (size_t)cols * sizeof(double);
   if (sm > 200 * 1024) return fail(QNB_E_UNSUPPORTED, "softmax row too long");
-  if (sm > 48 * 1024)
-    QNB_CUDA(cudaFuncSetAttribute(softmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  static bool attr = false;  // per-function attribute: set once to the maximum
+  if (sm > 48 * 1024 && !attr) {
+    QNB_CUDA(cudaFuncSetAttribute(softmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
   softmax_kernel<<<(unsigned)rows, 256, sm, as_stream(s)>>>(in, cols, out);
   count_launch();
   QNB_CUDA(cudaGetLastError());

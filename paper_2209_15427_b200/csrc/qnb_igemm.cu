@@ -2008,7 +2008,14 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
                                    : igemm_pair_stream_smem_bytes(a.n_rows, sstages);
       const int64_t ptiles = ceil_div(m_tiles, 2) * a.n_tiles * a.ksplit * groups;
       const int64_t np = resident ? npairs : std::min<int64_t>(num_sms() / 2, ptiles);
-      QNB_CUDA(cudaFuncSetAttribute(igemm_pair_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // the attribute is per function, not per launch: set it once to the maximum so that a
+      // smaller later launch never lowers it under an already captured / replayed larger one
+      static bool pair_attr = false;
+      if (!pair_attr) {
+        QNB_CUDA(cudaFuncSetAttribute(igemm_pair_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)cap));
+        pair_attr = true;
+      }
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)(2 * np));
       cfg.blockDim = dim3(kThreads);
