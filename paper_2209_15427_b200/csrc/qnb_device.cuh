@@ -202,6 +202,15 @@ __device__ __forceinline__ void umma2_i8(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// ------------------------------------------------- programmatic dependent launch
+// Persistent kernels trigger at their start (every CTA is resident by then, so a
+// dependent grid can never hold SMs a not-yet-resident CTA of this grid needs) and wait
+// for the preceding grid only after their prologue (barriers, TMEM, resident weights).
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // One lane of a converged warp (elect.sync): lets a whole warp run the MMA-issue loop
 // in uniform registers while exactly one thread issues each tcgen05 instruction.
 __device__ __forceinline__ bool elect_one() {

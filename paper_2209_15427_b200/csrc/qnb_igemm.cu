@@ -570,6 +570,7 @@ __device__ __forceinline__ void run_epilogue(const IgemmArgs& p, uint32_t tmem, 
 //              warps per TMEM lane quarter split the 16-column blocks.
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constant__ IgemmArgs p) {
+  griddep_launch_dependents();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int kbytes = p.kbytes;
@@ -624,6 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   if (cs > 1) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // the previous grid's output (our A operand) is complete from here on
 
   if (warp < 4 && p.a_tma) {
     // ------------------------------------------------------- TMA im2col producer
@@ -788,6 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
 //   bfull        each CTA's resident B half (expect_tx); bpeer on rank 0: rank 1's B
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_constant__ IgemmArgs p) {
+  griddep_launch_dependents();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int nb2 = p.n_rows >> 1;                 // B rows held by this CTA
@@ -857,6 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp != 4) griddep_wait();  // warp 4 first issues the resident weights (independent of it)
   if (warp < 4) {
     // ---------------------------------------------------------------- producers
     const int t = threadIdx.x;
@@ -928,6 +932,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
         bulk_g2s(sB + (size_t)kb * bh, bg + (int64_t)kb * p.n_rows * 128 + (int64_t)rank * bh, (uint32_t)bh, bfull);
     }
     __syncwarp();
+    griddep_wait();
     if (!stream && !idle) mbar_wait(bfull, 0);
     if (rank == 1) {
       // ------------------------------------------------------- forwarder (rank 1)
@@ -1031,6 +1036,7 @@ constexpr int kHkThreads = 14 * 32;  // warps 0-3, 5-12 epilogue (3 per TMEM lan
 constexpr int kHkEpiWarps = 12;
 template <int KIND>
 __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_constant__ IgemmArgs p) {
+  griddep_launch_dependents();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int b_stage = p.n_rows * 128;
@@ -1067,11 +1073,16 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp != 13) griddep_wait();  // warp 13 first issues the resident weights
   if (warp == 13) {
     if (lane == 0) {
       mbar_arrive_expect_tx(b_full, (uint32_t)b_bytes);
       for (int kb = 0; kb < p.num_kb; ++kb)
         bulk_g2s(sB + (size_t)kb * b_stage, p.b + (size_t)kb * b_stage, (uint32_t)b_stage, b_full);
+    }
+    __syncwarp();
+    griddep_wait();
+    if (lane == 0) {
       uint32_t j = 0;
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++j) {
         const uint32_t buf = j & 1;
@@ -1894,6 +1905,16 @@ static bool relu_clamp_free(const ReluRequant& r, const Requant& rq) {
   return r.out_zero + tmin >= r.out_min && r.out_zero + tmax <= r.out_max;
 }
 
+// Programmatic dependent launch for the persistent GEMM kernels (QNB_NO_PDL=1 disables).
+static bool pdl_on() {
+  static const bool on = std::getenv("QNB_NO_PDL") == nullptr;
+  return on;
+}
+static void set_pdl(cudaLaunchAttribute& at) {
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+}
+
 template <int KIND>
 static qnb_status launch_hk(const IgemmArgs& a, cudaStream_t s) {
   static bool attr_set = false;
@@ -1905,7 +1926,16 @@ static qnb_status launch_hk(const IgemmArgs& a, cudaStream_t s) {
   if (smem > 227 * 1024) return fail(QNB_E_UNSUPPORTED, "row-Hankel tile exceeds shared memory");
   const int64_t tiles = (int64_t)a.hk_pairs * a.oh;
   const int64_t grid = std::min<int64_t>(tiles, num_sms());
-  igemm_hk_kernel<KIND><<<(unsigned)grid, kHkThreads, smem, s>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kHkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  set_pdl(attr[0]);
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_hk_kernel<KIND>, a));
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;
@@ -2021,13 +2051,14 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
       cfg.blockDim = dim3(kThreads);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
-      cudaLaunchAttribute attr[1];
+      cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = 2;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
+      set_pdl(attr[1]);
       cfg.attrs = attr;
-      cfg.numAttrs = 1;
+      cfg.numAttrs = pdl_on() ? 2 : 1;
       QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_pair_kernel<KIND>, a));
       count_launch();
       QNB_CUDA(cudaGetLastError());
@@ -2044,13 +2075,14 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   if (a.kbytes != 128 && !a.a_tma) return fail(QNB_E_ARG, "cp.async producers need 128-byte stages");
   cfg.dynamicSmemBytes = igemm_smem_bytes(a.n_rows, a.kbytes);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)a.cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  set_pdl(attr[1]);
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
   QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_kernel<KIND>, a));
   count_launch();
   QNB_CUDA(cudaGetLastError());
