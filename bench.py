@@ -368,7 +368,8 @@ def run_qnb(a):
         li, kind, ops_, by = steps_info[dom]
         t = ms_steps[dom]
         if kind == "igemm":
-            roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": int8_peak, "unit": "TOPS",
+            roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": int8_peak, "unit": "TFLOP/s",
+                    "op_type": "int8 tensor ops (2 per u8 x u8 MAC), i.e. TOPS",
                     "kernel": f"igemm {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
         else:
             roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
