@@ -38,7 +38,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define QNB_ABI_VERSION 1
+#define QNB_ABI_VERSION 2  /* 2: qnb_layer_desc.inspect_top, qnb_plan_opts.flags, QCNM store */
 
 typedef void* qnb_stream; /* cudaStream_t (0 = legacy default stream) */
 

@@ -35,7 +35,7 @@ def test_library_exports_every_header_symbol():
 
 
 def test_abi_version():
-    assert _lib.lib().qnb_abi_version() == 1
+    assert _lib.lib().qnb_abi_version() == 2
 
 
 def test_host_math_matches_reference(oracle_impl):
