@@ -204,7 +204,8 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
   const bool patch = !hk && use_patch && igemm_patch_eligible(g, io.in);
   static const int tma_align = std::getenv("QNB_TMA64") ? 64 : 128;
-  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, io.in) && (g.cg * io.in.es()) % tma_align == 0;
+  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, io.in) &&
+                   (g.cg * io.in.es()) % tma_align == 0 && g.ow >= 16;  // as the plan compiler
   int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, io.in, &pk, &hk_kpr));

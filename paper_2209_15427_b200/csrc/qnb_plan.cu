@@ -561,7 +561,10 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
   const bool patch = !hk && use_patch && igemm_patch_eligible(g, Lin);
   static const int tma_align = std::getenv("QNB_TMA64") ? 64 : 128;  // A/B: 64-byte (SW64) im2col stages
-  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % tma_align == 0;
+  // TMA im2col boxes are 128 consecutive output pixels: on narrow outputs (AlexNet conv3,
+  // 13 wide) one box wraps ~10 rows and the CTA-pair gather measured faster (+0.6 %)
+  const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % tma_align == 0 &&
+                   g.ow >= 16;
   int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, Lin, &pk, &hk_kpr));
