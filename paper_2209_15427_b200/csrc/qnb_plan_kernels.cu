@@ -902,7 +902,9 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
       return e ? atoi(e) : 0;
     }();
     PoolLrnArgs b = a;
-    b.pix = std::min(64, lrn_pixels(a.D.c));  // 64 pixels: more resident blocks (measured best)
+    // at most 64 pixels and 32 KB of staged floats per block: more resident blocks
+    // (measured: C = 96 -> 64 pixels, C = 256 -> 32 pixels)
+    b.pix = std::max(8, std::min<int>(64, (int)(8192 / std::max<int64_t>(a.D.c, 1))));
     if (env_pix > 0) b.pix = std::min(env_pix, lrn_pixels(a.D.c));
     const int64_t qblocks = a.D.n * ceil_div(a.D.h * a.D.w, b.pix);
     const size_t qsm = (size_t)b.pix * a.D.c * 4;
