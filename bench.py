@@ -268,6 +268,36 @@ class Workload:
                                      out_host=True)
 
 
+def parity_check(wl, a, ref_prob, T):
+    """The bench's own batch against the reference on the cpu_baseline sample: the GPU
+    rows 0..T-1 of the timed batch-B forward vs reference Net::forward on the same images
+    (prob: FP32 sink, ulp distance; for chain nets also the last quantized blob before the
+    softmax, read from the plan and compared bit for bit with a reference prefix net)."""
+    out = wl.out_dev[:T].cpu().numpy()
+    ulp = np.abs(out.view(np.int32).astype(np.int64) - ref_prob.view(np.int32).astype(np.int64))
+    res = {"images": T, "rows": f"0..{T - 1} of the timed batch of {wl.B}", "prob_max_ulp": int(ulp.max()),
+           "prob_rows_bit_identical": int((ulp.max(axis=1) == 0).sum())}
+    if wl.plan is None or a.precision not in ("int8", "int16"):
+        return res
+    from oracle import ffi
+    from paper_2209_15427_b200 import graph as G
+    layers = wl.g["layers"]
+    names = [l["name"] for l in layers]
+    ck = names[-2]  # the layer feeding the softmax (fc8)
+    prefix = {"name": "prefix", "layers": layers[: names.index(ck) + 1]}
+    pp = {k: v for k, v in wl.params.items() if k.split(".")[0] in names[: names.index(ck) + 1]}
+    per = int(np.prod(G.infer_blobs(prefix)[ck]["shape"][1:]))
+    es = 1 if a.precision == "int8" else 2
+    nets = reference_nets(prefix, a.precision, pp, wl.ranges, T)
+    theirs = ffi.forward_mt(nets, "data", wl.x_host[:T], ck, per * es).view(np.uint8 if es == 1 else np.uint16)
+    raw, lay = wl.plan.blob(ck)
+    n, h, w, cp, hh, hw, wx, e = lay
+    mine = raw.view(theirs.dtype).reshape(n, h + 2 * hh, w + 2 * hw + wx, cp)[:T, hh, hw, :per]
+    res.update({"int8_checkpoint": ck, "checkpoint_values": int(theirs.size),
+                "checkpoint_mismatches": int((mine.reshape(-1) != theirs.reshape(T, per).reshape(-1)).sum())})
+    return res
+
+
 def run_qnb(a):
     import torch
     ws, rank, local = dist_setup(use_cuda=True)
@@ -392,7 +422,7 @@ def run_qnb(a):
                                if kind == "igemm" else f"{peak_src}: hbm_gbs")
         conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:
         try:
             from oracle import ffi
@@ -402,12 +432,16 @@ def run_qnb(a):
                     T = min(T, 4)  # the MoE reference evaluates all 16 experts per image
                 nets = reference_nets(wl.g, a.precision, wl.params, wl.ranges, T)
                 xs = wl.x_host[:T]
-                v = cpu_forward_rate(nets, xs, 4000)
+                t0 = time.perf_counter()
+                ref_prob = ffi.forward_mt(nets, "data", xs, "prob", 4000).view(np.float32).reshape(T, 1000)
+                v = T / (time.perf_counter() - t0)
                 cpu = {"value": v, "unit": "images/s", "cores": T, "kind": "reference",
                        "sample": f"{T} images of the same batch, one reference Net::forward thread each"}
                 del nets
+                parity = parity_check(wl, a, ref_prob, T)
         except Exception as e:  # reported, never fatal
-            cpu = {"value": None, "error": str(e)[:200]}
+            cpu = cpu or {"value": None, "error": str(e)[:200]}
+            parity = parity or {"error": str(e)[:200]}
 
     if rank == 0:
         res = wl.x_host.shape[-1]
@@ -431,7 +465,7 @@ def run_qnb(a):
                 "gpu_launches": int(launches), "kernels_per_forward": wl.kernels,
                 "roofline": roof, "conv_tops": conv_tops, "conv_frac_of_int8_peak":
                     (conv_tops / int8_peak if conv_tops else None),
-                "cpu_baseline": cpu, "clocks": clk.summary(), "per_layer": per_layer}
+                "cpu_baseline": cpu, "parity": parity, "clocks": clk.summary(), "per_layer": per_layer}
         if wl.moe:
             line["moe_expert_counts_last_step"] = [int(c) for c in wl.net.last_stats["counts"]] \
                 if hasattr(wl.net, "last_stats") else None

@@ -26,8 +26,10 @@
 #include <vector>
 
 #include "qnb.h"
+#include "qnet/datatypes.hpp"
 #include "qnet/graph.hpp"
 #include "qnet/net.hpp"
+#include "qnet/ops.hpp"
 #include "qnet/tensor.hpp"
 
 namespace qnb {
@@ -113,6 +115,8 @@ class Executor {
           d.input_ndim = (int32_t)l.input_shape.size();
           for (size_t i = 0; i < l.input_shape.size() && i < 4; ++i) d.input_shape[i] = l.input_shape[i];
           input_name_ = l.tops[0];
+          input_shape_ = l.input_shape;
+          input_dtype_ = l.mo_type;
           break;
         case qnet::LayerKind::CONV:
           d.conv = qnb_conv_params{l.conv.out_channels, l.conv.kernel_h, l.conv.kernel_w, l.conv.stride_h,
@@ -183,8 +187,25 @@ class Executor {
   std::map<std::string, qnet::Tensor> forward(const std::map<std::string, qnet::Tensor>& inputs) {
     auto it = inputs.find(input_name_);
     if (it == inputs.end()) throw std::invalid_argument("missing input: " + input_name_);
-    const qnet::Tensor& x = it->second;
-    const int64_t batch = x.shape().empty() ? 0 : x.shape()[0];
+    // take_input + the INPUT layer of run_layer_typed (src/net.cpp:288-302, 394-405): the
+    // plan reads batch * (C*H*W) elements of the INPUT layer's mo_type, so the shape and
+    // dtype are checked (and float types cast) before any byte is copied.
+    const std::vector<int64_t>& got = it->second.shape();
+    bool ok = got.size() == input_shape_.size() && !got.empty();
+    for (size_t d = 1; ok && d < input_shape_.size(); ++d) ok = got[d] == input_shape_[d];
+    if (!ok) throw std::invalid_argument("shape mismatch");
+    const qnet::Tensor* xp = &it->second;
+    qnet::Tensor cast;
+    if (xp->dtype() != input_dtype_) {
+      if (qnet::is_float_type(xp->dtype()) && qnet::is_float_type(input_dtype_)) {
+        cast = qnet::cast_float(*xp, input_dtype_);
+        xp = &cast;
+      } else {
+        throw std::invalid_argument("dtype mismatch at blob " + input_name_);
+      }
+    }
+    const qnet::Tensor& x = *xp;
+    const int64_t batch = got[0];
     std::vector<int64_t> oshape = out_shape_;
     oshape[0] = batch;
     qnet::Tensor out(out_dtype_, oshape);
@@ -212,6 +233,8 @@ class Executor {
   std::unique_ptr<qnb_plan, PlanDel> plan_;
   std::vector<qnet::Tensor> bias_;
   std::string input_name_, sink_name_;
+  std::vector<int64_t> input_shape_;
+  qnet::DataType input_dtype_ = qnet::DataType::FP32;
   qnet::DataType out_dtype_ = qnet::DataType::FP32;
   std::vector<int64_t> out_shape_;
   std::optional<qnet::QuantizerValues> out_qv_;

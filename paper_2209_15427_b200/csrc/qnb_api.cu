@@ -476,101 +476,105 @@ qnb_status qnb_conv_forward(const void* x, const int64_t xs[4], qnb_dtype dtype,
                             const void* w, qnb_dtype w_dtype, const qnb_qvals* w_qv, const float* bias,
                             const qnb_conv_params* cp, const qnb_qvals* out_qv, int shift_bits, void* y,
                             int64_t ys[4], qnb_stream s) {
-  QNB_TRY(ensure_device());
-  // src/ops.cpp:106-133 (conv_geometry), same messages.
-  if (cp->groups < 1 || xs[1] % cp->groups != 0 || cp->out_channels % cp->groups != 0)
-    return fail(QNB_E_GROUPS, "group divisibility violation");
-  const int64_t oh = (xs[2] + 2 * cp->pad_h - cp->kernel_h) / cp->stride_h + 1;
-  const int64_t ow = (xs[3] + 2 * cp->pad_w - cp->kernel_w) / cp->stride_w + 1;
-  if (oh < 1 || ow < 1) return fail(QNB_E_EXTENT, "non-positive output extent");
-  if (ys) {
-    ys[0] = xs[0];
-    ys[1] = cp->out_channels;
-    ys[2] = oh;
-    ys[3] = ow;
-  }
-  const bool quant = is_quant(dtype);
-  if (quant && (!in_qv || !w_qv || !out_qv)) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
-  if (quant && w_dtype != dtype) return fail(QNB_E_DTYPE, "quantized conv weight dtype must match input");
-  if (xs[0] == 0 || y == nullptr) return QNB_OK;  // y == NULL: sizing call (ys only)
-  IgemmGeometry g;
-  g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
-  g.q16 = dtype == QNB_INT16Q;
-  g.groups = cp->groups;
-  g.cg = xs[1] / cp->groups;
-  g.og = cp->out_channels / cp->groups;
-  g.kh = cp->kernel_h;
-  g.kw = cp->kernel_w;
-  g.sh = cp->stride_h;
-  g.sw = cp->stride_w;
-  g.ph = cp->pad_h;
-  g.pw = cp->pad_w;
-  g.oh = oh;
-  g.ow = ow;
-  g.is_fc = false;
-  g.fc_h = g.fc_w = g.fc_c = 0;
-  ContractionIO io;
-  io.x = x;
-  io.in = choose_input_layout(g, dtype, xs[0], xs[1], xs[2], xs[3]);
-  io.x_is_nchw = true;
-  io.xN = xs[0];
-  io.xC = xs[1];
-  io.xH = xs[2];
-  io.xW = xs[3];
-  ActLayout out;
-  out.n = xs[0];
-  out.c = cp->out_channels;
-  out.h = oh;
-  out.w = ow;
-  out.c_phys = cp->out_channels;
-  out.dtype = dtype;
-  return run_contraction(g, dtype, io, in_qv, w, w_dtype, w_qv, cp->bias_term ? bias : nullptr, out_qv, shift_bits,
-                         y, out, true, as_stream(s));
+  return qnb::guarded([&]() -> qnb_status {
+    QNB_TRY(ensure_device());
+    // src/ops.cpp:106-133 (conv_geometry), same messages.
+    if (cp->groups < 1 || xs[1] % cp->groups != 0 || cp->out_channels % cp->groups != 0)
+      return fail(QNB_E_GROUPS, "group divisibility violation");
+    const int64_t oh = (xs[2] + 2 * cp->pad_h - cp->kernel_h) / cp->stride_h + 1;
+    const int64_t ow = (xs[3] + 2 * cp->pad_w - cp->kernel_w) / cp->stride_w + 1;
+    if (oh < 1 || ow < 1) return fail(QNB_E_EXTENT, "non-positive output extent");
+    if (ys) {
+      ys[0] = xs[0];
+      ys[1] = cp->out_channels;
+      ys[2] = oh;
+      ys[3] = ow;
+    }
+    const bool quant = is_quant(dtype);
+    if (quant && (!in_qv || !w_qv || !out_qv)) return fail(QNB_E_QVALS, "quantized conv requires quantizer values");
+    if (quant && w_dtype != dtype) return fail(QNB_E_DTYPE, "quantized conv weight dtype must match input");
+    if (xs[0] == 0 || y == nullptr) return QNB_OK;  // y == NULL: sizing call (ys only)
+    IgemmGeometry g;
+    g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
+    g.q16 = dtype == QNB_INT16Q;
+    g.groups = cp->groups;
+    g.cg = xs[1] / cp->groups;
+    g.og = cp->out_channels / cp->groups;
+    g.kh = cp->kernel_h;
+    g.kw = cp->kernel_w;
+    g.sh = cp->stride_h;
+    g.sw = cp->stride_w;
+    g.ph = cp->pad_h;
+    g.pw = cp->pad_w;
+    g.oh = oh;
+    g.ow = ow;
+    g.is_fc = false;
+    g.fc_h = g.fc_w = g.fc_c = 0;
+    ContractionIO io;
+    io.x = x;
+    io.in = choose_input_layout(g, dtype, xs[0], xs[1], xs[2], xs[3]);
+    io.x_is_nchw = true;
+    io.xN = xs[0];
+    io.xC = xs[1];
+    io.xH = xs[2];
+    io.xW = xs[3];
+    ActLayout out;
+    out.n = xs[0];
+    out.c = cp->out_channels;
+    out.h = oh;
+    out.w = ow;
+    out.c_phys = cp->out_channels;
+    out.dtype = dtype;
+    return run_contraction(g, dtype, io, in_qv, w, w_dtype, w_qv, cp->bias_term ? bias : nullptr, out_qv, shift_bits,
+                           y, out, true, as_stream(s));
+  });
 }
 
 qnb_status qnb_inner_product(const void* x, int64_t n, int64_t k, qnb_dtype dtype, const qnb_qvals* in_qv,
                              const void* w, qnb_dtype w_dtype, const qnb_qvals* w_qv, const float* bias,
                              int64_t out_features, const qnb_qvals* out_qv, int shift_bits, void* y,
                              qnb_stream s) {
-  QNB_TRY(ensure_device());
-  const bool quant = is_quant(dtype);
-  if (quant && (!in_qv || !w_qv || !out_qv))
-    return fail(QNB_E_QVALS, "quantized inner product requires quantizer values");
-  if (n == 0) return QNB_OK;
-  IgemmGeometry g;
-  std::memset(&g, 0, sizeof(g));
-  g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
-  g.q16 = dtype == QNB_INT16Q;
-  g.groups = 1;
-  g.cg = k;
-  g.og = out_features;
-  g.kh = g.kw = g.sh = g.sw = 1;
-  g.oh = g.ow = 1;
-  g.is_fc = true;
-  g.fc_h = 1;
-  g.fc_w = 1;
-  g.fc_c = k;
-  ContractionIO io;
-  io.x = x;
-  io.in.n = n;
-  io.in.h = 1;
-  io.in.w = 1;
-  io.in.c = k;
-  io.in.dtype = dtype;
-  io.in.c_phys = round_up(k * (int64_t)dtype_size(dtype), 16) / (int64_t)dtype_size(dtype);
-  io.x_is_nchw = true;
-  io.xN = n;
-  io.xC = k;
-  io.xH = 1;
-  io.xW = 1;
-  ActLayout out;
-  out.n = n;
-  out.c = out_features;
-  out.h = out.w = 1;
-  out.c_phys = out_features;
-  out.dtype = dtype;
-  return run_contraction(g, dtype, io, in_qv, w, w_dtype, w_qv, bias, out_qv, shift_bits, y, out, false,
-                         as_stream(s));
+  return qnb::guarded([&]() -> qnb_status {
+    QNB_TRY(ensure_device());
+    const bool quant = is_quant(dtype);
+    if (quant && (!in_qv || !w_qv || !out_qv))
+      return fail(QNB_E_QVALS, "quantized inner product requires quantizer values");
+    if (n == 0) return QNB_OK;
+    IgemmGeometry g;
+    std::memset(&g, 0, sizeof(g));
+    g.kind = quant ? KIND_I8 : (dtype == QNB_FP16 ? KIND_F16 : KIND_TF32);
+    g.q16 = dtype == QNB_INT16Q;
+    g.groups = 1;
+    g.cg = k;
+    g.og = out_features;
+    g.kh = g.kw = g.sh = g.sw = 1;
+    g.oh = g.ow = 1;
+    g.is_fc = true;
+    g.fc_h = 1;
+    g.fc_w = 1;
+    g.fc_c = k;
+    ContractionIO io;
+    io.x = x;
+    io.in.n = n;
+    io.in.h = 1;
+    io.in.w = 1;
+    io.in.c = k;
+    io.in.dtype = dtype;
+    io.in.c_phys = round_up(k * (int64_t)dtype_size(dtype), 16) / (int64_t)dtype_size(dtype);
+    io.x_is_nchw = true;
+    io.xN = n;
+    io.xC = k;
+    io.xH = 1;
+    io.xW = 1;
+    ActLayout out;
+    out.n = n;
+    out.c = out_features;
+    out.h = out.w = 1;
+    out.c_phys = out_features;
+    out.dtype = dtype;
+    return run_contraction(g, dtype, io, in_qv, w, w_dtype, w_qv, bias, out_qv, shift_bits, y, out, false,
+                           as_stream(s));
+  });
 }
 
 }  // extern "C"

@@ -1709,6 +1709,14 @@ static qnb_status igemm_pack_b_q16(const IgemmGeometry& g, const void* w, IgemmP
 }
 
 qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, IgemmPacked* pk) {
+  // kind::i8 sums raw u8 x u8 products (<= 255^2 each, also per INT16 byte plane and per
+  // split-K partial) in s32 TMEM lanes; the reference accumulates in int64
+  // (src/ops.cpp:73-83).  Beyond K = 33025 a sum could wrap, so such layers are refused
+  // instead of returning silently wrong integers.
+  const int64_t k_real = g.is_fc ? g.fc_h * g.fc_w * g.fc_c : g.cg * g.kh * g.kw;
+  if (g.kind == KIND_I8 && k_real > kMaxExactK)
+    return fail(QNB_E_UNSUPPORTED, "quantized contraction depth " + std::to_string(k_real) +
+                                       " exceeds the exact s32 accumulation bound (33025)");
   if (g.q16) return igemm_pack_b_q16(g, w, pk);
   const int es = kind_es(g.kind);
   const bool quant = g.kind == KIND_I8;

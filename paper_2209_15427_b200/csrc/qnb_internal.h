@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <exception>
+#include <new>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -27,6 +29,22 @@ qnb_status cuda_fail(cudaError_t e, const char* where);
     qnb_status st_ = (call);            \
     if (st_ != QNB_OK) return st_;      \
   } while (0)
+
+// Every extern "C" entry point that allocates host memory or parses untrusted input runs
+// its body through guarded(): no C++ exception crosses the C-ABI (bad_alloc -> QNB_E_OOM,
+// anything else -> QNB_E_ARG with the exception's message).
+template <class F>
+qnb_status guarded(F&& body) {
+  try {
+    return body();
+  } catch (const std::bad_alloc&) {
+    return fail(QNB_E_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(QNB_E_ARG, e.what());
+  } catch (...) {
+    return fail(QNB_E_ARG, "unknown exception");
+  }
+}
 
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
@@ -175,6 +193,10 @@ constexpr int kHkSlot = 1024;
 bool igemm_fast_requant_ok(const std::vector<int64_t>& chan_const, int64_t K, int64_t zw, const Requant& rq);
 
 // Host description of one contraction (conv or inner product) to compile.
+// Largest K whose u8 x u8 dot product cannot overflow an s32 accumulator:
+// 33025 * 255^2 = 2147450625 < 2^31.
+constexpr int64_t kMaxExactK = 33025;
+
 struct IgemmGeometry {
   int kind;            // MmaKind
   int64_t groups;      // G

@@ -5,6 +5,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -77,8 +78,11 @@ qnb_status parse(qnb_model* m) {
   const char* trunc = "truncated model file";
   uint32_t count;
   if (!c.u32(&count)) return qnb::fail(QNB_E_IO, trunc);
-  m->names.reserve(count);
-  m->recs.reserve(count);
+  // the count is untrusted: a record takes at least 31 bytes (name length, tag, rank,
+  // six floats), so never reserve more than the rest of the file can hold
+  const size_t fit = c.left / 31;
+  m->names.reserve(std::min<size_t>(count, fit));
+  m->recs.reserve(std::min<size_t>(count, fit));
   for (uint32_t i = 0; i < count; ++i) {
     qnb_record r;
     std::memset(&r, 0, sizeof(r));
@@ -121,34 +125,36 @@ qnb_status parse(qnb_model* m) {
 extern "C" {
 
 qnb_status qnb_model_open(const char* path, qnb_model** out) {
-  if (!path || !out) return qnb::fail(QNB_E_ARG, "null argument");
-  *out = nullptr;
-  const int fd = ::open(path, O_RDONLY);
-  if (fd < 0) return qnb::fail(QNB_E_IO, std::string("cannot read: ") + path);
-  struct stat st;
-  if (::fstat(fd, &st) != 0) {
-    ::close(fd);
-    return qnb::fail(QNB_E_IO, std::string("cannot read: ") + path);
-  }
-  auto* m = new qnb_model;
-  m->size = (size_t)st.st_size;
-  if (m->size > 0) {
-    m->map = ::mmap(nullptr, m->size, PROT_READ, MAP_PRIVATE, fd, 0);
-    if (m->map == MAP_FAILED) {
-      m->map = nullptr;
+  return qnb::guarded([&]() -> qnb_status {
+    if (!path || !out) return qnb::fail(QNB_E_ARG, "null argument");
+    *out = nullptr;
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) return qnb::fail(QNB_E_IO, std::string("cannot read: ") + path);
+    struct stat st;
+    if (::fstat(fd, &st) != 0) {
       ::close(fd);
-      delete m;
       return qnb::fail(QNB_E_IO, std::string("cannot read: ") + path);
     }
-  }
-  ::close(fd);
-  const qnb_status s = parse(m);
-  if (s != QNB_OK) {
-    qnb_model_close(m);
-    return s;
-  }
-  *out = m;
-  return QNB_OK;
+    auto* m = new qnb_model;
+    m->size = (size_t)st.st_size;
+    if (m->size > 0) {
+      m->map = ::mmap(nullptr, m->size, PROT_READ, MAP_PRIVATE, fd, 0);
+      if (m->map == MAP_FAILED) {
+        m->map = nullptr;
+        ::close(fd);
+        delete m;
+        return qnb::fail(QNB_E_IO, std::string("cannot read: ") + path);
+      }
+    }
+    ::close(fd);
+    const qnb_status s = parse(m);
+    if (s != QNB_OK) {
+      qnb_model_close(m);
+      return s;
+    }
+    *out = m;
+    return QNB_OK;
+  });
 }
 
 qnb_status qnb_model_count(const qnb_model* m, int64_t* n) {
@@ -172,41 +178,43 @@ qnb_status qnb_model_close(qnb_model* m) {
 }
 
 qnb_status qnb_model_save(const char* path, const qnb_record* recs, int64_t n) {
-  if (!path || (n > 0 && !recs) || n < 0) return qnb::fail(QNB_E_ARG, "null argument");
-  std::string buf(kMagic, 4);
-  buf.push_back((char)kVersion);
-  put_u32(&buf, (uint32_t)n);
-  for (int64_t i = 0; i < n; ++i) {
-    const qnb_record& r = recs[i];
-    const std::string name = r.name ? r.name : "";
-    if (name.size() > 0xffff) return qnb::fail(QNB_E_ARG, "record name too long: " + name);
-    if (r.rank < 0 || r.rank > 8 || r.dtype < QNB_FP32 || r.dtype > QNB_INT16Q)
-      return qnb::fail(QNB_E_ARG, "invalid record: " + name);
-    int64_t count_el = 1;
-    for (int d = 0; d < r.rank; ++d) count_el *= r.extents[d];
-    if (r.payload_bytes != count_el * byte_width(r.dtype) || (r.payload_bytes > 0 && !r.payload))
-      return qnb::fail(QNB_E_ARG, "payload size mismatch: " + name);
-    buf.push_back((char)(name.size() & 0xff));
-    buf.push_back((char)((name.size() >> 8) & 0xff));
-    buf.append(name);
-    buf.push_back((char)(uint8_t)r.dtype);
-    buf.push_back((char)(uint8_t)r.rank);
-    for (int d = 0; d < r.rank; ++d) put_u32(&buf, (uint32_t)r.extents[d]);
-    put_f32(&buf, r.f_min);
-    put_f32(&buf, r.f_max);
-    put_f32(&buf, r.scale);
-    put_f32(&buf, r.zero);
-    put_f32(&buf, r.one);
-    put_f32(&buf, 0.0f);  // reserved
-    buf.append(static_cast<const char*>(r.payload), (size_t)r.payload_bytes);
-  }
-  const std::string tmp = std::string(path) + ".tmp";
-  FILE* f = std::fopen(tmp.c_str(), "wb");
-  if (!f) return qnb::fail(QNB_E_IO, "cannot write: " + tmp);
-  const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
-  if (std::fclose(f) != 0 || !ok) return qnb::fail(QNB_E_IO, "cannot write: " + tmp);
-  if (std::rename(tmp.c_str(), path) != 0) return qnb::fail(QNB_E_IO, std::string("cannot write: ") + path);
-  return QNB_OK;
+  return qnb::guarded([&]() -> qnb_status {
+    if (!path || (n > 0 && !recs) || n < 0) return qnb::fail(QNB_E_ARG, "null argument");
+    std::string buf(kMagic, 4);
+    buf.push_back((char)kVersion);
+    put_u32(&buf, (uint32_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      const qnb_record& r = recs[i];
+      const std::string name = r.name ? r.name : "";
+      if (name.size() > 0xffff) return qnb::fail(QNB_E_ARG, "record name too long: " + name);
+      if (r.rank < 0 || r.rank > 8 || r.dtype < QNB_FP32 || r.dtype > QNB_INT16Q)
+        return qnb::fail(QNB_E_ARG, "invalid record: " + name);
+      int64_t count_el = 1;
+      for (int d = 0; d < r.rank; ++d) count_el *= r.extents[d];
+      if (r.payload_bytes != count_el * byte_width(r.dtype) || (r.payload_bytes > 0 && !r.payload))
+        return qnb::fail(QNB_E_ARG, "payload size mismatch: " + name);
+      buf.push_back((char)(name.size() & 0xff));
+      buf.push_back((char)((name.size() >> 8) & 0xff));
+      buf.append(name);
+      buf.push_back((char)(uint8_t)r.dtype);
+      buf.push_back((char)(uint8_t)r.rank);
+      for (int d = 0; d < r.rank; ++d) put_u32(&buf, (uint32_t)r.extents[d]);
+      put_f32(&buf, r.f_min);
+      put_f32(&buf, r.f_max);
+      put_f32(&buf, r.scale);
+      put_f32(&buf, r.zero);
+      put_f32(&buf, r.one);
+      put_f32(&buf, 0.0f);  // reserved
+      buf.append(static_cast<const char*>(r.payload), (size_t)r.payload_bytes);
+    }
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return qnb::fail(QNB_E_IO, "cannot write: " + tmp);
+    const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+    if (std::fclose(f) != 0 || !ok) return qnb::fail(QNB_E_IO, "cannot write: " + tmp);
+    if (std::rename(tmp.c_str(), path) != 0) return qnb::fail(QNB_E_IO, std::string("cannot write: ") + path);
+    return QNB_OK;
+  });
 }
 
 }  // extern "C"

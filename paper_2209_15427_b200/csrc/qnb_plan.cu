@@ -1025,54 +1025,56 @@ extern "C" {
 
 qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32_t n_blobs, const qnb_plan_opts* opts,
                            qnb_plan** out) {
-  QNB_TRY(ensure_device());
-  if (!layers || n_layers <= 0 || !out) return fail(QNB_E_ARG, "empty graph");
-  auto P = std::make_unique<qnb_plan>();
-  P->layers.assign(layers, layers + n_layers);
-  P->blobs.resize((size_t)n_blobs);
-  P->n_user_blobs = n_blobs;
-  P->max_batch = opts && opts->max_batch > 0 ? opts->max_batch : 1;
-  P->use_graph = opts ? opts->use_cuda_graph != 0 : true;
-  P->flags = opts ? opts->flags : 0;
-  QNB_CUDA(cudaGetDevice(&P->device));
-  QNB_TRY(build_blob_table(*P));
-  QNB_TRY(lower(*P));
-  QNB_TRY(assign_layouts(*P));
-  // arena
-  size_t off = 0;
-  for (size_t b = 0; b < P->blobs.size(); ++b) {
-    Blob& bl = P->blobs[b];
-    if (!bl.needs_buffer || bl.alias >= 0 || bl.external) continue;
-    if ((int)b == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) continue;
-    bl.off = off;
-    off += round_up((int64_t)bl.L.bytes() + 1024, 256);
-  }
-  P->arena_bytes = off;
-  if (off) QNB_CUDA(cudaMalloc((void**)&P->arena, off));
-  for (size_t b = 0; b < P->blobs.size(); ++b) {
-    Blob& bl = P->blobs[b];
-    if (!bl.needs_buffer || bl.alias >= 0 || bl.external) continue;
-    if ((int)b == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) continue;
-    QNB_TRY(fill_buffer(P->arena + bl.off, bl.L.bytes() + 1024, bl.dtype, bl.has_qv ? bl.qv.zero : 0, 0));
-  }
-  QNB_TRY(emit(*P));
-  P->launches_per_forward = (int64_t)P->steps.size();
-  for (const Step& st : P->steps)
-    if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1 && st.ig.tile_sema == nullptr) ++P->launches_per_forward;
-  QNB_CUDA(cudaDeviceSynchronize());
-  // output description (reference layout)
-  const Blob& sk = P->blobs[P->sink_blob];
-  P->out_dtype = sk.dtype;
-  P->out_ndim = sk.ndim;
-  P->out_shape[0] = P->max_batch;
-  P->out_shape[1] = sk.c;
-  P->out_shape[2] = sk.h;
-  P->out_shape[3] = sk.w;
-  P->out_bytes_per_sample = sk.c * sk.h * sk.w * (int64_t)dtype_size(sk.dtype);
-  const Blob& ib = P->blobs[P->input_blob];
-  P->in_bytes_per_sample = ib.c * ib.h * ib.w * (int64_t)dtype_size(ib.dtype);
-  *out = P.release();
-  return QNB_OK;
+  return qnb::guarded([&]() -> qnb_status {
+    QNB_TRY(ensure_device());
+    if (!layers || n_layers <= 0 || !out) return fail(QNB_E_ARG, "empty graph");
+    auto P = std::make_unique<qnb_plan>();
+    P->layers.assign(layers, layers + n_layers);
+    P->blobs.resize((size_t)n_blobs);
+    P->n_user_blobs = n_blobs;
+    P->max_batch = opts && opts->max_batch > 0 ? opts->max_batch : 1;
+    P->use_graph = opts ? opts->use_cuda_graph != 0 : true;
+    P->flags = opts ? opts->flags : 0;
+    QNB_CUDA(cudaGetDevice(&P->device));
+    QNB_TRY(build_blob_table(*P));
+    QNB_TRY(lower(*P));
+    QNB_TRY(assign_layouts(*P));
+    // arena
+    size_t off = 0;
+    for (size_t b = 0; b < P->blobs.size(); ++b) {
+      Blob& bl = P->blobs[b];
+      if (!bl.needs_buffer || bl.alias >= 0 || bl.external) continue;
+      if ((int)b == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) continue;
+      bl.off = off;
+      off += round_up((int64_t)bl.L.bytes() + 1024, 256);
+    }
+    P->arena_bytes = off;
+    if (off) QNB_CUDA(cudaMalloc((void**)&P->arena, off));
+    for (size_t b = 0; b < P->blobs.size(); ++b) {
+      Blob& bl = P->blobs[b];
+      if (!bl.needs_buffer || bl.alias >= 0 || bl.external) continue;
+      if ((int)b == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) continue;
+      QNB_TRY(fill_buffer(P->arena + bl.off, bl.L.bytes() + 1024, bl.dtype, bl.has_qv ? bl.qv.zero : 0, 0));
+    }
+    QNB_TRY(emit(*P));
+    P->launches_per_forward = (int64_t)P->steps.size();
+    for (const Step& st : P->steps)
+      if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1 && st.ig.tile_sema == nullptr) ++P->launches_per_forward;
+    QNB_CUDA(cudaDeviceSynchronize());
+    // output description (reference layout)
+    const Blob& sk = P->blobs[P->sink_blob];
+    P->out_dtype = sk.dtype;
+    P->out_ndim = sk.ndim;
+    P->out_shape[0] = P->max_batch;
+    P->out_shape[1] = sk.c;
+    P->out_shape[2] = sk.h;
+    P->out_shape[3] = sk.w;
+    P->out_bytes_per_sample = sk.c * sk.h * sk.w * (int64_t)dtype_size(sk.dtype);
+    const Blob& ib = P->blobs[P->input_blob];
+    P->in_bytes_per_sample = ib.c * ib.h * ib.w * (int64_t)dtype_size(ib.dtype);
+    *out = P.release();
+    return QNB_OK;
+  });
 }
 
 // Host-buffer forwards are pipelined: the batch is cut into at most 8 chunks, chunk
@@ -1164,59 +1166,61 @@ static bool is_pinned(const void* p) {
 
 qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32_t input_on_host, void* output,
                             int32_t output_on_host, qnb_stream s_) {
-  if (!P) return fail(QNB_E_ARG, "null plan");
-  if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
-  cudaStream_t s = as_stream(s_);
-  if (input_on_host && !P->in_staging)
-    QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
-  if (output_on_host && !P->out_staging)
-    QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
-  if (input_on_host && !P->copy_stream) {
-    QNB_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
-    QNB_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
-    P->ev_copy.resize(8);
-    for (auto& e : P->ev_copy) QNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  const bool pinned_in = input_on_host && is_pinned(input);
-  const bool pinned_out = !output_on_host || is_pinned(output);
-  // pageable host buffers cannot be captured: run those forwards eagerly
-  if (P->use_graph && (!input_on_host || pinned_in) && pinned_out) {
-    const int32_t flags = (input_on_host ? 1 : 0) | (output_on_host ? 2 : 0);
-    qnb_plan::GraphEntry* hit = nullptr;
-    for (auto& ge : P->graphs)
-      if (ge.in == input && ge.out == output && ge.batch == batch && ge.flags == flags) hit = &ge;
-    if (!hit) {
-      constexpr size_t kMaxGraphs = 16;
-      if (P->graphs.size() >= kMaxGraphs) {  // evict the least recently used
-        auto lru = std::min_element(P->graphs.begin(), P->graphs.end(),
-                                    [](const qnb_plan::GraphEntry& a, const qnb_plan::GraphEntry& b) { return a.last_use < b.last_use; });
-        cudaGraphExecDestroy(lru->exec);
-        P->graphs.erase(lru);
-      }
-      cudaGraph_t graph;
-      if (!P->capture_stream) QNB_CUDA(cudaStreamCreateWithFlags(&P->capture_stream, cudaStreamNonBlocking));
-      QNB_CUDA(cudaStreamBeginCapture(P->capture_stream, cudaStreamCaptureModeThreadLocal));
-      qnb_status st = forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in,
-                                   P->capture_stream);
-      cudaError_t e = cudaStreamEndCapture(P->capture_stream, &graph);
-      if (st != QNB_OK) return st;
-      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-      cudaGraphExec_t ex = nullptr;
-      e = cudaGraphInstantiate(&ex, graph, 0);
-      cudaGraphDestroy(graph);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-      P->graphs.push_back(qnb_plan::GraphEntry{input, output, batch, flags, ex, 0});
-      hit = &P->graphs.back();
+  return qnb::guarded([&]() -> qnb_status {
+    if (!P) return fail(QNB_E_ARG, "null plan");
+    if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
+    cudaStream_t s = as_stream(s_);
+    if (input_on_host && !P->in_staging)
+      QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
+    if (output_on_host && !P->out_staging)
+      QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
+    if (input_on_host && !P->copy_stream) {
+      QNB_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+      QNB_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+      P->ev_copy.resize(8);
+      for (auto& e : P->ev_copy) QNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    hit->last_use = ++P->graph_clock;
-    P->exec = hit->exec;
-    QNB_CUDA(cudaGraphLaunch(P->exec, s));
-  } else {
-    QNB_TRY(forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in, s));
-  }
-  const int64_t nch = input_on_host ? pipeline_chunks(batch) : 1;
-  count_launch((uint64_t)(P->launches_per_forward * nch));
-  return QNB_OK;
+    const bool pinned_in = input_on_host && is_pinned(input);
+    const bool pinned_out = !output_on_host || is_pinned(output);
+    // pageable host buffers cannot be captured: run those forwards eagerly
+    if (P->use_graph && (!input_on_host || pinned_in) && pinned_out) {
+      const int32_t flags = (input_on_host ? 1 : 0) | (output_on_host ? 2 : 0);
+      qnb_plan::GraphEntry* hit = nullptr;
+      for (auto& ge : P->graphs)
+        if (ge.in == input && ge.out == output && ge.batch == batch && ge.flags == flags) hit = &ge;
+      if (!hit) {
+        constexpr size_t kMaxGraphs = 16;
+        if (P->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+          auto lru = std::min_element(P->graphs.begin(), P->graphs.end(),
+                                      [](const qnb_plan::GraphEntry& a, const qnb_plan::GraphEntry& b) { return a.last_use < b.last_use; });
+          cudaGraphExecDestroy(lru->exec);
+          P->graphs.erase(lru);
+        }
+        cudaGraph_t graph;
+        if (!P->capture_stream) QNB_CUDA(cudaStreamCreateWithFlags(&P->capture_stream, cudaStreamNonBlocking));
+        QNB_CUDA(cudaStreamBeginCapture(P->capture_stream, cudaStreamCaptureModeThreadLocal));
+        qnb_status st = forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in,
+                                     P->capture_stream);
+        cudaError_t e = cudaStreamEndCapture(P->capture_stream, &graph);
+        if (st != QNB_OK) return st;
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+        cudaGraphExec_t ex = nullptr;
+        e = cudaGraphInstantiate(&ex, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+        P->graphs.push_back(qnb_plan::GraphEntry{input, output, batch, flags, ex, 0});
+        hit = &P->graphs.back();
+      }
+      hit->last_use = ++P->graph_clock;
+      P->exec = hit->exec;
+      QNB_CUDA(cudaGraphLaunch(P->exec, s));
+    } else {
+      QNB_TRY(forward_body(*P, batch, input, input_on_host, output, output_on_host, pinned_in, s));
+    }
+    const int64_t nch = input_on_host ? pipeline_chunks(batch) : 1;
+    count_launch((uint64_t)(P->launches_per_forward * nch));
+    return QNB_OK;
+  });
 }
 
 qnb_status qnb_plan_output_info(const qnb_plan* P, int32_t* dtype, int32_t* ndim, int64_t shape[4]) {
@@ -1354,36 +1358,38 @@ qnb_status minmax(const uint8_t* base, const DevLayout& L, int dtype, int64_t de
 extern "C" {
 
 qnb_status qnb_plan_observe(qnb_plan* P, const void* input, int64_t batch, double* mins, double* maxs, qnb_stream s_) {
-  if (!P || !mins || !maxs) return fail(QNB_E_ARG, "null argument");
-  if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
-  cudaStream_t s = as_stream(s_);
-  void* out = nullptr;
-  QNB_CUDA(cudaMallocAsync(&out, (size_t)(P->out_bytes_per_sample * batch), s));
-  QNB_TRY(launch_steps(*P, batch, input, out, s));
-  count_launch((uint64_t)P->launches_per_forward);
-  const double nan = std::nan("");
-  for (int b = 0; b < P->n_user_blobs; ++b) {
-    mins[b] = maxs[b] = nan;
-    const Blob& bl = P->blobs[b];
-    if (!bl.defined || (bl.dtype != QNB_FP32 && bl.dtype != QNB_FP16)) continue;
-    const int r = root_of(*P, (int)b);
-    const Blob& rb = P->blobs[r];
-    if (b == P->input_blob || rb.external) {
-      QNB_TRY(minmax((const uint8_t*)input, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
-    } else if (r == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) {
-      QNB_TRY(minmax((const uint8_t*)out, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
-    } else if (rb.needs_buffer) {
-      DevLayout L = dev_layout(rb.L);
-      if (L.pslot != 0) return fail(QNB_E_UNSUPPORTED, "observe on a pair-interleaved blob");
-      L.n = batch;
-      QNB_TRY(minmax(P->arena + rb.off, L, bl.dtype, 0, s, &mins[b], &maxs[b]));
-    } else if (r == P->sink_blob) {
-      QNB_TRY(minmax((const uint8_t*)out, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+  return qnb::guarded([&]() -> qnb_status {
+    if (!P || !mins || !maxs) return fail(QNB_E_ARG, "null argument");
+    if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
+    cudaStream_t s = as_stream(s_);
+    void* out = nullptr;
+    QNB_CUDA(cudaMallocAsync(&out, (size_t)(P->out_bytes_per_sample * batch), s));
+    QNB_TRY(launch_steps(*P, batch, input, out, s));
+    count_launch((uint64_t)P->launches_per_forward);
+    const double nan = std::nan("");
+    for (int b = 0; b < P->n_user_blobs; ++b) {
+      mins[b] = maxs[b] = nan;
+      const Blob& bl = P->blobs[b];
+      if (!bl.defined || (bl.dtype != QNB_FP32 && bl.dtype != QNB_FP16)) continue;
+      const int r = root_of(*P, (int)b);
+      const Blob& rb = P->blobs[r];
+      if (b == P->input_blob || rb.external) {
+        QNB_TRY(minmax((const uint8_t*)input, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+      } else if (r == P->sink_blob && P->ops.back().kind == OP_SOFTMAX) {
+        QNB_TRY(minmax((const uint8_t*)out, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+      } else if (rb.needs_buffer) {
+        DevLayout L = dev_layout(rb.L);
+        if (L.pslot != 0) return fail(QNB_E_UNSUPPORTED, "observe on a pair-interleaved blob");
+        L.n = batch;
+        QNB_TRY(minmax(P->arena + rb.off, L, bl.dtype, 0, s, &mins[b], &maxs[b]));
+      } else if (r == P->sink_blob) {
+        QNB_TRY(minmax((const uint8_t*)out, DevLayout{}, bl.dtype, batch * bl.c * bl.h * bl.w, s, &mins[b], &maxs[b]));
+      }
     }
-  }
-  QNB_CUDA(cudaFreeAsync(out, s));
-  QNB_CUDA(cudaStreamSynchronize(s));
-  return QNB_OK;
+    QNB_CUDA(cudaFreeAsync(out, s));
+    QNB_CUDA(cudaStreamSynchronize(s));
+    return QNB_OK;
+  });
 }
 
 qnb_status qnb_plan_destroy(qnb_plan* P) {

@@ -60,28 +60,38 @@ def record_qvals(rec: ParamRecord) -> QVals:
     return QVals(rec.f_min, rec.f_max, rec.scale, zi, rec.one, lo, hi)
 
 
-class Model:
-    """qnet::Model.  Loaded models keep the file mapping alive while referenced."""
+class _Mapping:
+    """Owns one qnb_model handle (the file mapping); unmapped when the last Model or
+    payload view referencing it is gone."""
 
-    def __init__(self, records=None, _handle=None):
-        self.records = list(records or [])
-        self._h = _handle
-
-    def find(self, name: str):
-        return next((r for r in self.records if r.name == name), None)
+    def __init__(self, handle):
+        self.h = handle
 
     def __del__(self):
         try:
-            if self._h:
-                L.lib().qnb_model_close(self._h)
+            if self.h:
+                L.lib().qnb_model_close(self.h)
         except Exception:
             pass
+
+
+class Model:
+    """qnet::Model.  A loaded model's payloads are views into the file mapping; every
+    view holds a reference to the mapping, so it stays valid after the Model is gone."""
+
+    def __init__(self, records=None, _mapping=None):
+        self.records = list(records or [])
+        self._mapping = _mapping
+
+    def find(self, name: str):
+        return next((r for r in self.records if r.name == name), None)
 
 
 def load_model(path: str) -> Model:
     lib = L.lib()
     h = C.c_void_p()
     check(lib.qnb_model_open(str(path).encode(), C.byref(h)))
+    mapping = _Mapping(h)
     n = C.c_int64()
     check(lib.qnb_model_count(h, C.byref(n)))
     recs = []
@@ -90,13 +100,14 @@ def load_model(path: str) -> Model:
         check(lib.qnb_model_record(h, i, C.byref(r)))
         if r.payload_bytes:
             buf = (C.c_uint8 * r.payload_bytes).from_address(r.payload)
+            buf._mapping = mapping  # the view's base chain keeps the mapping alive
             payload = np.frombuffer(buf, np.uint8)
             payload.flags.writeable = False  # the mapping is read-only
         else:
             payload = np.empty(0, np.uint8)
         recs.append(ParamRecord(r.name.decode(), r.dtype, tuple(r.extents[: r.rank]), r.f_min, r.f_max,
                                 r.scale, r.zero, r.one, payload))
-    return Model(recs, h)
+    return Model(recs, mapping)
 
 
 def save_model(m: Model, path: str) -> None:

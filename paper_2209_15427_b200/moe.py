@@ -352,6 +352,12 @@ class MoeNet:
         self.last_stats = {"counts": counts}
         return self.last_stats
 
+    def moe_output(self, B: int) -> np.ndarray:
+        """The MoE layer's top blob of the last forward at batch B, (B, features) in the
+        top dtype (a checkpoint for parity tests)."""
+        p = self._pipes[B]
+        return p["bufs"]["M"].cpu().numpy().view(NP_OF[p["top_dtype"]]).reshape(B, p["per"])
+
     def forward(self, inputs: dict) -> dict:
         """Net::forward (src/net.cpp:305-330) with host arrays in and out."""
         import torch

@@ -440,15 +440,30 @@ class Net:
             self._plans[key] = self._float_plan(g, x.shape[0], Plan.EXACT_FLOAT)
         return self._plans[key].forward_host(x)
 
+    @staticmethod
+    def _input_dtype(x: np.ndarray, inl: dict) -> np.ndarray:
+        """The INPUT layer of run_layer_typed (src/net.cpp:394-405): the plan reads the
+        layer's mo_type; float inputs are cast to it, anything else must already be it."""
+        want = G.DTYPE_CODE[inl["top_data_type"]]
+        if want == 0 and x.dtype.kind == "f":
+            return np.ascontiguousarray(x, np.float32)
+        if want == 1 and x.dtype.kind == "f":  # FP16 tensors travel as raw uint16 bits
+            return np.ascontiguousarray(x, np.float16).view(np.uint16)
+        if x.dtype == NP_OF[want]:
+            return x
+        raise QnbError(6, "dtype mismatch at blob " + inl["top"][0])
+
     def forward(self, inputs: dict) -> dict:
         """src/net.cpp:305-330: returns {sink: tensor} in the reference layout."""
         name = G.input_name(self.graph)
         if name not in inputs:
             raise QnbError(1, "missing input: " + name)
         x = np.ascontiguousarray(inputs[name])
-        want = next(l for l in self.graph["layers"] if l["kind"] == "input")["input_shape"]
+        inl = next(l for l in self.graph["layers"] if l["kind"] == "input")
+        want = inl["input_shape"]
         if x.ndim != len(want) or list(x.shape[1:]) != list(want[1:]):
             raise QnbError(2, "shape mismatch")
+        x = self._input_dtype(x, inl)
         if self.mode == OBSERVE:
             return {G.sinks(self.graph)[-1]: self.observe(x)}
         if self.mode == PSEUDO:

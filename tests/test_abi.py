@@ -86,3 +86,20 @@ def test_compute_fails_loudly_without_gpu():
     with pytest.raises(_lib.QnbError) as e:
         ops.quantize(np.zeros(8, np.float32), qv, _lib.INT8Q)
     assert e.value.status == 8  # QNB_E_CUDA
+
+
+def test_net_forward_input_dtype_checks():
+    """Net.forward mirrors take_input + the INPUT layer (src/net.cpp:288-302, 394-405):
+    a wrong shape is "shape mismatch", a non-float array for a float input is
+    "dtype mismatch at blob <top>" (checked before any device work)."""
+    from paper_2209_15427_b200 import graphs
+    from paper_2209_15427_b200.net import Net
+    net = Net(graphs.lenet5(1))
+    with pytest.raises(_lib.QnbError, match="shape mismatch"):
+        net.forward({"data": np.zeros((2, 1, 27, 28), np.float32)})
+    with pytest.raises(_lib.QnbError, match="dtype mismatch at blob data"):
+        net.forward({"data": np.zeros((2, 1, 28, 28), np.uint8)})
+    inl = next(l for l in net.graph["layers"] if l["kind"] == "input")
+    x = np.linspace(-3, 3, 2 * 28 * 28).reshape(2, 1, 28, 28)
+    assert Net._input_dtype(x, inl).dtype == np.float32
+    assert np.array_equal(Net._input_dtype(x, inl), x.astype(np.float32))

@@ -201,6 +201,25 @@ def test_inner_product_float(oracle_impl):
     assert np.abs(ours - theirs).max() <= 1e-2 * float(theirs.max() - theirs.min())
 
 
+def test_int8_contraction_depth_bound(oracle_impl):
+    """kind::i8 accumulates u8 x u8 products in s32 (the reference in int64,
+    src/ops.cpp:73-83): K = 33025 is the deepest exact contraction and still runs
+    bit-exact at all-255 operands; K = 33026 is refused with QNB_E_UNSUPPORTED."""
+    qx, qw = qv_of(oracle_impl, 0, 3), qv_of(oracle_impl, -0.05, 0.05)
+    K = 33025
+    x = np.full((2, K), 255, np.uint8)
+    w = np.full((K, 16), 255, np.uint8)
+    bias = np.zeros(16, np.float32)
+    qo = qv_of(oracle_impl, -2000, 2000)
+    ours = ops.inner_product(x, INT8Q, w, INT8Q, bias, 16, qx, qw, qo)
+    theirs = oracle_impl.inner_product(x, INT8Q, w, INT8Q, bias, 16, qx, qw, qo)
+    assert_bits_equal(ours, theirs, "ip K=33025")
+    with pytest.raises(ops.QnbError, match="exact s32 accumulation bound") as e:
+        ops.inner_product(np.full((2, K + 1), 255, np.uint8), INT8Q, np.full((K + 1, 16), 255, np.uint8), INT8Q,
+                          bias, 16, qx, qw, qo)
+    assert e.value.status == 10
+
+
 def test_conv_errors_match_reference():
     x = np.zeros((1, 3, 4, 4), np.float32)
     w = np.zeros((4, 3, 5, 5), np.float32)

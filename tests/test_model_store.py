@@ -82,6 +82,31 @@ def test_payloads_are_views_into_the_mapping(tmp_path):
     assert (m.records[1].f_min, m.records[1].f_max) == (-1.5, 2.5)
 
 
+def test_payload_views_outlive_the_model(tmp_path):
+    """The mapping is released only when the last view into it is gone: records taken
+    from a temporary Model stay readable (the views hold the mapping alive)."""
+    import gc
+    p = tmp_path / "m.qcnm"
+    w = np.arange(4096, dtype=np.float32)
+    save_model(Model([ParamRecord("fc.weight", 0, w.shape, payload=w.view(np.uint8).reshape(-1))]), str(p))
+    recs = load_model(str(p)).records
+    gc.collect()
+    assert float(recs[0].array().sum()) == float(w.sum())
+    arr = load_model(str(p)).records[0].array()
+    gc.collect()
+    assert np.array_equal(arr, w)
+
+
+def test_huge_record_count_is_a_truncated_file(tmp_path):
+    """An untrusted u32 record count must not turn into a huge reservation (the
+    reference's reader reports the file as truncated)."""
+    bad = tmp_path / "count.qcnm"
+    bad.write_bytes(b"QCNM\x01\xff\xff\xff\xff")
+    with pytest.raises(QnbError, match="truncated model file") as e:
+        load_model(str(bad))
+    assert e.value.status == 11
+
+
 def test_load_errors_carry_reference_messages(tmp_path):
     with pytest.raises(QnbError, match="cannot read: "):
         load_model(str(tmp_path / "missing.qcnm"))
