@@ -163,10 +163,20 @@ qnb_status qnb_moe_gate(const float* feats, int64_t batch, int64_t dim, const fl
                         const float* wb, const float* wc, int64_t n_experts, int64_t top_k,
                         int noise_enabled, uint64_t seed, int64_t* idx, float* weights,
                         qnb_stream s);
-/* weighted combine in selection order  src/moe.cpp:206-217, 240-249.
- * expert_out: [n_experts][batch][per] (only selected rows are read). */
+/* qnb_moe_gate for the batch rows [sample_offset, sample_offset + batch) of a larger
+ * logical batch: gating_noise is keyed on the GLOBAL sample index (src/moe.cpp:93-94,
+ * 188), so a rank holding a shard of the batch draws the reference's noise. */
+qnb_status qnb_moe_gate_at(const float* feats, int64_t batch, int64_t dim, const float* wa,
+                           const float* wb, const float* wc, int64_t n_experts, int64_t top_k,
+                           int noise_enabled, uint64_t seed, int64_t sample_offset, int64_t* idx,
+                           float* weights, qnb_stream s);
 /* expf exactly as the reference's libm computes it (used by gating; host copy). */
 float qnb_gating_expf(float x);
+/* gating_noise (src/moe.cpp:53-71), host: SplitMix64 keying + Box-Muller with the host
+ * libm; the device reads a table of these values. */
+float qnb_gating_noise(uint64_t seed, int64_t sample, int64_t expert, int32_t stream);
+/* weighted combine in selection order  src/moe.cpp:206-217, 240-249.
+ * expert_out: [n_experts][batch][per] (only selected rows are read). */
 qnb_status qnb_moe_combine(const float* expert_out, int64_t batch, int64_t per, int64_t top_k,
                            const int64_t* idx, const float* weights, float* out, qnb_stream s);
 

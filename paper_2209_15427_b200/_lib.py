@@ -158,6 +158,8 @@ _SIGS = {
                                  _P, _I64, C.POINTER(QVals), _I32, _P, _P]),
     "qnb_moe_gate": (_I32, [_P, _I64, _I64, _P, _P, _P, _I64, _I64, _I32, C.c_uint64, _P, _P, _P]),
     "qnb_gating_expf": (C.c_float, [C.c_float]),
+    "qnb_moe_gate_at": (_I32, [_P, _I64, _I64, _P, _P, _P, _I64, _I64, _I32, C.c_uint64, _I64, _P, _P, _P]),
+    "qnb_gating_noise": (C.c_float, [C.c_uint64, _I64, _I64, _I32]),
     "qnb_moe_combine": (_I32, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
     "qnb_moe_route": (_I32, [_P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     "qnb_gather_rows": (_I32, [_P, _I64, _P, _I64, _P, _P]),

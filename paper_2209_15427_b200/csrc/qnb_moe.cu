@@ -9,6 +9,9 @@
 // copy of this function against the host libm over ~3e8 inputs.
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "qnb_device.cuh"
 #include "qnb_internal.h"
@@ -73,15 +76,20 @@ __host__ __device__ inline float gate_expf(float x) {
   return (float)y;
 }
 
-// Counter-keyed SplitMix64 + Box-Muller (src/moe.cpp:32-38, 53-71).
-__device__ inline uint64_t sm64(uint64_t& st) {
+// Counter-keyed SplitMix64 + Box-Muller (src/moe.cpp:32-38, 53-71), evaluated on the HOST
+// with the same libm the reference links (std::log / std::cos / std::sqrt in double): the
+// draws depend only on (seed, sample, expert, stream), never on data, so the plan computes
+// the B x N x 2 table once per (seed, sample offset, batch) and the gate kernel reads it.
+// That makes the noisy logits bit-identical to the reference by construction (a device
+// log/cos differs from glibc in the last ulp often enough to flip ~1 % of selections).
+static uint64_t sm64(uint64_t& st) {
   st += 0x9E3779B97F4A7C15ull;
   uint64_t z = st;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-__device__ inline float gate_noise(uint64_t seed, int64_t sample, int64_t expert, int stream) {
+float host_gating_noise(uint64_t seed, int64_t sample, int64_t expert, int stream) {
   uint64_t st = seed;
   (void)sm64(st);
   st ^= 0x632BE59BD9B4E019ull * (uint64_t)(sample + 1);
@@ -90,17 +98,45 @@ __device__ inline float gate_noise(uint64_t seed, int64_t sample, int64_t expert
   (void)sm64(st);
   st ^= 0xC2B2AE3D27D4EB4Full * (uint64_t)(stream + 1);
   const uint64_t a = sm64(st), b = sm64(st);
-  const double u1 = __ddiv_rn(__dadd_rn((double)(a >> 11), 1.0), 9007199254740993.0);
-  const double u2 = __ddiv_rn((double)(b >> 11), 9007199254740992.0);
-  return __double2float_rn(__dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586476925287, u2))));
+  const double u1 = ((double)(a >> 11) + 1.0) / 9007199254740993.0;
+  const double u2 = (double)(b >> 11) / 9007199254740992.0;
+  const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925287 * u2);
+  return (float)z;
+}
+
+// Device table of (e1, e2) per (sample, expert): e1 = noise(.., 0), e2 = 10 * noise(.., 1)
+// (src/moe.cpp:92-95), for samples [offset, offset + B).  Cached per process.
+static std::mutex g_noise_mu;
+static std::map<std::tuple<uint64_t, int64_t, int64_t, int64_t>, float*> g_noise;
+
+qnb_status noise_table(uint64_t seed, int64_t offset, int64_t B, int64_t N, const float** out) {
+  std::lock_guard<std::mutex> lk(g_noise_mu);
+  const auto key = std::make_tuple(seed, offset, B, N);
+  auto it = g_noise.find(key);
+  if (it != g_noise.end()) {
+    *out = it->second;
+    return QNB_OK;
+  }
+  std::vector<float> h((size_t)(B * N * 2));
+  for (int64_t s = 0; s < B; ++s)
+    for (int64_t i = 0; i < N; ++i) {
+      h[(size_t)((s * N + i) * 2)] = host_gating_noise(seed, offset + s, i, 0);
+      h[(size_t)((s * N + i) * 2 + 1)] = 10.0f * host_gating_noise(seed, offset + s, i, 1);
+    }
+  float* d = nullptr;
+  QNB_CUDA(cudaMalloc(&d, h.size() * sizeof(float)));
+  QNB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  g_noise.emplace(key, d);
+  *out = d;
+  return QNB_OK;
 }
 
 constexpr int kMaxExperts = 64;
 
 __global__ void moe_gate_kernel(const float* __restrict__ feats, int64_t B, int64_t D, const float* __restrict__ wa,
                                 const float* __restrict__ wb, const float* __restrict__ wc, int64_t N, int64_t K,
-                                int noise, uint64_t seed, int64_t* __restrict__ idx, float* __restrict__ wout,
-                                int* __restrict__ err) {
+                                const float* __restrict__ noise, int64_t* __restrict__ idx,
+                                float* __restrict__ wout, int* __restrict__ err) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= B) return;
   float z[kMaxExperts], p[kMaxExperts];
@@ -113,8 +149,8 @@ __global__ void moe_gate_kernel(const float* __restrict__ feats, int64_t B, int6
     }
     float e1 = 0.0f, e2 = 0.0f;
     if (noise) {
-      e1 = gate_noise(seed, s, i, 0);
-      e2 = __fmul_rn(10.0f, gate_noise(seed, s, i, 1));
+      e1 = noise[(s * N + i) * 2];
+      e2 = noise[(s * N + i) * 2 + 1];
     }
     z[i] = __fadd_rn(__fadd_rn(da, __fmul_rn(db, e1)), __fmul_rn(wc[i], e2));
   }
@@ -154,6 +190,19 @@ __global__ void moe_gate_kernel(const float* __restrict__ feats, int64_t B, int6
   }
 }
 
+qnb_status launch_moe_gate(const float* feats, int64_t batch, int64_t dim, const float* wa, const float* wb,
+                           const float* wc, int64_t n_experts, int64_t top_k, const float* noise, int64_t* idx,
+                           float* weights, int* err, cudaStream_t s) {
+  if (top_k < 1 || top_k > n_experts) return fail(QNB_E_ARG, "top_k out of range");
+  if (n_experts > kMaxExperts) return fail(QNB_E_UNSUPPORTED, "more than 64 experts");
+  if (batch <= 0) return QNB_OK;
+  moe_gate_kernel<<<(unsigned)ceil_div(batch, 128), 128, 0, s>>>(feats, batch, dim, wa, wb, wc, n_experts, top_k,
+                                                                  noise, idx, weights, err);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
 }  // namespace qnb
 
 using namespace qnb;
@@ -162,20 +211,29 @@ extern "C" {
 
 float qnb_gating_expf(float x) { return gate_expf(x); }
 
+float qnb_gating_noise(uint64_t seed, int64_t sample, int64_t expert, int32_t stream) {
+  return host_gating_noise(seed, sample, expert, stream);
+}
+
 qnb_status qnb_moe_gate(const float* feats, int64_t batch, int64_t dim, const float* wa, const float* wb,
                         const float* wc, int64_t n_experts, int64_t top_k, int noise_enabled, uint64_t seed,
                         int64_t* idx, float* weights, qnb_stream s) {
+  return qnb_moe_gate_at(feats, batch, dim, wa, wb, wc, n_experts, top_k, noise_enabled, seed, 0, idx, weights, s);
+}
+
+qnb_status qnb_moe_gate_at(const float* feats, int64_t batch, int64_t dim, const float* wa, const float* wb,
+                           const float* wc, int64_t n_experts, int64_t top_k, int noise_enabled, uint64_t seed,
+                           int64_t sample_offset, int64_t* idx, float* weights, qnb_stream s) {
   QNB_TRY(ensure_device());
   if (top_k < 1 || top_k > n_experts) return fail(QNB_E_ARG, "top_k out of range");
   if (n_experts > kMaxExperts) return fail(QNB_E_UNSUPPORTED, "more than 64 experts");
   if (batch <= 0) return QNB_OK;
+  const float* tab = nullptr;
+  if (noise_enabled) QNB_TRY(guarded([&] { return noise_table(seed, sample_offset, batch, n_experts, &tab); }));
   int* err = nullptr;
   QNB_CUDA(cudaMallocAsync(&err, sizeof(int), as_stream(s)));
   QNB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), as_stream(s)));
-  moe_gate_kernel<<<(unsigned)ceil_div(batch, 128), 128, 0, as_stream(s)>>>(
-      feats, batch, dim, wa, wb, wc, n_experts, top_k, noise_enabled, seed, idx, weights, err);
-  count_launch();
-  QNB_CUDA(cudaGetLastError());
+  QNB_TRY(launch_moe_gate(feats, batch, dim, wa, wb, wc, n_experts, top_k, tab, idx, weights, err, as_stream(s)));
   int h_err = 0;
   QNB_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, as_stream(s)));
   QNB_CUDA(cudaStreamSynchronize(as_stream(s)));

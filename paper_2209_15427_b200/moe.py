@@ -283,9 +283,10 @@ class MoeNet:
         else:
             check(lib.qnb_cast_float(b["T"].data_ptr(), n, p["in_dtype"], L.FP32, b["F"].data_ptr(), sp))
         p["gating"].forward_device(b["F"].data_ptr(), b["feats"].data_ptr(), B, s)
-        check(lib.qnb_moe_gate(b["feats"].data_ptr(), B, p["D"], b["wa"].data_ptr(), b["wb"].data_ptr(),
-                               b["wc"].data_ptr(), self.n_experts, self.top_k, 1 if self.noise else 0,
-                               C.c_uint64(self.seed), b["idx"].data_ptr(), b["w"].data_ptr(), sp))
+        # the gating noise is keyed on the global sample index (rank r holds rows r*B..)
+        check(lib.qnb_moe_gate_at(b["feats"].data_ptr(), B, p["D"], b["wa"].data_ptr(), b["wb"].data_ptr(),
+                                  b["wc"].data_ptr(), self.n_experts, self.top_k, 1 if self.noise else 0,
+                                  C.c_uint64(self.seed), self.rank * B, b["idx"].data_ptr(), b["w"].data_ptr(), sp))
         # one rank: fixed per-expert segments (stride B + BUCKET rows) -> every expert's plan
         # replays a cached CUDA graph at a bucketed batch size, concurrently on its own
         # stream; N ranks: dense rows (the all-to-all splits count real pairs)

@@ -217,16 +217,21 @@ def inner_product(x: np.ndarray, dtype: int, weight: np.ndarray, w_dtype: int, b
     return dy.to_numpy(NP_OF[dtype], (N, out_features))
 
 
+def gating_noise(seed: int, sample: int, expert: int, stream: int) -> float:
+    """gating_noise (src/moe.cpp:53-71), host restatement used for the device table."""
+    return float(L.lib().qnb_gating_noise(seed, sample, expert, stream))
+
+
 def moe_gate(feats: np.ndarray, wa: np.ndarray, wb: np.ndarray, wc: np.ndarray, top_k: int,
-             noise_enabled: bool = False, seed: int = 0):
+             noise_enabled: bool = False, seed: int = 0, sample_offset: int = 0):
     """gating_logits + gating_probs + select_topk per sample (src/moe.cpp:73-144)."""
     B, D = feats.shape
     N = wa.shape[0]
     bufs = [DeviceArray.from_numpy(np.ascontiguousarray(a, dtype=np.float32)) for a in (feats, wa, wb, wc)]
     didx = DeviceArray(B * top_k * 8)
     dw = DeviceArray(B * top_k * 4)
-    check(L.lib().qnb_moe_gate(bufs[0].ptr, B, D, bufs[1].ptr, bufs[2].ptr, bufs[3].ptr, N, top_k,
-                               1 if noise_enabled else 0, seed, didx.ptr, dw.ptr, None))
+    check(L.lib().qnb_moe_gate_at(bufs[0].ptr, B, D, bufs[1].ptr, bufs[2].ptr, bufs[3].ptr, N, top_k,
+                                  1 if noise_enabled else 0, seed, sample_offset, didx.ptr, dw.ptr, None))
     return didx.to_numpy(np.int64, (B, top_k)), dw.to_numpy(np.float32, (B, top_k))
 
 

@@ -321,3 +321,17 @@ def test_glibc_expf_restatement_matches_libm():
     for x in xs:
         a, b = ops.gating_expf(float(x)), libm.expf(float(x))
         assert struct.pack("f", a) == struct.pack("f", b), x
+
+
+def test_host_gating_noise_matches_reference(reference):
+    """qnb_gating_noise (the table the device gate reads) is the reference's
+    gating_noise bit for bit (src/moe.cpp:53-71) over many (seed, sample, expert, stream)."""
+    from paper_2209_15427_b200 import ops
+    rng = np.random.default_rng(9)
+    for seed in (0, 7, 99, 2**63 + 5):
+        for sample in list(range(40)) + [int(v) for v in rng.integers(0, 1 << 40, 40)]:
+            for expert in (0, 3, 15):
+                for stream in (0, 1):
+                    a = ops.gating_noise(seed, sample, expert, stream)
+                    b = reference.gating_noise(seed, sample, expert, stream)
+                    assert struct.pack("f", a) == struct.pack("f", b), (seed, sample, expert, stream)
