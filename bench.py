@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=3)
+    ap.add_argument("--sweep-ck", default="", help="convsweep: comma list of C=K values (default 64,128,256,512)")
     return ap.parse_args()
 
 
@@ -148,7 +149,12 @@ def model_setup(model: str, precision: str):
         params = graphs.synth_params_moe(g)
     else:
         params = graphs.synth_params(g, shapes)
-    with open(os.path.join(ROOT, "tests", "golden", f"{model}_{precision}_calib.json")) as f:
+    # OBSERVE ranges are FP32 statistics, independent of the target precision: every
+    # precision finalizes its grids from the same calibration fixture
+    path = os.path.join(ROOT, "tests", "golden", f"{model}_{precision}_calib.json")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "tests", "golden", f"{model}_int8_calib.json")
+    with open(path) as f:
         ranges = json.load(f)["ranges"]
     return g, shapes, params, ranges
 
@@ -277,6 +283,13 @@ def parity_check(wl, a, ref_prob, T):
     ulp = np.abs(out.view(np.int32).astype(np.int64) - ref_prob.view(np.int32).astype(np.int64))
     res = {"images": T, "rows": f"0..{T - 1} of the timed batch of {wl.B}", "prob_max_ulp": int(ulp.max()),
            "prob_rows_bit_identical": int((ulp.max(axis=1) == 0).sum())}
+    if a.precision in ("fp16", "fp32"):
+        # north_star tolerance for float graphs: max-abs <= 1e-2 x the activation range
+        d = float(np.abs(out.astype(np.float64) - ref_prob.astype(np.float64)).max())
+        rng = float(ref_prob.max() - ref_prob.min())
+        res.update({"prob_max_abs": d, "prob_range": rng, "within_1e-2_of_range": d <= 1e-2 * rng})
+    top1 = (out.argmax(axis=1) == ref_prob.argmax(axis=1)).sum()
+    res["top1_agree"] = int(top1)
     if wl.plan is None or a.precision not in ("int8", "int16"):
         return res
     from oracle import ffi
@@ -296,6 +309,122 @@ def parity_check(wl, a, ref_prob, T):
     res.update({"int8_checkpoint": ck, "checkpoint_values": int(theirs.size),
                 "checkpoint_mismatches": int((mine.reshape(-1) != theirs.reshape(T, per).reshape(-1)).sum())})
     return res
+
+
+SWEEP_CK = (64, 128, 256, 512)
+SWEEP_R = (3, 5, 11)
+SWEEP_S = (1, 2, 4)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def int8_peak_tops(peaks):
+    """Dense int8 tensor peak: the measured kind::i8 figure when the box has one
+    (profiles/int8_peak.json, scripts/int8_peak.py), else 2 x the measured bf16 peak."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
+            m = json.load(f)
+        return float(m["int8_tops"]), f"measured kind::i8 ({m.get('how', 'profiles/int8_peak.json')})"
+    except Exception:
+        return 2.0 * peaks["bf16_tflops"], f"2 x bf16_tflops {peaks['bf16_tflops']} (dense int8 = 2x bf16)"
+
+
+def fp16_peak_tflops(peaks):
+    """Dense fp16 tensor peak: the measured kind::f16 MMA ceiling (profiles/int8_peak.json)
+    when present, else the measured cuBLAS bf16 number (dense fp16 = bf16 on B200)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
+            m = json.load(f)
+        return float(m["fp16_tflops"]), "measured kind::f16 MMA ceiling (profiles/int8_peak.json)"
+    except Exception:
+        return peaks["bf16_tflops"], "MEASURED_PEAKS.json bf16_tflops (dense fp16 = bf16)"
+
+
+def run_convsweep(a):
+    """BASELINE configs[4]: one convolution, N=128 (a.batch), 56x56, C=K in {64..512},
+    R in {3, 5, 11} (pad R//2), stride in {1, 2, 4}, INT8 vs FP16.  Each shape is a
+    compiled two-step plan (input pack + the conv); the conv kernel is timed with CUDA
+    events on the plan's stream (plan.profile), after warm-up, inputs (> L2 for C >= 128)
+    resident in HBM."""
+    import torch
+    from paper_2209_15427_b200 import graph as G
+    from paper_2209_15427_b200 import graphs
+    from paper_2209_15427_b200._lib import QnbError, check, lib
+    from paper_2209_15427_b200.net import QUANTIZED, Net
+    check(lib().qnb_device_check(0))
+    peaks, src = load_peaks()
+    i8_peak, i8_src = int8_peak_tops(peaks)
+    f16_peak, f16_src = fp16_peak_tflops(peaks)
+    N, res = a.batch if a.batch != 256 else 128, 56
+    cks = [int(v) for v in a.sweep_ck.split(",")] if a.sweep_ck else SWEEP_CK
+    rows = []
+    tot = {"int8": [0.0, 0.0], "fp16": [0.0, 0.0]}
+    launches0 = lib().qnb_kernel_launch_count()
+    with ClockSampler(0) as clk:
+        for C in cks:
+            x = (torch.rand((N, C, res, res), device="cuda") * 255.0).contiguous()
+            for R in SWEEP_R:
+                for st in SWEEP_S:
+                    g = graphs.conv_layer(N, C, res, C, R, st)
+                    shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
+                    params = graphs.synth_params(g, shapes)
+                    oh = shapes["conv"][2]
+                    ops_ = 2.0 * N * oh * oh * C * C * R * R
+                    row = {"C": C, "K": C, "R": R, "stride": st, "pad": R // 2, "out": oh, "gop": ops_ / 1e9}
+                    for prec in ("int8", "fp16"):
+                        net = Net(G.override_precision(g, prec))
+                        for k, v in params.items():
+                            net.set_param(k, v)
+                        net.set_range("data", 0.0, 255.0)
+                        net.set_range("conv", -150.0, 150.0)
+                        net.finalize_quantizers()
+                        net.set_quant_mode(QUANTIZED)
+                        try:
+                            plan = net.compile(N, use_cuda_graph=False)
+                        except QnbError as e:
+                            row[prec] = {"unsupported": str(e)[:120]}
+                            continue
+                        out = torch.empty(N * int(np.prod(plan.out_shape[1:])) * 4, dtype=torch.uint8,
+                                          device="cuda")
+                        plan.profile(x.data_ptr(), out.data_ptr(), N, 2, 0)  # warm-up
+                        ms = plan.profile(x.data_ptr(), out.data_ptr(), N, a.profile_reps, 0)
+                        steps = plan.steps()
+                        j = next(i for i, s_ in enumerate(steps) if s_[1] == "igemm")
+                        t = ms[j]
+                        pk = i8_peak if prec == "int8" else f16_peak
+                        tops = ops_ / (t * 1e-3) / 1e12
+                        row[prec] = {"ms": round(t, 4), "tops": round(tops, 1), "frac": round(tops / pk, 3)}
+                        tot[prec][0] += ops_
+                        tot[prec][1] += t
+                        del plan, net, out
+                    rows.append(row)
+                    print(json.dumps(row), file=sys.stderr, flush=True)
+            del x
+            torch.cuda.empty_cache()
+    launches = lib().qnb_kernel_launch_count() - launches0
+    agg = {p: (v[0] / (v[1] * 1e-3) / 1e12 if v[1] else None) for p, v in tot.items()}
+    line = {"metric": "conv TOPS vs int8 tensor peak (single conv-layer sweep, BASELINE configs[4])",
+            "value": agg["int8"], "unit": "TOPS", "n_gpus": 1, "steps": a.profile_reps, "warmup": 2,
+            "ms_per_step": tot["int8"][1], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 (s32 accumulate); f16 (f32 accumulate) alongside", "data": "synthetic U(0,255) input, "
+            "seeded random-init weights",
+            "config": {"workload": f"single conv layer, N={N}, {res}x{res}, C=K in {list(cks)}, R in {list(SWEEP_R)} "
+                                   f"(pad R//2), stride in {list(SWEEP_S)}, INT8 vs FP16",
+                       "parallelism": "dp1 (single GPU)",
+                       "l2": "conv inputs for C >= 128 exceed the 126 MB L2; each step is one launch per shape"},
+            "roofline": {"bound": "tensor", "achieved": agg["int8"], "peak": i8_peak, "unit": "TFLOP/s",
+                         "frac": (agg["int8"] / i8_peak) if agg["int8"] else None, "traffic": None,
+                         "peak_source": i8_src, "kernel": "igemm (all sweep shapes, ops-weighted)"},
+            "fp16": {"tops": agg["fp16"], "peak": f16_peak, "peak_source": f16_src,
+                     "frac": (agg["fp16"] / f16_peak) if agg["fp16"] else None},
+            "e2e": None, "gpu_launches": int(launches), "clocks": clk.summary(), "per_shape": rows}
+    print(json.dumps(line))
 
 
 def run_qnb(a):
@@ -368,15 +497,12 @@ def run_qnb(a):
     torch.cuda.synchronize()
     h2d_ms = e0.elapsed_time(e1) / a.steps
 
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-        peak_src = "measured"
-    except Exception:
-        peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
-        peak_src = "fallback"
-    int8_peak = 2.0 * peaks["bf16_tflops"]  # dense int8 = 2x dense bf16 on B200
+    peaks, peak_src = load_peaks()
+    int8_peak, int8_src = int8_peak_tops(peaks)
+    # FP16 / FP32 graphs run kind::f16 / kind::tf32: their contractions are reported
+    # against the measured dense fp16 (= bf16) peak
+    f16_peak, f16_src = fp16_peak_tflops(peaks)
+    mma_peak = int8_peak if a.precision in ("int8", "int16") else f16_peak
     hbm_peak = peaks["hbm_gbs"]
     per_layer, roof, conv_tops = [], None, None
     if wl.plan is not None:
@@ -398,8 +524,9 @@ def run_qnb(a):
         li, kind, ops_, by = steps_info[dom]
         t = ms_steps[dom]
         if kind == "igemm":
-            roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": int8_peak, "unit": "TFLOP/s",
-                    "op_type": "int8 tensor ops (2 per u8 x u8 MAC), i.e. TOPS",
+            roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": mma_peak, "unit": "TFLOP/s",
+                    "op_type": ("int8 tensor ops (2 per u8 x u8 MAC), i.e. TOPS" if a.precision in ("int8", "int16")
+                                else f"{a.precision} flops (2 per MAC)"),
                     "kernel": f"igemm {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
         else:
             roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -418,7 +545,7 @@ def run_qnb(a):
                 roof["algorithmic_bytes"] = alg
         except Exception:
             pass
-        roof["peak_source"] = (f"{peak_src}: 2 x bf16_tflops {peaks['bf16_tflops']} (dense int8 = 2x bf16)"
+        roof["peak_source"] = ((int8_src if a.precision in ("int8", "int16") else f16_src)
                                if kind == "igemm" else f"{peak_src}: hbm_gbs")
         conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
 
@@ -463,8 +590,10 @@ def run_qnb(a):
                         "h2d_bytes_per_step": int(wl.x_host.nbytes), "d2h_bytes_per_step": int(B * wl.n_out * 4),
                         "h2d_only_ms": h2d_ms, "pcie_bound_images_per_s": B / (h2d_ms / 1e3)},
                 "gpu_launches": int(launches), "kernels_per_forward": wl.kernels,
-                "roofline": roof, "conv_tops": conv_tops, "conv_frac_of_int8_peak":
-                    (conv_tops / int8_peak if conv_tops else None),
+                "roofline": roof, "conv_tops": conv_tops, "conv_frac_of_peak":
+                    (conv_tops / mma_peak if conv_tops else None),
+                "conv_frac_of_spec_peak": (conv_tops / (4500.0 if a.precision in ("int8", "int16") else 2250.0)
+                                           if conv_tops else None),
                 "cpu_baseline": cpu, "parity": parity, "clocks": clk.summary(), "per_layer": per_layer}
         if wl.moe:
             line["moe_expert_counts_last_step"] = [int(c) for c in wl.net.last_stats["counts"]] \
@@ -479,6 +608,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.model == "convsweep":
+        run_convsweep(a)
     else:
         run_qnb(a)
 

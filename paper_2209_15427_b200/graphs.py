@@ -180,6 +180,15 @@ def alexnet_moe(batch: int = 1, dtype: str = "int8", n_experts: int = 16, top_k:
     return {"name": "alexnet_moe", "layers": L}
 
 
+def conv_layer(batch: int = 128, channels: int = 64, res: int = 56, out_channels: int = 64, k: int = 3,
+               stride: int = 1, pad: int = -1) -> dict:
+    """One convolution (BASELINE configs[4]: the single conv-layer sweep, C/K 64-512,
+    3x3/5x5/11x11, stride 1/2/4 at 56x56).  pad defaults to k // 2."""
+    p = k // 2 if pad < 0 else pad
+    L = [_input("data", [batch, channels, res, res]), _conv("conv", "data", out_channels, k, stride, p)]
+    return {"name": f"conv_c{channels}_k{out_channels}_r{k}_s{stride}", "layers": L}
+
+
 MODELS = {"alexnet": alexnet, "vgg16": vgg16, "lenet5": lenet5,
           "vgg16_32": lambda batch=1: vgg16(batch, res=32)}
 
