@@ -870,6 +870,7 @@ qnb_status emit(qnb_plan& P) {
         a.a_n = lr.lrn_alpha / (double)lr.lrn_local_size;
         a.beta = lr.lrn_beta;
         a.k = lr.lrn_k;
+        a.exact_float = (P.flags & QNB_PLAN_EXACT_FLOAT) ? 1 : 0;
         break;
       }
       case OP_CONVERT: {

@@ -10,6 +10,7 @@
 //   softmax_rows   [dequant ->] softmax over rows (src/ops.cpp:445-467)
 //   unpack         NHWC -> NCHW for sinks
 #include <cuda_fp16.h>
+#include <algorithm>
 #include <cstdlib>
 
 #include "qnb_device.cuh"
@@ -336,6 +337,42 @@ __global__ void pool_u8_kernel(const uint8_t* __restrict__ src, DevLayout S, uin
           m[3].add(v.w);
         }
       }
+    }
+    *reinterpret_cast<uint4*>(at(dst, D, n, oy, ox) + ch * 16) =
+        make_uint4(m[0].get(), m[1].get(), m[2].get(), m[3].get());
+  }
+}
+
+// pool_u8 for a compile-time window: floor-mode pooling without padding never leaves
+// the input ((out - 1) * s + k <= in), so all K*K 16-byte loads of a thread are issued
+// before the first max (the generic loop's bounds checks serialised them).
+template <int K>
+__global__ void __launch_bounds__(256) pool_u8_k_kernel(const uint8_t* __restrict__ src, DevLayout S,
+                                                        uint8_t* __restrict__ dst, DevLayout D, int st) {
+  const int chunks = (int)(S.c_phys / 16);
+  const int total = (int)(D.n * D.h * D.w * chunks);  // host checks < 2^31
+  const int Dw = (int)D.w, Dh = (int)D.h;
+  const int srow = (int)S.row, spix = (int)S.pix;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int ch = i % chunks, pix = i / chunks;
+    const int ox = pix % Dw, t = pix / Dw, oy = t % Dh, n = t / Dh;
+    const uint8_t* wp = at(src, S, n, (int64_t)oy * st, (int64_t)ox * st) + ch * 16;
+    uint4 v[K * K];
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) v[ky * K + kx] = __ldg(reinterpret_cast<const uint4*>(wp + ky * srow + kx * spix));
+    MaxU8x4 m[4];
+    m[0].init(v[0].x);
+    m[1].init(v[0].y);
+    m[2].init(v[0].z);
+    m[3].init(v[0].w);
+#pragma unroll
+    for (int j = 1; j < K * K; ++j) {
+      m[0].add(v[j].x);
+      m[1].add(v[j].y);
+      m[2].add(v[j].z);
+      m[3].add(v[j].w);
     }
     *reinterpret_cast<uint4*>(at(dst, D, n, oy, ox) + ch * 16) =
         make_uint4(m[0].get(), m[1].get(), m[2].get(), m[3].get());
@@ -672,6 +709,195 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
   }
 }
 
+// Register-resident pool + LRN (local_size 5), C = 16 * CH channels, any storage types
+// (IT / OT: QNB_FP32, QNB_FP16, QNB_INT8Q, QNB_INT16Q).  Lane (pixel slot, 16-channel
+// chunk): the CH lanes of one output pixel are adjacent in the warp (32 / CH pixels per
+// warp), so the two channels below and above a chunk that the 5-wide window needs come
+// from the neighbouring lanes by shuffle -- no shared-memory staging, no block barriers.
+// Per lane: the pool window's 16-byte loads issued together; raw-integer max for
+// quantized inputs (16-bit SIMD for u8), "keep the first unless a later one is strictly
+// greater" for float inputs (src/ops.cpp:344-390); dequantise (u8 through a 256-entry
+// table) / widen to FP32; 16 float LRN evaluations (MUFU lg2/ex2, relative error
+// < 1.1e-6).  Quantized outputs keep that integer unless it lies within 3e-6 relative of
+// a bin edge, where the reference's double formula decides (lrn_exact5): bit-identical.
+// Float outputs (FP16 / FP32 graphs, tolerance 1e-2 x range) take the float value; plans
+// that need the reference's exact FP32 bits (QNB_PLAN_EXACT_FLOAT) use pool_lrn_kernel.
+// Window channels outside [0, C) enter as +0.0: adding +0.0 to the reference's double
+// sum of squares leaves it bit-identical, so the clipped window needs no predicates.
+__device__ __noinline__ int64_t lrn_exact5(float m2, float m1, float x, float p1, float p2, double k, double a_n,
+                                           double beta, DevQ q) {
+  const float e[5] = {m2, m1, x, p1, p2};
+  double sum = 0.0;
+#pragma unroll
+  for (int d = 0; d < 5; ++d) sum = __dadd_rn(sum, __dmul_rn((double)e[d], (double)e[d]));
+  const double b = __dadd_rn(k, __dmul_rn(a_n, sum));
+  return qz(__double2float_rn(__ddiv_rn((double)x, pow(b, beta))), q);
+}
+
+template <int T>
+struct LrnIo {
+  static constexpr int es = T == QNB_FP32 ? 4 : (T == QNB_INT8Q ? 1 : 2);
+  static constexpr int vecs = es;  // 16-byte vectors per 16 channels
+};
+
+template <int PK, int CH, int IT, int OT>
+__global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_t total_pix) {
+  __shared__ float lut[256];
+  if constexpr (IT == QNB_INT8Q) {
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dq(v, a.in_q);
+    __syncthreads();
+  }
+  constexpr int PPW = 32 / CH;  // output pixels per warp
+  constexpr int IV = LrnIo<IT>::vecs, OV = LrnIo<OT>::vecs;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / CH, ch = lane - sub * CH;
+  const bool lane_on = sub < PPW;
+  const int Dw = (int)a.D.w, Dhw = (int)(a.D.h * a.D.w);
+  const int st = PK > 0 ? (int)a.pool_s : 1;
+  const int srow = (int)a.S.row, spix = (int)a.S.pix;
+  const float fa_n = (float)a.a_n, fk = (float)a.k, nbeta = -(float)a.beta, finv = (float)(1.0 / a.out_q.scale);
+  const float zf = (float)a.out_q.zero;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = gw * PPW; base < total_pix; base += nw * PPW) {
+    const int pix = (int)base + sub;
+    const bool ok = lane_on && pix < total_pix;
+    float x[16];
+    if (ok) {
+      const int n = pix / Dhw, rem = pix - n * Dhw, oy = rem / Dw, ox = rem - oy * Dw;
+      const uint8_t* wp = at(a.src, a.S, n, (int64_t)oy * st, (int64_t)ox * st) + ch * 16 * LrnIo<IT>::es;
+      constexpr int W = PK > 0 ? PK * PK : 1;
+      uint4 v[W][IV];
+#pragma unroll
+      for (int ky = 0; ky < (PK > 0 ? PK : 1); ++ky)
+#pragma unroll
+        for (int kx = 0; kx < (PK > 0 ? PK : 1); ++kx)
+#pragma unroll
+          for (int u = 0; u < IV; ++u)
+            v[ky * (PK > 0 ? PK : 1) + kx][u] =
+                __ldg(reinterpret_cast<const uint4*>(wp + ky * srow + kx * spix) + u);
+      if constexpr (IT == QNB_INT8Q) {
+        MaxU8x4 m[4];
+        m[0].init(v[0][0].x);
+        m[1].init(v[0][0].y);
+        m[2].init(v[0][0].z);
+        m[3].init(v[0][0].w);
+#pragma unroll
+        for (int i = 1; i < W; ++i) {
+          m[0].add(v[i][0].x);
+          m[1].add(v[i][0].y);
+          m[2].add(v[i][0].z);
+          m[3].add(v[i][0].w);
+        }
+#pragma unroll
+        for (int b = 0; b < 16; ++b) x[b] = lut[(m[b >> 2].get() >> (8 * (b & 3))) & 0xFFu];
+      } else if constexpr (IT == QNB_INT16Q) {
+        uint32_t w[8];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          w[4 * u] = v[0][u].x;
+          w[4 * u + 1] = v[0][u].y;
+          w[4 * u + 2] = v[0][u].z;
+          w[4 * u + 3] = v[0][u].w;
+        }
+#pragma unroll
+        for (int i = 1; i < W; ++i)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            w[4 * u] = __vmaxu2(w[4 * u], v[i][u].x);
+            w[4 * u + 1] = __vmaxu2(w[4 * u + 1], v[i][u].y);
+            w[4 * u + 2] = __vmaxu2(w[4 * u + 2], v[i][u].z);
+            w[4 * u + 3] = __vmaxu2(w[4 * u + 3], v[i][u].w);
+          }
+#pragma unroll
+        for (int b = 0; b < 16; ++b) x[b] = dq((int64_t)((w[b >> 1] >> (16 * (b & 1))) & 0xFFFFu), a.in_q);
+      } else {
+        // float storage: the first element stays unless a later one is strictly greater
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+          auto elem = [&](int i) -> float {
+            if constexpr (IT == QNB_FP16) {
+              const uint32_t wv = (&v[i][b >> 3].x)[(b & 7) >> 1];
+              return h2f_bits((uint16_t)(wv >> (16 * (b & 1))));
+            } else {
+              return __uint_as_float((&v[i][b >> 2].x)[b & 3]);
+            }
+          };
+          float m = elem(0);
+#pragma unroll
+          for (int i = 1; i < W; ++i) {
+            const float f = elem(i);
+            m = f > m ? f : m;
+          }
+          x[b] = m;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 16; ++b) x[b] = 0.0f;
+    }
+    // the window's neighbours from the adjacent chunks of the same pixel
+    float m2 = __shfl_up_sync(0xffffffffu, x[14], 1), m1 = __shfl_up_sync(0xffffffffu, x[15], 1);
+    float p1 = __shfl_down_sync(0xffffffffu, x[0], 1), p2 = __shfl_down_sync(0xffffffffu, x[1], 1);
+    if (ch == 0) m2 = m1 = 0.0f;
+    if (ch == CH - 1) p1 = p2 = 0.0f;
+    if (!ok) continue;
+    float e[20], sq[20];
+    e[0] = m2;
+    e[1] = m1;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) e[2 + b] = x[b];
+    e[18] = p1;
+    e[19] = p2;
+#pragma unroll
+    for (int b = 0; b < 20; ++b) sq[b] = __fmul_rn(e[b], e[b]);
+    uint32_t packed[4 * OV];
+#pragma unroll
+    for (int i = 0; i < 4 * OV; ++i) packed[i] = 0;
+    uint32_t slow = 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float sf = __fadd_rn(__fadd_rn(__fadd_rn(sq[c], sq[c + 1]), __fadd_rn(sq[c + 2], sq[c + 3])), sq[c + 4]);
+      const float bse = __fmaf_rn(fa_n, sf, fk);
+      const float rden = ex2_ftz(__fmul_rn(nbeta, lg2_ftz(bse)));
+      if constexpr (OT == QNB_INT8Q || OT == QNB_INT16Q) {
+        const float t = __fmul_rn(__fmul_rn(e[c + 2], rden), finv);
+        const float r = rintf(t);
+        slow |= (fabsf(__fsub_rn(t, r)) < __fsub_rn(0.5f, __fmaf_rn(3e-6f, fabsf(t), 1e-6f)) ? 0u : 1u) << c;
+        if constexpr (OT == QNB_INT8Q) {
+          packed[c >> 2] |= sat_u8(r + zf) << (8 * (c & 3));  // INT8Q grid: i_min 0, i_max 255
+        } else {
+          const uint32_t q = (uint32_t)fminf(fmaxf(r + zf, 0.0f), 65535.0f);  // INT16Q grid
+          packed[c >> 1] |= q << (16 * (c & 1));
+        }
+      } else {
+        const float y = __fmul_rn(e[c + 2], rden);
+        if constexpr (OT == QNB_FP16) packed[c >> 1] |= (uint32_t)f2h_bits(y) << (16 * (c & 1));
+        else packed[c] = __float_as_uint(y);
+      }
+    }
+    if constexpr (OT == QNB_INT8Q || OT == QNB_INT16Q) {
+      if (slow) {  // rare: the reference's exact double arithmetic decides
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          if (!((slow >> c) & 1u)) continue;
+          const uint32_t qv =
+              (uint32_t)lrn_exact5(e[c], e[c + 1], e[c + 2], e[c + 3], e[c + 4], a.k, a.a_n, a.beta, a.out_q);
+          if constexpr (OT == QNB_INT8Q)
+            packed[c >> 2] = (packed[c >> 2] & ~(0xFFu << (8 * (c & 3)))) | ((qv & 0xFFu) << (8 * (c & 3)));
+          else
+            packed[c >> 1] = (packed[c >> 1] & ~(0xFFFFu << (16 * (c & 1)))) | ((qv & 0xFFFFu) << (16 * (c & 1)));
+        }
+      }
+    }
+    const int n = pix / Dhw, rem = pix - n * Dhw, oy = rem / Dw, ox = rem - oy * Dw;
+    uint4* dst = reinterpret_cast<uint4*>(at(a.dst, a.D, n, oy, ox) + ch * 16 * LrnIo<OT>::es);
+#pragma unroll
+    for (int u = 0; u < OV; ++u)
+      dst[u] = make_uint4(packed[4 * u], packed[4 * u + 1], packed[4 * u + 2], packed[4 * u + 3]);
+  }
+}
+
 // ---------------------------------------------------------------- convert
 // Generic elementwise op between layouts (interior, real channels only).
 __global__ void convert_kernel(ConvertArgs a) {
@@ -863,6 +1089,17 @@ void launch_pack_input(const PackArgs& p, cudaStream_t s) {
 void launch_pool(const PoolArgs& p, cudaStream_t s) {
   if (p.dtype == QNB_INT8Q && p.S.c_phys % 16 == 0 && p.D.c_phys == p.S.c_phys && p.S.c == p.S.c_phys &&
       p.S.pix % 16 == 0 && p.D.pix % 16 == 0 && p.S.origin % 16 == 0 && p.D.origin % 16 == 0 && p.S.row % 16 == 0 &&
+      p.D.row % 16 == 0 && p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16) < (int64_t(1) << 31) &&
+      (p.k == 2 || p.k == 3) && (p.D.h - 1) * p.s + p.k <= p.S.h && (p.D.w - 1) * p.s + p.k <= p.S.w &&
+      p.S.img < (int64_t(1) << 31) && !p.S.pslot && !p.D.pslot) {
+    const int64_t work = p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(work, 256), 148 * 8);
+    if (p.k == 3) pool_u8_k_kernel<3><<<blocks, 256, 0, s>>>(p.src, p.S, p.dst, p.D, (int)p.s);
+    else pool_u8_k_kernel<2><<<blocks, 256, 0, s>>>(p.src, p.S, p.dst, p.D, (int)p.s);
+    return;
+  }
+  if (p.dtype == QNB_INT8Q && p.S.c_phys % 16 == 0 && p.D.c_phys == p.S.c_phys && p.S.c == p.S.c_phys &&
+      p.S.pix % 16 == 0 && p.D.pix % 16 == 0 && p.S.origin % 16 == 0 && p.D.origin % 16 == 0 && p.S.row % 16 == 0 &&
       p.D.row % 16 == 0 && p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16) < (int64_t(1) << 31)) {
     pool_u8_kernel<<<blocks_for(p.D.n * p.D.h * p.D.w * (p.S.c_phys / 16), 256), 256, 0, s>>>(p.src, p.S, p.dst, p.D,
                                                                                             p.k, p.s);
@@ -896,6 +1133,46 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
                   a.S.origin % 16 == 0 && a.D.pix % 4 == 0 && a.D.row % 4 == 0 && a.D.img % 4 == 0 &&
                   a.D.origin % 4 == 0;
   // windows never leave the input: (out-1)*s + k <= in for floor-mode pooling
+  const int64_t CH = a.D.c / 16;
+  const bool float_out = a.out_dtype == QNB_FP32 || a.out_dtype == QNB_FP16;
+  const int ies = (int)dtype_size(a.in_dtype), oes = (int)dtype_size(a.out_dtype);
+  const bool v2 = a.half == 2 && (a.pool_k == 3 || a.pool_k == 0) && a.D.c == a.D.c_phys && a.S.c == a.D.c &&
+                  (!float_out || !a.exact_float) && a.S.pix % 16 == 0 && a.S.row % 16 == 0 &&
+                  a.S.img % 16 == 0 && a.S.origin % 16 == 0 && (a.S.c_phys * ies) % 16 == 0 &&
+                  a.D.pix % 16 == 0 && a.D.row % 16 == 0 && a.D.img % 16 == 0 && a.D.origin % 16 == 0 &&
+                  a.D.c % 16 == 0 && a.D.n * a.D.h * a.D.w < (int64_t(1) << 31) &&
+                  (CH == 6 || CH == 16 || CH == 8 || CH == 4) &&
+                  (a.pool_k == 0 || ((a.D.h - 1) * a.pool_s + 3 <= a.S.h && (a.D.w - 1) * a.pool_s + 3 <= a.S.w)) &&
+                  !std::getenv("QNB_LRN_V1");
+  (void)oes;
+  if (v2) {
+    const int32_t total = (int32_t)(a.D.n * a.D.h * a.D.w);
+    const int64_t ppb = 8 * (32 / CH);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(total, ppb), 148 * 3);
+#define QNB_PLV2_T(PK, C_, IT, OT) pool_lrn5_kernel<PK, C_, IT, OT><<<blocks, 256, 0, s>>>(a, total)
+#define QNB_PLV2_IO(PK, C_)                                                                         \
+  do {                                                                                              \
+    if (a.in_dtype == QNB_INT8Q && a.out_dtype == QNB_INT8Q) QNB_PLV2_T(PK, C_, QNB_INT8Q, QNB_INT8Q); \
+    else if (a.in_dtype == QNB_INT16Q) QNB_PLV2_T(PK, C_, QNB_INT16Q, QNB_INT16Q);                  \
+    else if (a.in_dtype == QNB_FP16) QNB_PLV2_T(PK, C_, QNB_FP16, QNB_FP16);                        \
+    else QNB_PLV2_T(PK, C_, QNB_FP32, QNB_FP32);                                                    \
+  } while (0)
+#define QNB_PLV2(PK)                          \
+  do {                                        \
+    if (CH == 6) QNB_PLV2_IO(PK, 6);          \
+    else if (CH == 16) QNB_PLV2_IO(PK, 16);   \
+    else if (CH == 8) QNB_PLV2_IO(PK, 8);     \
+    else QNB_PLV2_IO(PK, 4);                  \
+  } while (0)
+    if (a.in_dtype == a.out_dtype) {
+      if (a.pool_k == 3) QNB_PLV2(3);
+      else QNB_PLV2(0);
+      return;
+    }
+#undef QNB_PLV2
+#undef QNB_PLV2_IO
+#undef QNB_PLV2_T
+  }
   if (q8 && (a.pool_k == 3 || a.pool_k == 2 || a.pool_k == 0)) {
     static int env_pix = [] {
       const char* e = std::getenv("QNB_LRN_PIX");

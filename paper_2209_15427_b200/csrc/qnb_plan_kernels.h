@@ -74,6 +74,7 @@ struct PoolLrnArgs {
   int64_t half;
   double a_n, beta, k;
   int32_t pix;  // output pixels per block (pool_lrn_q8); set by launch_pool_lrn
+  int32_t exact_float;  // float outputs must carry the reference's exact FP32 bits
 };
 
 enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3, CVT_PSEUDO = 4 };

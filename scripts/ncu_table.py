@@ -28,7 +28,7 @@ def get(r, k):
 
 names = ["data", "conv1", "pool1", "conv2", "pool2", "conv3", "conv4", "conv5", "pool5", "fc6", "fc6_finalize",
          "fc7", "fc7_finalize", "fc8", "fc8_finalize", "fc8_to_fp32"]
-lines = ["| layer | kernel | us | dram read MB | dram write MB | tensor % | dram % | SM % |",
+lines = ["| layer | kernel | us | dram read MB | dram write MB | UMMA dense % | dram % | SM % |",
          "|---|---|---|---|---|---|---|---|"]
 traffic = {}
 for name, r in zip(names, data):
@@ -40,7 +40,13 @@ for name, r in zip(names, data):
         us *= 1000.0
     rd = get(r, "dram__bytes_read.sum")
     wr = get(r, "dram__bytes_write.sum")
-    ten = get(r, "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed")
+    # tcgen05 UMMA utilisation: ncu's utcimma / utchmma op counters are normalised to the
+    # 2:4-sparse peak; x2 gives the dense fraction (validated: scripts/int8_peak.cu's
+    # back-to-back MMA kernel reads 49.9 % -> 99.8 %, profiles/ncu/r2b_umma_counter_validation.csv).
+    # (sm__pipe_tensor_cycles_active does not count tcgen05 work.)
+    ten = 2 * max(get(r, "sm__ops_path_tensor_op_utcimma_src_int8_realtime.avg.pct_of_peak_sustained_elapsed"),
+                  get(r, "sm__ops_path_tensor_op_utchmma_src_fp16_dst_fp32_realtime.avg.pct_of_peak_sustained_elapsed"),
+                  0.0)
     dr = get(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")
     sm = get(r, "sm__throughput.avg.pct_of_peak_sustained_elapsed")
     # units: ncu reports bytes in the unit row (byte / Kbyte / Mbyte)
