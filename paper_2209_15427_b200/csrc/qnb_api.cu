@@ -375,7 +375,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
       std::fclose(f);
     }
   }
-  if (a.ksplit > 1) QNB_TRY(igemm_finalize(a, s));
+  // (a split-K launch runs its own igemm_finalize pass inside igemm_launch)
   if (unpack_nchw) QNB_TRY(launch_nhwc_to_nchw(yout, dtype, out_layout, y, s));
   // Temporaries are released stream-ordered; host vectors must outlive the async copies.
   QNB_CUDA(cudaStreamSynchronize(s));

@@ -111,6 +111,15 @@ __device__ __forceinline__ void tma_im2col_4d(void* smem_dst, const CUtensorMap*
       : "memory");
 }
 
+// TMA tile load of a 2-D tensor box at (c0, c1); completes on `bar`.
+__device__ __forceinline__ void tma_tile_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 // TMA tile load of a 3-D tensor box at (c0, c1, c2); completes on `bar`.
 __device__ __forceinline__ void tma_tile_3d(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {

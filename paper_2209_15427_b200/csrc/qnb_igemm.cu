@@ -242,6 +242,82 @@ __device__ __noinline__ void splitk_fixup(const IgemmArgs& p, int64_t mt, int nt
   if (et == 0) *sema = 0;  // self-reset (graph replays reuse the counters)
 }
 
+// Parallel fused split-K (IgemmArgs::ks_fused): every CTA of the tile's K-split group
+// has written its s32 partial; one thread per CTA announces it and waits (all CTAs of
+// the launch are co-resident, host-checked) until the tile's ksplit partials are in, then
+// the CTA reduces rows [ks * rows / ksplit, (ks + 1) * rows / ksplit) of the tile (exact
+// integer adds, L2 reads) and applies the INT8 epilogue to them.  The last CTA to finish
+// resets both counters for the next launch.  Replaces the separate igemm_finalize pass.
+__device__ __noinline__ void splitk_reduce_par(const IgemmArgs& p, int64_t mt, int nt, int ks, const Q8Consts& k) {
+  const int et = threadIdx.x - 5 * 32;  // 0 .. 255 across the epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  int32_t* sema = p.tile_sema + mt * p.n_tiles + nt;
+  int32_t* done = p.tile_done + mt * p.n_tiles + nt;
+  if (et == 0) {
+    __threadfence();
+    atomicAdd(sema, 1);
+    int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(sema) : "memory");
+      if (v >= p.ksplit) break;
+      __nanosleep(64);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  const int n0 = nt * p.n_per_tile;
+  const int n_here = min(p.n_per_tile, p.n_real - n0);
+  const int quads = (n_here + 3) >> 2;
+  const int64_t row_stride = (int64_t)p.n_tiles * p.n_rows;
+  const int64_t split_stride = p.m_total * row_stride;
+  const int64_t r0 = mt * kBM;
+  const int rows = (int)(p.m_total - r0 < kBM ? p.m_total - r0 : kBM);
+  const int lo = (int)((int64_t)rows * ks / p.ksplit), hi = (int)((int64_t)rows * (ks + 1) / p.ksplit);
+  for (int i = et; i < (hi - lo) * quads; i += kEpiWarps * 32) {
+    const int rr = lo + i / quads, j = (i % quads) * 4;
+    const int64_t row = r0 + rr;
+    const int32_t* w = p.ws + row * row_stride + (int64_t)nt * p.n_rows;
+    int32_t d[4] = {0, 0, 0, 0};
+    int32_t rs = 0;
+    for (int s = 0; s < p.ksplit; ++s) {
+      const int32_t* wsp = w + s * split_stride;
+      const int4 v = __ldcg(reinterpret_cast<const int4*>(wsp + j));
+      d[0] += v.x;
+      d[1] += v.y;
+      d[2] += v.z;
+      d[3] += v.w;
+      rs += __ldcg(wsp + p.ones_col);
+    }
+    const int o0 = n0 + j;
+    uint8_t* dst = p.out + row * p.o_img + p.o_origin + o0;  // inner product: oh = ow = 1
+    uint32_t packed = 0;
+    const int cnt = min(4, p.n_real - o0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u >= cnt) break;
+      int64_t q;
+      if (p.fast_rq && p.chan_const32) {
+        q = q8_fast<false, 0>(d[u] + p.chan_const32[o0 + u] + (int32_t)(-p.zw * rs), k, ReluFastK{});
+      } else {
+        q = requant_clamp((int64_t)d[u] + p.chan_const[o0 + u] - p.zw * (int64_t)rs, p.rq);
+      }
+      if (p.has_relu) q = p.relu_lut ? (int64_t)p.relu_lut[q] : relu_requant(q, p.relu);
+      packed |= ((uint32_t)q & 0xFFu) << (8 * u);
+    }
+    if (cnt == 4 && ((uintptr_t)dst & 3) == 0) {
+      *reinterpret_cast<uint32_t*>(dst) = packed;
+    } else {
+      for (int u = 0; u < cnt; ++u) dst[u] = (uint8_t)(packed >> (8 * u));
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  if (et == 0) {
+    if (atomicAdd(done, 1) == p.ksplit - 1) {  // every CTA of the group is past its wait
+      *sema = 0;
+      *done = 0;
+    }
+  }
+}
+
 // Hands an accumulator buffer back to the MMA issuer (rank 0's barrier in pair mode).
 __device__ __forceinline__ void epi_release(const IgemmArgs& p, uint64_t* bar) {
   if (p.pair) mbar_arrive_cluster_relaxed(bar, 0);
@@ -322,7 +398,8 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
       tc_fence_before();
       __syncwarp();
       if (lane == 0) epi_release(p, &acc_empty[buf]);
-      if (p.tile_sema != nullptr) splitk_fixup(p, mt, c.nt, k, reinterpret_cast<int32_t*>(lut));
+      if (p.ks_fused) splitk_reduce_par(p, mt, c.nt, ks, k);
+      else if (p.tile_sema != nullptr) splitk_fixup(p, mt, c.nt, k, reinterpret_cast<int32_t*>(lut));
       continue;
     }
     if constexpr (MODE == EPIM_Q16) {
@@ -839,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 128u + (stream ? 1u : 0u) + (rank == 0 ? 1u : 0u));
+      mbar_init(&full[i], (p.a_tma2d ? 1u : 128u + (stream ? 1u : 0u)) + (rank == 0 ? 1u : 0u));
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -861,7 +938,36 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   const uint32_t tmem = *tmem_slot;
 
   if (warp != 4) griddep_wait();  // warp 4 first issues the resident weights (independent of it)
-  if (warp < 4) {
+  if (warp < 4 && p.a_tma2d) {
+    // ---------------------------------------------------------------- TMA producer
+    // one thread: per stage a 128 x 128 B tile of the samples' contiguous K bytes (2-D
+    // tensor map, hardware 128B swizzle; rows past the batch and K past the sample are
+    // zero-filled) plus, when streamed, this CTA's half of the B stage
+    if (threadIdx.x == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_a)) : "memory");
+      uint32_t st_ph = 0;
+      int st_s = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        const TileCoord c = tile_of(ct, m_pairs, ntk);
+        const int64_t mt = c.mt * 2 + rank;
+        const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const uint8_t* bsrc =
+            p.b + ((int64_t)(c.g * p.n_tiles + ntile) * p.num_kb) * (p.n_rows * 128) + (int64_t)rank * bh;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int s = st_s;
+          mbar_wait(&empty[s], st_ph ^ 1);
+          if (++st_s == S) {
+            st_s = 0;
+            st_ph ^= 1;
+          }
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(a_stage + (stream ? bh : 0)));
+          tma_tile_2d(sA + (size_t)s * a_stage, &p.tmap_a, kb * 128, (int)(mt * kBM), &full[s]);
+          if (stream) bulk_g2s(sB + (size_t)s * bh, bsrc + (int64_t)kb * p.n_rows * 128, (uint32_t)bh, &full[s]);
+        }
+      }
+    }
+  } else if (warp < 4) {
     // ---------------------------------------------------------------- producers
     const int t = threadIdx.x;
     const int jc = lane & 7, rr = lane >> 3;
@@ -1223,6 +1329,24 @@ qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const u
   return QNB_OK;
 }
 
+qnb_status igemm_encode_tma2d(const uint8_t* base, int64_t rows, int64_t kbytes, int64_t row_stride, CUtensorMap* map) {
+  if ((uintptr_t)base % 16 != 0 || row_stride % 16 != 0 || kbytes % 16 != 0)
+    return fail(QNB_E_UNSUPPORTED, "2-D TMA operand not 16-byte aligned");
+  const cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)row_stride};
+  const cuuint32_t box[2] = {128, (cuuint32_t)kBM};
+  const cuuint32_t estr[2] = {1, 1};
+  using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static const EncodeTiled encode = driver_fn<EncodeTiled>("cuTensorMapEncodeTiled");
+  if (!encode) return fail(QNB_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(QNB_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return QNB_OK;
+}
 
 // ---------------------------------------------------------------- patch kernel
 // Stride-1 convolutions (AlexNet conv2-5, VGG-16): see IgemmArgs::patch.
@@ -1873,6 +1997,49 @@ qnb_status igemm_finalize(const IgemmArgs& a, cudaStream_t s) {
   return QNB_OK;
 }
 
+static int num_sms();
+template <int KIND>
+__global__ void igemm_pair_kernel(const __grid_constant__ IgemmArgs p);
+
+// Parallel fused split-K needs every (m-pair, n-tile, k-split) tile on its own CTA pair
+// and all pairs resident at once (the K-split CTAs of a tile wait for each other).
+static bool pair_fused_fits(const IgemmArgs& a, int64_t groups, int sstages) {
+  const int64_t m_tiles = ceil_div(a.m_total, kBM);
+  const int64_t ptiles = ceil_div(m_tiles, 2) * a.n_tiles * a.ksplit * groups;
+  if (ptiles > num_sms() / 2) return false;
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(num_sms() & ~1));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 227 * 1024;  // the pair kernel's attribute maximum (one CTA per SM)
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaFuncSetAttribute(igemm_pair_kernel<KIND_I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(igemm_pair_kernel<KIND_I8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, igemm_pair_kernel<KIND_I8>, &cfg) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    max_clusters = n;
+  }
+  (void)sstages;
+  return ptiles <= max_clusters;
+}
+
+bool igemm_splitk_fused_ok(const IgemmArgs& a, int64_t groups) {
+  IgemmArgs b = a;
+  if (b.ksplit <= 1 || b.tile_sema == nullptr || b.tile_done == nullptr) return false;
+  if (std::getenv("QNB_NO_PAIR") || std::getenv("QNB_NO_PAIR_STREAM") || std::getenv("QNB_NO_FUSED_SPLITK"))
+    return false;
+  return b.kbytes == 128 && b.n_rows % 16 == 0 && b.n_rows <= 256 && 2 * b.tmem_cols <= 512 &&
+         ceil_div(b.m_total, kBM) >= 2 && pair_fused_fits(b, groups, 4);
+}
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -2038,6 +2205,8 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
                                                         ((size_t)(kBM + a.n_rows / 2) * 128));
     if (sstages > 6) sstages = 6;
     const bool streamed = shape_ok && !resident && !no_stream && sstages >= 4;
+    if (a.ks_fused && !(streamed && a.epi_mode == EPIM_RAW32 && pair_fused_fits(a, groups, sstages)))
+      a.ks_fused = 0;  // plan asked for it but this launch cannot guarantee co-residency
     if (resident || streamed) {
       a.pair = resident ? stages : sstages;
       a.pair_stream = resident ? 0 : 1;
@@ -2070,6 +2239,7 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
       QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_pair_kernel<KIND>, a));
       count_launch();
       QNB_CUDA(cudaGetLastError());
+      if (a.ksplit > 1 && !a.ks_fused && a.tile_sema == nullptr) QNB_TRY(igemm_finalize(a, s));
       return QNB_OK;
     }
   }
@@ -2091,9 +2261,11 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
   set_pdl(attr[1]);
   cfg.attrs = attr;
   cfg.numAttrs = pdl_on() ? 2 : 1;
+  a.ks_fused = 0;  // the parallel fused split-K runs in the pair kernel only
   QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_kernel<KIND>, a));
   count_launch();
   QNB_CUDA(cudaGetLastError());
+  if (a.ksplit > 1 && a.tile_sema == nullptr) QNB_TRY(igemm_finalize(a, s));
   return QNB_OK;
 }
 

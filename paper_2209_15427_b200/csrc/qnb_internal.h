@@ -137,6 +137,16 @@ struct IgemmArgs {
   // the last CTA of a tile to finish sums the partials and runs the INT8 epilogue, so no
   // separate igemm_finalize launch is needed
   int32_t* tile_sema;
+  // parallel fused split-K (ks_fused = 1, CTA-pair streamed mode, every pair owns exactly
+  // one (m, n, k-split) tile and all pairs are co-resident): each CTA writes its s32
+  // partial, waits until the tile's ksplit partials are in (tile_sema), then reduces and
+  // requantizes its 1/ksplit slice of the tile's rows; tile_done resets the counters.
+  int32_t ks_fused;
+  int32_t* tile_done;
+  // A operand by 2-D TMA (a_tma2d = 1; inner products whose K bytes are contiguous per
+  // sample): one cp.async.bulk.tensor.2d per stage (128 rows x 128 B, 128B swizzle)
+  // replaces the 128-thread cp.async gather.
+  int32_t a_tma2d;
   // CTA-pair mode (igemm_pair_kernel): cta_group::2 MMAs with M = 256 and each CTA's
   // half of B resident in smem for the whole launch.
   int32_t pair;
@@ -244,6 +254,11 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
 // TMA im2col A operand (see IgemmArgs::tmap_a): eligibility, stage list (chunk_off
 // holds {c0, s, r} per stage) and K map; then the tensor map over the activation.
 bool igemm_tma_eligible(const IgemmGeometry& g, const ActLayout& in);
+// True when the CTA-pair kernel can run this split-K contraction with the parallel
+// fused reduction (IgemmArgs::ks_fused) -- then no igemm_finalize launch follows.
+bool igemm_splitk_fused_ok(const IgemmArgs& a, int64_t groups);
+// 2-D tensor map over `rows` samples of `kbytes` contiguous bytes, `row_stride` apart.
+qnb_status igemm_encode_tma2d(const uint8_t* base, int64_t rows, int64_t kbytes, int64_t row_stride, CUtensorMap* map);
 qnb_status igemm_plan_tma(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk);
 qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base, int32_t kbytes,
                             CUtensorMap* map);

@@ -715,13 +715,29 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
       void* ws = nullptr;
       QNB_TRY(dev_alloc(P, &ws, (size_t)a.ksplit * P.max_batch * pk.n_tiles * pk.n_rows * 4));
       a.ws = (int32_t*)ws;
-      if (std::getenv("QNB_FUSED_FIXUP")) {  // opt-in: serial last-CTA fixup (measured slower: 1 CTA reduces a tile)
-        const size_t n_sema = (size_t)ceil_div(P.max_batch, 128) * pk.n_tiles;
-        void* sema = nullptr;
-        QNB_TRY(dev_alloc(P, &sema, n_sema * 4));
-        QNB_CUDA(cudaMemset(sema, 0, n_sema * 4));
-        a.tile_sema = (int32_t*)sema;
+      // parallel fused split-K: per (m-tile, n-tile) arrival and completion counters
+      const size_t n_sema = (size_t)ceil_div(P.max_batch, 128) * pk.n_tiles;
+      void* sema = nullptr;
+      QNB_TRY(dev_alloc(P, &sema, 2 * n_sema * 4));
+      QNB_CUDA(cudaMemset(sema, 0, 2 * n_sema * 4));
+      a.tile_sema = (int32_t*)sema;
+      a.tile_done = (int32_t*)sema + n_sema;
+      a.ks_fused = igemm_splitk_fused_ok(a, g.groups) ? 1 : 0;
+      if (!a.ks_fused && !std::getenv("QNB_FUSED_FIXUP")) {  // serial last-CTA fixup is opt-in only
+        a.tile_sema = nullptr;
+        a.tile_done = nullptr;
       }
+    }
+  }
+  // inner products read each sample's K bytes contiguously: the A stages come from a 2-D
+  // tensor map (one TMA per stage) instead of the 128-thread cp.async gather
+  if (g.is_fc && g.kind == KIND_I8 && !std::getenv("QNB_NO_FC_TMA")) {
+    const int64_t kb_sample = Lin.c_phys * Lin.h * Lin.w * Lin.es();
+    const uint8_t* base = blob_ptr(P, op.in) + a.a_origin;  // the gather's sample origin
+    if (Lin.hh == 0 && Lin.hw == 0 && Lin.pair_slot == 0 && (uintptr_t)base % 16 == 0 && Lin.img() % 16 == 0 &&
+        kb_sample % 16 == 0) {
+      QNB_TRY(igemm_encode_tma2d(base, P.max_batch, kb_sample, Lin.img(), &a.tmap_a));
+      a.a_tma2d = 1;
     }
   }
   a.out = blob_ptr(P, op.out);
@@ -967,13 +983,12 @@ qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cuda
           launch_pack_input(st.pack, s);
           break;
         case OP_IGEMM:
-          QNB_TRY(igemm_launch(st.mma_kind, st.ig, st.groups, s));
-          g_launches.fetch_sub(1);  // counted below with the others
-          if (st.ig.ksplit > 1 && st.ig.tile_sema == nullptr) {
-            QNB_TRY(igemm_finalize(st.ig, s));
-            g_launches.fetch_sub(1);
-          }
+        {
+          const uint64_t l0 = g_launches.load();
+          QNB_TRY(igemm_launch(st.mma_kind, st.ig, st.groups, s));  // + igemm_finalize for unfused split-K
+          g_launches.fetch_sub(g_launches.load() - l0);  // counted below with the others
           break;
+        }
         case OP_FEXACT:
           launch_fexact(st.fx, s);
           break;
@@ -1060,7 +1075,8 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
     QNB_TRY(emit(*P));
     P->launches_per_forward = (int64_t)P->steps.size();
     for (const Step& st : P->steps)
-      if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1 && st.ig.tile_sema == nullptr) ++P->launches_per_forward;
+      if (st.kind == OP_IGEMM && !st.unpack && st.ig.ksplit > 1 && st.ig.tile_sema == nullptr && !st.ig.ks_fused)
+        ++P->launches_per_forward;
     QNB_CUDA(cudaDeviceSynchronize());
     // output description (reference layout)
     const Blob& sk = P->blobs[P->sink_blob];
