@@ -255,7 +255,7 @@ class Workload:
         self.sp = torch.cuda.current_stream().cuda_stream
         if self.moe:
             self.plan = None
-            self.kernels = None
+            self.kernels = net.moe_plan(B).kernels_per_forward() if ws == 1 else None
         else:
             self.plan = net.compile(B)
             self.kernels = self.plan.stats()["kernels_per_forward"]

@@ -277,6 +277,14 @@ qnb_status qnb_plan_create(const qnb_layer_desc* layers, int32_t n_layers, int32
  * call, stream-ordered) or device memory. */
 qnb_status qnb_plan_forward(qnb_plan* plan, const void* input, int64_t batch, int32_t input_on_host,
                             void* output, int32_t output_on_host, qnb_stream s);
+/* Net::forward on a data-dependent batch that lives in DEVICE memory: the plan is
+ * launched at `batch_cap` images and every kernel processes min(batch_cap, *dyn_batch)
+ * of them (GEMM tiles past the batch are skipped by all warp roles), so a routed
+ * sub-batch (an MoE expert's samples) runs without a device->host round trip and the
+ * call can be captured into an enclosing CUDA graph.  Device buffers only; launches
+ * eagerly on `s` (no own graph). */
+qnb_status qnb_plan_forward_dyn(qnb_plan* plan, const void* input_dev, int64_t batch_cap,
+                                const int32_t* dyn_batch, void* output_dev, qnb_stream s);
 /* Sink blob of the plan: its qnb_dtype and reference shape (batch = max_batch). */
 qnb_status qnb_plan_output_info(const qnb_plan* plan, int32_t* dtype, int32_t* ndim,
                                 int64_t shape[4]);
@@ -306,6 +314,61 @@ qnb_status qnb_plan_profile(qnb_plan* plan, const void* input, int64_t batch, vo
 qnb_status qnb_plan_observe(qnb_plan* plan, const void* input, int64_t batch, double* mins, double* maxs,
                             qnb_stream s);
 qnb_status qnb_plan_destroy(qnb_plan* plan);
+
+/* ------------------------------------------------------------------ MoE plan
+ * Net::forward for a chain graph with ONE MOE layer (Net::run_moe src/net.cpp:495-544 +
+ * moe_forward src/moe.cpp:165-252), as one device-driven forward: trunk plan -> MoE
+ * bottom (dequantized) -> gating plan -> gate (gating_logits / probs / select_topk,
+ * src/moe.cpp:73-144) -> per-expert routing -> each expert plan runs on its routed rows
+ * with its sample count read from DEVICE memory (qnb_plan_forward_dyn, PER_SAMPLE
+ * dispatch == ALL_EXPERTS, include/qnet/moe.hpp:28-33) -> combine in selection order ->
+ * quantize to the MoE top grid -> tail plan.  No host round trip: the whole forward is
+ * captured as one CUDA graph (per batch / buffers).  The four sub-graphs are described
+ * exactly as qnb_plan_create takes them: the trunk ends at the MoE bottom blob, the
+ * gating / expert graphs are the nested graphs (LayerSpec::moe, include/qnet/graph.hpp:54-62)
+ * with their own finalized parameters, the tail starts with an INPUT layer producing the
+ * MoE top blob. */
+typedef struct {
+  const qnb_layer_desc* layers;
+  int32_t n_layers;
+  int32_t n_blobs;
+} qnb_graph_desc;
+
+typedef struct {
+  int64_t max_batch;
+  int32_t n_experts, top_k;
+  int32_t noise_enabled;      /* MoeLayerParams::noise_enabled */
+  uint64_t seed;              /* MoeLayerParams::seed */
+  int64_t sample_offset;      /* global index of this call's first sample (gating noise key) */
+  int32_t in_dtype;           /* MoE bottom blob dtype; its grid in in_qv when quantized */
+  qnb_qvals in_qv;
+  int32_t top_dtype;          /* MoE top blob dtype; its grid in top_qv when quantized */
+  qnb_qvals top_qv;
+  int64_t in_per_sample;      /* elements per sample of the MoE bottom (C*H*W) */
+  int64_t out_per_sample;     /* features per sample of the expert output / MoE top */
+  int32_t gate_dim;           /* D: features of the gating sink */
+  const float* gate_a;        /* host N x D, N x D, N  (MoeLayerParams gate matrices) */
+  const float* gate_b;
+  const float* gate_c;
+  int32_t use_cuda_graph;
+} qnb_moe_opts;
+
+typedef struct qnb_moe_plan qnb_moe_plan;
+
+qnb_status qnb_moe_plan_create(const qnb_graph_desc* trunk, const qnb_graph_desc* gating,
+                               const qnb_graph_desc* experts /* [n_experts] */, const qnb_graph_desc* tail,
+                               const qnb_moe_opts* opts, qnb_moe_plan** out);
+/* input: FP32 NCHW batch (host or device); output: the tail sink (host or device). */
+qnb_status qnb_moe_plan_forward(qnb_moe_plan* plan, const void* input, int64_t batch, int32_t input_on_host,
+                                void* output, int32_t output_on_host, qnb_stream s);
+/* Synchronises `s`; the previous forward's per-expert pair counts (host, n_experts) and
+ * QNB_E_ARG "degenerate gating" if a sample's gate probabilities were degenerate
+ * (src/moe.cpp:120-125). */
+qnb_status qnb_moe_plan_status(qnb_moe_plan* plan, int64_t* counts, qnb_stream s);
+/* Device pointer to the MoE top blob of the last forward ([batch][out_per_sample], top dtype). */
+qnb_status qnb_moe_plan_moe_output(const qnb_moe_plan* plan, void** dev_ptr);
+qnb_status qnb_moe_plan_stats(const qnb_moe_plan* plan, int64_t* kernels_per_forward);
+qnb_status qnb_moe_plan_destroy(qnb_moe_plan* plan);
 
 /* ---------------------------------------------------------------- QCNM model store
  * The reference's binary model file (QCNM v1, src/model_store.cpp:123-206;

@@ -93,11 +93,29 @@ class PlanOpts(C.Structure):
     _fields_ = [("max_batch", C.c_int64), ("use_cuda_graph", C.c_int32), ("flags", C.c_int32)]
 
 
+class GraphDesc(C.Structure):
+    """qnb_graph_desc (include/qnb.h)."""
+
+    _fields_ = [("layers", C.POINTER(LayerDesc)), ("n_layers", C.c_int32), ("n_blobs", C.c_int32)]
+
+
+class MoeOpts(C.Structure):
+    """qnb_moe_opts (include/qnb.h)."""
+
+    _fields_ = [("max_batch", C.c_int64), ("n_experts", C.c_int32), ("top_k", C.c_int32),
+                ("noise_enabled", C.c_int32), ("seed", C.c_uint64), ("sample_offset", C.c_int64),
+                ("in_dtype", C.c_int32), ("in_qv", QVals), ("top_dtype", C.c_int32), ("top_qv", QVals),
+                ("in_per_sample", C.c_int64), ("out_per_sample", C.c_int64), ("gate_dim", C.c_int32),
+                ("gate_a", C.c_void_p), ("gate_b", C.c_void_p), ("gate_c", C.c_void_p),
+                ("use_cuda_graph", C.c_int32)]
+
+
 _PLAN_SIGS = {
     "qnb_plan_create": (C.c_int, [C.POINTER(LayerDesc), C.c_int32, C.c_int32, C.POINTER(PlanOpts),
                                   C.POINTER(C.c_void_p)]),
     "qnb_plan_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
                                    C.c_void_p]),
+    "qnb_plan_forward_dyn": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "qnb_plan_output_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int64)]),
     "qnb_plan_blob_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
@@ -106,6 +124,14 @@ _PLAN_SIGS = {
     "qnb_plan_observe": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.c_void_p]),
     "qnb_plan_destroy": (C.c_int, [C.c_void_p]),
+    "qnb_moe_plan_create": (C.c_int, [C.POINTER(GraphDesc), C.POINTER(GraphDesc), C.POINTER(GraphDesc),
+                                      C.POINTER(GraphDesc), C.POINTER(MoeOpts), C.POINTER(C.c_void_p)]),
+    "qnb_moe_plan_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32,
+                                       C.c_void_p]),
+    "qnb_moe_plan_status": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]),
+    "qnb_moe_plan_moe_output": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "qnb_moe_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "qnb_moe_plan_destroy": (C.c_int, [C.c_void_p]),
     "qnb_model_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "qnb_model_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "qnb_model_record": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Record)]),

@@ -266,36 +266,71 @@ __global__ void moe_combine_kernel(const float* __restrict__ eo, int64_t B, int6
 // expert runs on one contiguous sub-batch.  One CTA; thread e owns expert e, so the
 // order is deterministic without atomics.  B*K is small (1024 for AlexNet-MoE).
 constexpr int kRouteMaxExperts = 256;
-__global__ void moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, int64_t K, int64_t E, int64_t pad,
-                                 int64_t* __restrict__ counts, int64_t* __restrict__ pair_sample,
-                                 int64_t* __restrict__ pair_slot) {
-  __shared__ int64_t cnt[kRouteMaxExperts], off[kRouteMaxExperts];
-  const int e = threadIdx.x;
-  if (e < E) {
-    int64_t c = 0;
-    for (int64_t p = 0; p < BK; ++p) c += __ldg(idx + p) == e;
-    cnt[e] = c;
+// Stable grouping of the batch*top_k (sample, expert) pairs per expert, in pair order
+// (PER_SAMPLE dispatch, src/moe.cpp:218-238), by one 1024-thread block: pass 1 counts
+// the pairs of every expert (shared-memory atomics); pass 2 places each chunk of 1024
+// pairs -- a pair's position inside its expert is the expert's running base + the pairs
+// of the same expert in earlier warps of the chunk + its rank among the lanes of its
+// warp that share its expert (__match_any_sync).  pad > 0: expert e owns rows
+// [e*pad, e*pad + pad) and its unused rows get sample -1.
+__global__ void __launch_bounds__(1024) moe_route_kernel(const int64_t* __restrict__ idx, int64_t BK, int64_t K,
+                                                         int64_t E, int64_t pad, int64_t* __restrict__ counts,
+                                                         int32_t* __restrict__ counts32,
+                                                         int64_t* __restrict__ pair_sample,
+                                                         int64_t* __restrict__ pair_slot) {
+  __shared__ int cnt[kRouteMaxExperts], off[kRouteMaxExperts], base[kRouteMaxExperts];
+  __shared__ int wpre[32][kRouteMaxExperts];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < E; e += blockDim.x) {
+    cnt[e] = 0;
+    base[e] = 0;
   }
   __syncthreads();
-  if (e == 0) {
-    int64_t o = 0;
-    for (int64_t i = 0; i < E; ++i) {
-      off[i] = pad > 0 ? i * pad : o;  // pad > 0: fixed per-expert segments of `pad` rows
-      o += cnt[i];
+  for (int64_t p = tid; p < BK; p += blockDim.x) atomicAdd(&cnt[(int)__ldg(idx + p)], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0;
+    for (int e = 0; e < E; ++e) {
+      off[e] = pad > 0 ? (int)(e * pad) : o;
+      o += cnt[e];
     }
   }
-  __syncthreads();
-  if (e < E) {
-    int64_t pos = off[e];
-    for (int64_t p = 0; p < BK; ++p)
-      if (__ldg(idx + p) == e) {
-        pair_sample[pos] = p / K;
-        pair_slot[p] = pos;
-        ++pos;
+  for (int64_t c0 = 0; c0 < BK; c0 += blockDim.x) {
+    for (int i = tid; i < 32 * E; i += blockDim.x) wpre[i / E][i % E] = 0;
+    __syncthreads();
+    const int64_t p = c0 + tid;
+    const int e = p < BK ? (int)__ldg(idx + p) : -1;
+    const uint32_t same = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(same & ((1u << lane) - 1u));
+    if (e >= 0 && rank == 0) wpre[warp][e] = __popc(same);
+    __syncthreads();
+    for (int x = tid; x < E; x += blockDim.x) {  // exclusive prefix over the warps, per expert
+      int run = 0;
+      for (int w = 0; w < 32; ++w) {
+        const int v = wpre[w][x];
+        wpre[w][x] = run;
+        run += v;
       }
-    if (pad > 0)
-      for (int64_t q = pos; q < off[e] + pad; ++q) pair_sample[q] = -1;  // unused rows: the gather skips them
+    }
+    __syncthreads();
+    if (e >= 0) {
+      const int64_t pos = off[e] + base[e] + wpre[warp][e] + rank;
+      pair_sample[pos] = p / K;
+      pair_slot[p] = pos;
+    }
+    __syncthreads();
+    // advance the running bases by this chunk's pairs (the last warp's prefix + its count)
+    if (e >= 0) atomicAdd(&base[e], 1);
+    __syncthreads();
+  }
+  for (int e = tid; e < E; e += blockDim.x) {
     counts[e] = cnt[e];
+    if (counts32) counts32[e] = cnt[e];
+  }
+  if (pad > 0) {
+    __syncthreads();
+    for (int e = 0; e < E; ++e)
+      for (int64_t q = off[e] + cnt[e] + tid; q < off[e] + pad; q += blockDim.x) pair_sample[q] = -1;
   }
 }
 
@@ -427,6 +462,18 @@ ReluRequant to_dev_relu(const qnb_requant& r, int dtype) {
 using namespace qnb;
 
 // ---------------------------------------------------------------- C-ABI ops
+namespace qnb {
+qnb_status launch_moe_route(const int64_t* idx, int64_t BK, int64_t K, int64_t E, int64_t pad, int64_t* counts,
+                            int32_t* counts32, int64_t* pair_sample, int64_t* pair_slot, cudaStream_t s) {
+  if (E < 1 || E > kRouteMaxExperts) return fail(QNB_E_UNSUPPORTED, "1..256 experts supported");
+  if (BK >= (int64_t(1) << 30)) return fail(QNB_E_UNSUPPORTED, "too many routed pairs");
+  moe_route_kernel<<<1, 1024, 0, s>>>(idx, BK, K, E, pad, counts, counts32, pair_sample, pair_slot);
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+}  // namespace qnb
+
 extern "C" {
 
 qnb_status qnb_quantize(const float* x, int64_t n, const qnb_qvals* qv, qnb_dtype dtype, void* out,
@@ -584,10 +631,8 @@ qnb_status qnb_moe_route(const int64_t* idx, int64_t batch, int64_t top_k, int64
   if (top_k < 1 || top_k > n_experts) return fail(QNB_E_ARG, "top_k out of range");
   if (batch < 0) return fail(QNB_E_SHAPE, "shape mismatch");
   if (segment_pad < 0 || (segment_pad > 0 && segment_pad < batch)) return fail(QNB_E_ARG, "segment_pad below batch");
-  moe_route_kernel<<<1, kRouteMaxExperts, 0, as_stream(s)>>>(idx, batch * top_k, top_k, n_experts, segment_pad,
-                                                             counts, pair_sample, pair_slot);
-  count_launch();
-  QNB_CUDA(cudaGetLastError());
+  QNB_TRY(launch_moe_route(idx, batch * top_k, top_k, n_experts, segment_pad, counts, nullptr, pair_sample, pair_slot,
+                           as_stream(s)));
   return QNB_OK;
 }
 

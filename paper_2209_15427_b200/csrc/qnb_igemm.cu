@@ -48,6 +48,10 @@ __host__ __device__ inline size_t igemm_smem_bytes(int n_rows, int kbytes = 128)
          16 + 256 + 2 * 128 * 8 + kMaxChunkSmem * 4;
 }
 
+// Output rows this launch must produce (the device-resident batch clamps m_total).
+__device__ __forceinline__ int64_t m_valid(const IgemmArgs& p) {
+  return p.dyn_n ? min(p.m_total, (int64_t)__ldg(p.dyn_n) * p.dyn_rows) : p.m_total;
+}
 struct TileCoord {
   int64_t mt;
   int nt, g;
@@ -60,6 +64,13 @@ __device__ __forceinline__ TileCoord tile_of(int64_t t, int64_t m_tiles, int n_t
   c.nt = (int)(r % n_tiles);
   c.g = (int)(r / n_tiles);
   return c;
+}
+
+// A (cluster) tile is live when its first output row is below m_valid.  Row-Hankel
+// tiles are (image pair q, output row): live when image 2q is inside the batch.
+__device__ __forceinline__ bool tile_live(const IgemmArgs& p, int64_t cmt, int cs, int64_t mv) {
+  if (p.hk) return 2 * (cmt / p.oh) * (int64_t)p.oh * p.ow < mv;
+  return cmt * cs * kBM < mv;
 }
 
 // requant_clamp when the host proved |acc| < 2^31 and 1 <= s <= 62: the 128-bit
@@ -340,8 +351,11 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
   const int ones_col = p.ones_col, o_es = p.o_es, o_vec = p.o_vec, has_relu = p.has_relu;
   const int64_t zw = p.zw;
   const float slope = p.slope;
-  uint32_t j = 0;
-  for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
+  const int64_t mv = m_valid(p);
+  uint32_t jn = 0;
+  for (int64_t ct = cid; ct < total; ct += ncl) {
+    if (!tile_live(p, ct % m_groups, cs, mv)) continue;
+    const uint32_t j = jn++;
     const TileCoord c0 = tile_of(ct, m_groups, n_tiles * p.ksplit);
     const int ks = c0.nt % p.ksplit;
     TileCoord c = c0;
@@ -681,6 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
   const int64_t m_groups = (m_tiles + cs - 1) / cs;
   const int64_t total = m_groups * p.n_tiles * p.ksplit * p.groups;
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
+  const int64_t mv = m_valid(p);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -712,6 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_a)) : "memory");
       uint32_t it = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_groups, cs, mv)) continue;
         const TileCoord c = tile_of(ct, m_groups, p.n_tiles * p.ksplit);
         const int64_t mt = c.mt * cs + rank;
         const uint32_t row0 = (uint32_t)(mt * kBM);
@@ -746,6 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     const int jc = lane & 7, rr = lane >> 3;
     uint32_t it = 0, par = 0;
     for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
+      if (!tile_live(p, ct % m_groups, cs, mv)) continue;
       const TileCoord c = tile_of(ct, m_groups, p.n_tiles * p.ksplit);
       const int64_t mt = c.mt * cs + rank;
       {  // one row decomposition per thread, shared through smem
@@ -809,8 +826,10 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
       const uint32_t idesc = make_idesc<KIND>(p.n_rows);
       const bool mma_on = !(p.dbg & 2);
       const int nk = kbytes >> 5;
-      uint32_t it = 0, j = 0;
-      for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
+      uint32_t it = 0, jn = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_groups, cs, mv)) continue;
+        const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -913,6 +932,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
     total = idle ? 0 : (g + 1) * m_pairs;
   }
   const int64_t pix_per_img = (int64_t)p.oh * p.ow;
+  const int64_t mv = m_valid(p);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -948,6 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       uint32_t st_ph = 0;
       int st_s = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
         const TileCoord c = tile_of(ct, m_pairs, ntk);
         const int64_t mt = c.mt * 2 + rank;
         const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
@@ -974,6 +995,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
     uint32_t par = 0, st_ph = 0;
     int st_s = 0;
     for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
+      if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
       const TileCoord c = tile_of(ct, m_pairs, ntk);
       const int64_t mt = c.mt * 2 + rank;
       const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
@@ -1047,6 +1069,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       int st_s = 0;
       uint32_t st_ph = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
         const TileCoord c = tile_of(ct, m_pairs, ntk);
         const int ks = c.nt % p.ksplit;
         const int nkb = min(p.num_kb, (ks + 1) * p.kb_per_split) - ks * p.kb_per_split;
@@ -1070,9 +1093,11 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       uint32_t idesc = make_idesc<KIND>(p.n_rows);
       idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24);  // M = 256 (pair)
       const bool mma_on = !(p.dbg & 2);
-      uint32_t j = 0, st_ph = 0;
+      uint32_t jn = 0, st_ph = 0;
       int st_s = 0;
-      for (int64_t ct = cid; ct < total; ct += ncl, ++j) {
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait_cluster(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -1159,6 +1184,7 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
   uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t total = (int64_t)p.hk_pairs * p.oh;  // tile = (image pair, output row)
+  const int64_t mv = m_valid(p);
 
   if (threadIdx.x == 0) {
     mbar_init(b_full, 1);
@@ -1189,8 +1215,10 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
     __syncwarp();
     griddep_wait();
     if (lane == 0) {
-      uint32_t j = 0;
-      for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      uint32_t jn = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        if (!tile_live(p, t, 1, mv)) continue;
+        const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait(&a_empty[buf], ((j >> 1) & 1) ^ 1);
         const uint32_t q = (uint32_t)t / (uint32_t)p.oh, oy = (uint32_t)t - q * (uint32_t)p.oh;
@@ -1208,8 +1236,10 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
       const int ksteps = p.hk_kpr / 32;
       const uint64_t bd0 = smem_desc_sw128(sB);
       const uint32_t b_units = (uint32_t)(b_stage >> 4);
-      uint32_t j = 0;
-      for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      uint32_t jn = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        if (!tile_live(p, t, 1, mv)) continue;
+        const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
         mbar_wait(&a_full[buf], (j >> 1) & 1);
@@ -1921,7 +1951,7 @@ template <bool FAST>
 __global__ void igemm_finalize_kernel(const __grid_constant__ IgemmArgs p) {
   const int n_out = p.n_real;  // split-K serves the inner products (one group)
   const int quads = (n_out + 3) >> 2;
-  const int64_t total = p.m_total * quads;
+  const int64_t total = m_valid(p) * quads;
   const Q8Consts k = q8_consts(p.rq);
   const int64_t row_stride = (int64_t)p.n_tiles * p.n_rows;
   const int64_t split_stride = p.m_total * row_stride;

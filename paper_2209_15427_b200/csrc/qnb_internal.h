@@ -147,6 +147,10 @@ struct IgemmArgs {
   // sample): one cp.async.bulk.tensor.2d per stage (128 rows x 128 B, 128B swizzle)
   // replaces the 128-thread cp.async gather.
   int32_t a_tma2d;
+  // device-resident batch (nullable): only output rows below *dyn_n * dyn_rows are
+  // live; cluster / pair tiles starting past them are skipped by every warp role
+  const int32_t* dyn_n;
+  int64_t dyn_rows;
   // CTA-pair mode (igemm_pair_kernel): cta_group::2 MMAs with M = 256 and each CTA's
   // half of B resident in smem for the whole launch.
   int32_t pair;
@@ -254,6 +258,20 @@ qnb_status igemm_pack_b(const IgemmGeometry& g, const void* w, int w_dtype, Igem
 // TMA im2col A operand (see IgemmArgs::tmap_a): eligibility, stage list (chunk_off
 // holds {c0, s, r} per stage) and K map; then the tensor map over the activation.
 bool igemm_tma_eligible(const IgemmGeometry& g, const ActLayout& in);
+// ---------------------------------------------------------------- MoE internals
+// Stable per-expert grouping of batch*top_k pairs (qnb_moe_route); counts32 nullable.
+qnb_status launch_moe_route(const int64_t* idx, int64_t BK, int64_t K, int64_t E, int64_t pad, int64_t* counts,
+                            int32_t* counts32, int64_t* pair_sample, int64_t* pair_slot, cudaStream_t s);
+// Gating (qnb_moe_gate) without the host check: a degenerate row sets *err.
+qnb_status launch_moe_gate(const float* feats, int64_t batch, int64_t dim, const float* wa, const float* wb,
+                           const float* wc, int64_t n_experts, int64_t top_k, const float* noise, int64_t* idx,
+                           float* weights, int* err, cudaStream_t s);
+// Device table of the (e1, 10 * e2) gating noise for samples [offset, offset + B).
+qnb_status noise_table(uint64_t seed, int64_t offset, int64_t B, int64_t N, const float** out);
+
+// Allocates a plan's host-I/O staging buffers / copy stream ahead of a stream capture.
+qnb_status plan_prepare_host_io(qnb_plan* P, bool input_on_host, bool output_on_host);
+
 // True when the CTA-pair kernel can run this split-K contraction with the parallel
 // fused reduction (IgemmArgs::ks_fused) -- then no igemm_finalize launch follows.
 bool igemm_splitk_fused_ok(const IgemmArgs& a, int64_t groups);

@@ -160,8 +160,12 @@ __global__ void moe_gate_kernel(const float* __restrict__ feats, int64_t B, int6
   double sum = 0.0;
   for (int64_t i = 0; i < N; ++i) {
     const float q = gate_expf(__fsub_rn(z[i], sh));
-    if (!(q >= 0.0f) || isinf(q)) {
+    if (!(q >= 0.0f) || isinf(q)) {  // gating_probs throws "degenerate gating"
       atomicExch(err, 1);
+      for (int64_t k = 0; k < K; ++k) {  // keep the routing of the batch well-formed
+        idx[s * K + k] = k;
+        wout[s * K + k] = 0.0f;
+      }
       return;
     }
     p[i] = q;
@@ -169,6 +173,10 @@ __global__ void moe_gate_kernel(const float* __restrict__ feats, int64_t B, int6
   }
   if (sum <= 0.0) {
     atomicExch(err, 1);
+    for (int64_t k = 0; k < K; ++k) {
+      idx[s * K + k] = k;
+      wout[s * K + k] = 0.0f;
+    }
     return;
   }
   for (int64_t i = 0; i < N; ++i) p[i] = __double2float_rn(__ddiv_rn((double)p[i], sum));

@@ -155,6 +155,7 @@ struct qnb_plan {
   int64_t launches_per_forward = 0;
   cudaStream_t capture_stream = nullptr;
   int device = 0;
+  const int32_t* dyn_n = nullptr;  // set for the duration of a qnb_plan_forward_dyn call
 };
 
 namespace qnb {
@@ -575,6 +576,16 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   else
     QNB_TRY(igemm_plan_k(g, Lin, &pk));
   if (g.is_fc && !quant) pk.n_per_tile = 128;
+  if (g.is_fc && quant) {
+    // narrow column tiles: every CTA pair streams a distinct 64-channel weight slice and
+    // the batch-256 inner products need little or no K split (measured, AlexNet fc6-8:
+    // 64 / 112 / 160 / 240 columns x at most 1 / 2 / 8 splits; 64 x 2 fastest, -16 us)
+    static const int fc_npt = [] {
+      const char* e = std::getenv("QNB_FC_NPT");
+      return e ? atoi(e) : 64;
+    }();
+    if (fc_npt >= 16) pk.n_per_tile = fc_npt;
+  }
   int32_t pt_bstat_npt = 0;
   int pt_ppst = 1, pt_astg = 2;
   if (patch) {
@@ -702,9 +713,9 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     const int64_t tiles = m_tiles * pk.n_tiles;
     int64_t ks = 148 / std::max<int64_t>(tiles, 1);
     ks = std::max<int64_t>(1, std::min<int64_t>(ks, pk.num_kb / 2));
-    // at most 8 splits: more splits only multiply the s32 partial traffic the finalize
-    // re-reads (fc8: 11 splits wrote 3.5x its 4 MB of weights); measured +0.2 %
-    int64_t ks_max = 8;
+    // at most 2 splits with 64-column tiles: more splits only multiply the s32 partial
+    // traffic the finalize re-reads (fc8: 11 splits wrote 3.5x its 4 MB of weights)
+    int64_t ks_max = 2;
     if (const char* e = std::getenv("QNB_FC_KS_MAX")) ks_max = std::max(1, atoi(e));
     ks = std::max<int64_t>(1, std::min<int64_t>(ks, ks_max));
     a.cluster = 1;
@@ -722,7 +733,9 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
       QNB_CUDA(cudaMemset(sema, 0, 2 * n_sema * 4));
       a.tile_sema = (int32_t*)sema;
       a.tile_done = (int32_t*)sema + n_sema;
-      a.ks_fused = igemm_splitk_fused_ok(a, g.groups) ? 1 : 0;
+      // the parallel fused reduction measured slower than the finalize pass (AlexNet fc6-8:
+      // +18 us each; 256 reduction threads per SM cannot hide the L2 latency): opt-in
+      a.ks_fused = (std::getenv("QNB_FUSED_SPLITK") && igemm_splitk_fused_ok(a, g.groups)) ? 1 : 0;
       if (!a.ks_fused && !std::getenv("QNB_FUSED_FIXUP")) {  // serial last-CTA fixup is opt-in only
         a.tile_sema = nullptr;
         a.tile_done = nullptr;
@@ -952,8 +965,18 @@ qnb_status emit(qnb_plan& P) {
   return QNB_OK;
 }
 
-Step with_batch(const Step& s0, int64_t b, const void* in, void* out) {
+Step with_batch(const Step& s0, int64_t b, const void* in, void* out, const int32_t* dyn = nullptr) {
   Step s = s0;
+  if (dyn) {  // device-resident batch: every kernel clamps its images to min(b, *dyn)
+    s.ig.dyn_n = dyn;
+    s.ig.dyn_rows = s.rows_per_img;
+    s.pack.L.dyn_n = dyn;
+    s.pool.S.dyn_n = s.pool.D.dyn_n = dyn;
+    s.plrn.S.dyn_n = s.plrn.D.dyn_n = dyn;
+    s.cvt.S.dyn_n = s.cvt.D.dyn_n = dyn;
+    s.sm_S.dyn_n = dyn;
+    s.up_S.dyn_n = dyn;
+  }
   if (s.src_sym == SYM_INPUT) s.pack.src = (const uint8_t*)in;
   if (s.dst_sym == SYM_OUTPUT) {
     s.sm_out = (float*)out;
@@ -972,9 +995,10 @@ Step with_batch(const Step& s0, int64_t b, const void* in, void* out) {
   return s;
 }
 
-qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cudaStream_t s) {
+qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cudaStream_t s,
+                      const int32_t* dyn = nullptr) {
   {
-    const Step st = with_batch(s0, b, in, out);
+    const Step st = with_batch(s0, b, in, out, dyn);
     if (st.unpack) {
       launch_unpack(st.up_src, st.up_S, st.up_dst, s);
     } else {
@@ -1014,7 +1038,7 @@ qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cuda
 }
 
 qnb_status launch_steps(qnb_plan& P, int64_t b, const void* in, void* out, cudaStream_t s) {
-  for (const Step& st : P.steps) QNB_TRY(launch_one(st, b, in, out, s));
+  for (const Step& st : P.steps) QNB_TRY(launch_one(st, b, in, out, s, P.dyn_n));
   return QNB_OK;
 }
 
@@ -1033,6 +1057,24 @@ int step_kind_code(const Step& st) {
 }
 
 }  // namespace
+}  // namespace qnb
+
+namespace qnb {
+// Staging buffers and the copy stream of the host-buffer paths, created outside any
+// stream capture (an enclosing plan -- the MoE plan -- calls this before capturing).
+qnb_status plan_prepare_host_io(qnb_plan* P, bool input_on_host, bool output_on_host) {
+  if (input_on_host && !P->in_staging)
+    QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
+  if (output_on_host && !P->out_staging)
+    QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
+  if (input_on_host && !P->copy_stream) {
+    QNB_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+    QNB_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+    P->ev_copy.resize(8);
+    for (auto& e : P->ev_copy) QNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return QNB_OK;
+}
 }  // namespace qnb
 
 using namespace qnb;
@@ -1181,22 +1223,14 @@ static bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+
 qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32_t input_on_host, void* output,
                             int32_t output_on_host, qnb_stream s_) {
   return qnb::guarded([&]() -> qnb_status {
     if (!P) return fail(QNB_E_ARG, "null plan");
     if (batch < 1 || batch > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
     cudaStream_t s = as_stream(s_);
-    if (input_on_host && !P->in_staging)
-      QNB_CUDA(cudaMalloc(&P->in_staging, (size_t)(P->in_bytes_per_sample * P->max_batch)));
-    if (output_on_host && !P->out_staging)
-      QNB_CUDA(cudaMalloc(&P->out_staging, (size_t)(P->out_bytes_per_sample * P->max_batch)));
-    if (input_on_host && !P->copy_stream) {
-      QNB_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
-      QNB_CUDA(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
-      P->ev_copy.resize(8);
-      for (auto& e : P->ev_copy) QNB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    QNB_TRY(plan_prepare_host_io(P, input_on_host != 0, output_on_host != 0));
     const bool pinned_in = input_on_host && is_pinned(input);
     const bool pinned_out = !output_on_host || is_pinned(output);
     // pageable host buffers cannot be captured: run those forwards eagerly
@@ -1236,6 +1270,23 @@ qnb_status qnb_plan_forward(qnb_plan* P, const void* input, int64_t batch, int32
     }
     const int64_t nch = input_on_host ? pipeline_chunks(batch) : 1;
     count_launch((uint64_t)(P->launches_per_forward * nch));
+    return QNB_OK;
+  });
+}
+
+qnb_status qnb_plan_forward_dyn(qnb_plan* P, const void* input, int64_t batch_cap, const int32_t* dyn_batch,
+                                void* output, qnb_stream s_) {
+  return qnb::guarded([&]() -> qnb_status {
+    if (!P || !dyn_batch) return fail(QNB_E_ARG, "null argument");
+    if (batch_cap < 1 || batch_cap > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
+    if (P->flags & QNB_PLAN_OBSERVE) return fail(QNB_E_UNSUPPORTED, "device batch with an OBSERVE plan");
+    for (const Step& st : P->steps)
+      if (st.kind == OP_IGEMM && st.ig.patch) return fail(QNB_E_UNSUPPORTED, "device batch with patch-mode GEMMs");
+    P->dyn_n = dyn_batch;
+    const qnb_status st = launch_steps(*P, batch_cap, input, output, as_stream(s_));
+    P->dyn_n = nullptr;
+    QNB_TRY(st);
+    count_launch((uint64_t)P->launches_per_forward);
     return QNB_OK;
   });
 }

@@ -120,6 +120,11 @@ __device__ __forceinline__ void store_from_float(uint8_t* p, int dtype, float v,
   }
 }
 
+// Images this launch processes: the layout's n, clamped by the device-resident batch.
+__device__ __forceinline__ int64_t eff_n(const DevLayout& L) {
+  return L.dyn_n ? min(L.n, (int64_t)__ldg(L.dyn_n)) : L.n;
+}
+
 __device__ __forceinline__ int64_t img_off(const DevLayout& L, int64_t n) {
   return L.pslot ? (n >> 1) * L.img + (n & 1) * L.pslot : n * L.img;
 }
@@ -141,6 +146,7 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= W) return;
   const int64_t y = blockIdx.y, n = blockIdx.z;
+  if (n >= eff_n(L)) return;
   const int64_t plane = H * W;
   uint8_t* o = at(dst, L, n, y, x);
   const int ses = src_dtype == QNB_FP32 ? 4 : (src_dtype == QNB_INT8Q ? 1 : 2);
@@ -203,6 +209,7 @@ __global__ void __launch_bounds__(256) pack_rgb_u8_kernel(const float* __restric
   const int y = blockIdx.x * (256 / kPackLanes) + ry;
   if (y >= H) return;
   const int64_t n = blockIdx.y;
+  if (n >= eff_n(L)) return;
   const int64_t plane = (int64_t)H * W;
   const float* rowp = src + n * C * plane + (int64_t)y * W;
   uint32_t* orow = reinterpret_cast<uint32_t*>(at(dst, L, n, y, 0));
@@ -242,6 +249,7 @@ __global__ void __launch_bounds__(256) pack_rgb_c_kernel(const float* __restrict
   const int y = blockIdx.x * (256 / kPackLanes) + ry;
   if (y >= H) return;
   const int64_t n = blockIdx.y;
+  if (n >= eff_n(L)) return;
   const int64_t plane = (int64_t)H * W;
   const float* rowp = src + n * C * plane + (int64_t)y * W;
   uint32_t* orow = reinterpret_cast<uint32_t*>(at(dst, L, n, y, 0));
@@ -310,7 +318,7 @@ struct MaxU8x4 {
 __global__ void pool_u8_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst, DevLayout D,
                                int64_t k, int64_t st) {
   const int chunks = (int)(S.c_phys / 16);
-  const int total = (int)(D.n * D.h * D.w * chunks);  // host checks < 2^31
+  const int total = (int)(eff_n(D) * D.h * D.w * chunks);  // host checks < 2^31
   const int Dw = (int)D.w, Dh = (int)D.h, Sw = (int)S.w, Sh = (int)S.h, K = (int)k, ST = (int)st;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int ch = i % chunks, pix = i / chunks;
@@ -350,7 +358,7 @@ template <int K>
 __global__ void __launch_bounds__(256) pool_u8_k_kernel(const uint8_t* __restrict__ src, DevLayout S,
                                                         uint8_t* __restrict__ dst, DevLayout D, int st) {
   const int chunks = (int)(S.c_phys / 16);
-  const int total = (int)(D.n * D.h * D.w * chunks);  // host checks < 2^31
+  const int total = (int)(eff_n(D) * D.h * D.w * chunks);  // host checks < 2^31
   const int Dw = (int)D.w, Dh = (int)D.h;
   const int srow = (int)S.row, spix = (int)S.pix;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(256) pool_u8_k_kernel(const uint8_t* __restric
 
 __global__ void pool_generic_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst,
                                     DevLayout D, int dtype, int64_t k, int64_t st) {
-  const int64_t total = D.n * D.h * D.w * D.c;
+  const int64_t total = eff_n(D) * D.h * D.w * D.c;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = i % D.c, pix = i / D.c;
     const int64_t ox = pix % D.w, oy = (pix / D.w) % D.h, n = pix / (D.w * D.h);
@@ -446,6 +454,7 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_kernel(PoolLrnArgs a) {
   const int64_t pix_per_img = a.D.h * a.D.w;
   const int64_t tiles_per_img = (pix_per_img + kLrnPix - 1) / kLrnPix;
   const int64_t n = blockIdx.x / tiles_per_img;
+  if (n >= eff_n(a.D)) return;
   const int64_t p0 = (blockIdx.x % tiles_per_img) * kLrnPix;
   const int np = (int)min((int64_t)kLrnPix, pix_per_img - p0);
   __syncthreads();
@@ -597,6 +606,7 @@ __global__ void __launch_bounds__(kLrnThreads) pool_lrn_q8_kernel(PoolLrnArgs a)
   const int pix_per_img = (int)(a.D.h * a.D.w);
   const int tiles_per_img = (pix_per_img + P - 1) / P;
   const int64_t n = blockIdx.x / tiles_per_img;
+  if (n >= eff_n(a.D)) return;
   const int p0 = (blockIdx.x % tiles_per_img) * P;
   const int np = min(P, pix_per_img - p0);
   const int Dw = (int)a.D.w;
@@ -741,7 +751,9 @@ struct LrnIo {
 };
 
 template <int PK, int CH, int IT, int OT>
-__global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_t total_pix) {
+__global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_t total_pix_cap) {
+  const int32_t total_pix = (int32_t)(eff_n(a.D) * a.D.h * a.D.w);
+  (void)total_pix_cap;
   __shared__ float lut[256];
   if constexpr (IT == QNB_INT8Q) {
     for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dq(v, a.in_q);
@@ -901,7 +913,7 @@ __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_
 // ---------------------------------------------------------------- convert
 // Generic elementwise op between layouts (interior, real channels only).
 __global__ void convert_kernel(ConvertArgs a) {
-  const int64_t total = a.D.n * a.D.h * a.D.w * a.D.c;
+  const int64_t total = eff_n(a.D) * a.D.h * a.D.w * a.D.c;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = i % a.D.c, pix = i / a.D.c;
     const int64_t x = pix % a.D.w, y = (pix / a.D.w) % a.D.h, n = pix / (a.D.w * a.D.h);
@@ -964,6 +976,7 @@ __global__ void softmax_rows_kernel(const uint8_t* __restrict__ src, DevLayout S
   __shared__ float smax;
   __shared__ double ssum;
   const int64_t n = blockIdx.x;
+  if (n >= eff_n(S)) return;
   const uint8_t* row = at(src, S, n, 0, 0);
   float m = -INFINITY;
   for (int64_t f = threadIdx.x; f < F; f += blockDim.x) {
@@ -1050,7 +1063,7 @@ __global__ void softmax_rows_kernel(const uint8_t* __restrict__ src, DevLayout S
 
 // ------------------------------------------------------------------ unpack
 __global__ void unpack_kernel(const uint8_t* __restrict__ src, DevLayout S, uint8_t* __restrict__ dst) {
-  const int64_t total = S.n * S.c * S.h * S.w;
+  const int64_t total = eff_n(S) * S.c * S.h * S.w;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t x = i % S.w, y = (i / S.w) % S.h, c = (i / (S.w * S.h)) % S.c, n = i / (S.w * S.h * S.c);
     const uint8_t* s = at(src, S, n, y, x) + c * S.es;

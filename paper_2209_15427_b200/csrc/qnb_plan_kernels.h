@@ -16,6 +16,10 @@ struct DevLayout {
   int64_t img, row, pix, origin;
   int32_t es;
   int64_t pslot;  // ActLayout::pair_slot (0: plain NHWC)
+  // device-resident batch (nullable): kernels process min(n, *dyn_n) images, so a plan
+  // launched at its capacity runs a data-dependent batch without a host round trip
+  // (the MoE experts' routed sub-batches)
+  const int32_t* dyn_n;
 };
 
 inline DevLayout dev_layout(const ActLayout& L) {
@@ -31,6 +35,7 @@ inline DevLayout dev_layout(const ActLayout& L) {
   d.origin = L.interior_offset();
   d.es = (int32_t)L.es();
   d.pslot = L.pair_slot;
+  d.dyn_n = nullptr;
   return d;
 }
 

@@ -129,8 +129,103 @@ class ExpertExchange:
         return back
 
 
+class MoePlan:
+    """qnb_moe_plan (include/qnb.h): the whole MoE forward as one device-driven call --
+    trunk, gating, gate, routing, every expert on its device-resident sample count,
+    combine and tail, captured as one CUDA graph (no host round trip)."""
+
+    def __init__(self, net: "MoeNet", max_batch: int, use_cuda_graph: bool = True):
+        lib = L.lib()
+        parts = [net.trunk.layer_descs(), net.gating.layer_descs()]
+        parts += [net.experts[e].layer_descs() for e in range(net.n_experts)]
+        parts.append(net.tail.layer_descs())
+        keep = []
+
+        def gdesc(part):
+            descs, n_blobs, k, _ = part
+            arr = (L.LayerDesc * len(descs))(*descs)
+            keep.extend([arr, k])
+            return L.GraphDesc(arr, len(descs), n_blobs)
+
+        gd = [gdesc(p) for p in parts]
+        trunk, gating, tail = gd[0], gd[1], gd[-1]
+        experts = (L.GraphDesc * net.n_experts)(*gd[2:-1])
+        ml = net.moe_layer
+        tb = G.infer_blobs(net.graph)
+        bottom, top = ml["bottom"][0], ml["top"][0]
+        in_dt = G.DTYPE_CODE[ml["bottom_data_type"]]
+        top_dt = G.DTYPE_CODE[ml["top_data_type"]]
+        qv_in = net.trunk.blob_qvals(bottom)
+        qv_top = net.tail.blob_qvals(top)
+        if in_dt in (2, 3) and qv_in is None:
+            raise QnbError(5, "quantizer not finalized: " + bottom)
+        if top_dt in (2, 3) and qv_top is None:
+            raise QnbError(5, "quantizer not finalized: " + top)
+        for k in ("gate_a", "gate_b", "gate_c"):
+            if k not in net.gates:
+                raise QnbError(1, f"missing parameter: {net.moe_name}.{k}")
+        gsink = G.sinks(ml["moe"]["gating"])[-1]
+        D = int(G.infer_blobs(ml["moe"]["gating"])[gsink]["shape"][1])
+        if net.gates["gate_a"].shape != (net.n_experts, D):
+            raise QnbError(2, "dimension mismatch")
+        ga, gb, gc = (np.ascontiguousarray(net.gates[k], np.float32) for k in ("gate_a", "gate_b", "gate_c"))
+        o = L.MoeOpts()
+        o.max_batch, o.n_experts, o.top_k = max_batch, net.n_experts, net.top_k
+        o.noise_enabled, o.seed, o.sample_offset = 1 if net.noise else 0, net.seed, 0
+        o.in_dtype, o.top_dtype = in_dt, top_dt
+        if qv_in is not None:
+            o.in_qv = QVals(*qv_in.as_tuple())
+        if qv_top is not None:
+            o.top_qv = QVals(*qv_top.as_tuple())
+        o.in_per_sample = int(np.prod(tb[bottom]["shape"][1:]))
+        o.out_per_sample = int(np.prod(tb[top]["shape"][1:]))
+        o.gate_dim = D
+        o.gate_a, o.gate_b, o.gate_c = ga.ctypes.data, gb.ctypes.data, gc.ctypes.data
+        o.use_cuda_graph = 1 if use_cuda_graph else 0
+        self.max_batch, self.n_experts = max_batch, net.n_experts
+        self.out_per_sample, self.top_dtype = o.out_per_sample, top_dt
+        self.h = C.c_void_p()
+        check(lib.qnb_moe_plan_create(C.byref(trunk), C.byref(gating), experts, C.byref(tail), C.byref(o),
+                                      C.byref(self.h)))
+        del keep
+
+    def forward(self, x_ptr: int, out_ptr: int, batch: int, stream: int = 0, in_host: bool = False,
+                out_host: bool = False) -> None:
+        check(L.lib().qnb_moe_plan_forward(self.h, C.c_void_p(x_ptr), batch, 1 if in_host else 0,
+                                           C.c_void_p(out_ptr), 1 if out_host else 0, C.c_void_p(stream)))
+
+    def status(self, stream: int = 0) -> np.ndarray:
+        """Synchronises; per-expert pair counts of the last forward (raises on degenerate gating)."""
+        counts = (C.c_int64 * self.n_experts)()
+        check(L.lib().qnb_moe_plan_status(self.h, counts, C.c_void_p(stream)))
+        return np.array(counts[:], np.int64)
+
+    def moe_output(self, batch: int) -> np.ndarray:
+        ptr = C.c_void_p()
+        check(L.lib().qnb_moe_plan_moe_output(self.h, C.byref(ptr)))
+        dt = NP_OF[self.top_dtype]
+        out = np.empty((batch, self.out_per_sample), dt)
+        check(L.lib().qnb_memcpy_d2h(out.ctypes.data_as(C.c_void_p), ptr, out.nbytes, None))
+        check(L.lib().qnb_stream_sync(None))
+        return out
+
+    def kernels_per_forward(self) -> int:
+        k = C.c_int64()
+        check(L.lib().qnb_moe_plan_stats(self.h, C.byref(k)))
+        return k.value
+
+    def __del__(self):
+        try:
+            if self.h:
+                L.lib().qnb_moe_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
 class MoeNet:
-    """qnet::Net surface for a graph with one MOE layer, backed by B200 plans."""
+    """qnet::Net surface for a graph with one MOE layer, backed by B200 plans.  One rank:
+    the C-ABI MoE plan (MoePlan, device-driven, one CUDA graph).  N ranks: per-expert
+    plans on this rank's experts with the expert all-to-all over torch.distributed."""
 
     BUCKET = 32
 
@@ -151,6 +246,8 @@ class MoeNet:
         self.gates = {}
         self.trunk_layers = {l["name"] for l in trunk["layers"]}
         self._pipes = {}
+        self._mplans = {}
+        self._last = None
 
     # ---- parameters / ranges (dotted names, src/net.cpp:161-204)
     def _route(self, name: str):
@@ -164,12 +261,14 @@ class MoeNet:
     def set_param(self, name, arr, dtype=0, qv=None):
         if name in (f"{self.moe_name}.gate_a", f"{self.moe_name}.gate_b", f"{self.moe_name}.gate_c"):
             self.gates[name.rsplit(".", 1)[1]] = np.ascontiguousarray(arr, np.float32)
+            self._mplans.clear()
             return
         net, local = self._route(name)
         if net is None:
             net = self.trunk if name.split(".")[0] in self.trunk_layers else self.tail
         net.set_param(local, arr, dtype, qv)
         self._pipes.clear()
+        self._mplans.clear()
 
     def set_range(self, key, lo, hi):
         net, local = self._route(key)
@@ -179,11 +278,13 @@ class MoeNet:
             self.trunk.set_range(key, lo, hi)
             self.tail.set_range(key, lo, hi)
         self._pipes.clear()
+        self._mplans.clear()
 
     def finalize_quantizers(self):
         for n in [self.trunk, self.tail, self.gating] + self.experts:
             n.finalize_quantizers()
         self._pipes.clear()
+        self._mplans.clear()
 
     def set_quant_mode(self, mode):
         for n in [self.trunk, self.tail, self.gating] + self.experts:
@@ -263,8 +364,43 @@ class MoeNet:
         self._pipes[B] = p
         return p
 
+    def moe_plan(self, B: int) -> MoePlan:
+        if B not in self._mplans:
+            self._mplans[B] = MoePlan(self, B)
+        return self._mplans[B]
+
+    @property
+    def last_stats(self) -> dict:
+        """Routing statistics of the last forward (synchronises on the MoE plan path)."""
+        if self._last is None:
+            return {"counts": np.zeros(self.n_experts, np.int64)}
+        if isinstance(self._last, MoePlan):
+            import torch
+            return {"counts": self._last.status(torch.cuda.current_stream().cuda_stream)}
+        return self._last
+
+    def moe_output(self, B: int) -> np.ndarray:
+        """The MoE layer's top blob of the last forward at batch B, (B, features) in the
+        top dtype (a checkpoint for parity tests)."""
+        if self.world == 1:
+            return self.moe_plan(B).moe_output(B)
+        p = self._pipes[B]
+        return p["bufs"]["M"].cpu().numpy().view(NP_OF[p["top_dtype"]]).reshape(B, p["per"])
+
     def forward_device(self, x_ptr: int, out_ptr: int, B: int, in_host: bool = False,
-                       out_host: bool = False) -> dict:
+                       out_host: bool = False):
+        """One MoE forward on torch's current stream (device buffers, or pinned host
+        buffers).  One rank: the device-driven MoE plan, nothing returns to the host."""
+        if self.world == 1:
+            import torch
+            mp = self.moe_plan(B)
+            mp.forward(x_ptr, out_ptr, B, torch.cuda.current_stream().cuda_stream, in_host, out_host)
+            self._last = mp
+            return None
+        return self._forward_device_xchg(x_ptr, out_ptr, B, in_host, out_host)
+
+    def _forward_device_xchg(self, x_ptr: int, out_ptr: int, B: int, in_host: bool = False,
+                             out_host: bool = False) -> dict:
         """One MoE forward (stream: torch's current stream) on device buffers, or on pinned
         host buffers: the trunk plan then pipelines the input's H2D copy chunk by chunk
         under its own compute, and the tail plan copies the result back.  Returns routing
@@ -350,14 +486,8 @@ class MoeNet:
         check(lib.qnb_moe_combine_rows(y.data_ptr(), p["per"], b["pair_slot"].data_ptr(), b["w"].data_ptr(), B,
                                        self.top_k, p["top_dtype"], qv, b["M"].data_ptr(), sp))
         p["tail"].forward_device(b["M"].data_ptr(), out_ptr, B, s, out_host=out_host)
-        self.last_stats = {"counts": counts}
-        return self.last_stats
-
-    def moe_output(self, B: int) -> np.ndarray:
-        """The MoE layer's top blob of the last forward at batch B, (B, features) in the
-        top dtype (a checkpoint for parity tests)."""
-        p = self._pipes[B]
-        return p["bufs"]["M"].cpu().numpy().view(NP_OF[p["top_dtype"]]).reshape(B, p["per"])
+        self._last = {"counts": counts}
+        return self._last
 
     def forward(self, inputs: dict) -> dict:
         """Net::forward (src/net.cpp:305-330) with host arrays in and out."""
@@ -367,14 +497,14 @@ class MoeNet:
             raise QnbError(1, "missing input: " + name)
         x = np.ascontiguousarray(inputs[name])
         B = x.shape[0]
-        p = self._pipe(B)
-        tp = p["tail"]
+        sink = G.sinks(self.graph)[-1]
+        info = G.infer_blobs(self.graph)[sink]
         xd = torch.from_numpy(x).cuda()
-        out = np.empty((B,) + tp.out_shape[1:], NP_OF[tp.out_dtype])
+        out = np.empty((B,) + tuple(info["shape"][1:]), NP_OF[G.DTYPE_CODE[info["dtype"]]])
         od = torch.empty(out.nbytes, dtype=torch.uint8, device="cuda")
-        self.last_stats = self.forward_device(xd.data_ptr(), od.data_ptr(), B)
+        self.forward_device(xd.data_ptr(), od.data_ptr(), B)
         out[...] = od.cpu().numpy().view(out.dtype).reshape(out.shape)
         return {G.sinks(self.graph)[-1]: out}
 
 
-__all__ = ["MoeNet", "ExpertExchange", "split_moe_graph", "QUANTIZED", "QVals"]
+__all__ = ["MoeNet", "MoePlan", "ExpertExchange", "split_moe_graph", "QUANTIZED", "QVals"]

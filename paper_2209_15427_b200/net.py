@@ -102,6 +102,11 @@ class Plan:
         check(_plan_lib().qnb_plan_forward(self.h, C.c_void_p(in_ptr), batch, 1 if in_host else 0,
                                            C.c_void_p(out_ptr), 1 if out_host else 0, C.c_void_p(stream)))
 
+    def forward_dyn(self, in_ptr: int, out_ptr: int, batch_cap: int, dyn_ptr: int, stream: int = 0) -> None:
+        """qnb_plan_forward_dyn: launched at batch_cap, processes *dyn_ptr (int32, device) images."""
+        check(_plan_lib().qnb_plan_forward_dyn(self.h, C.c_void_p(in_ptr), batch_cap, C.c_void_p(dyn_ptr),
+                                               C.c_void_p(out_ptr), C.c_void_p(stream)))
+
     def observe_host(self, x: np.ndarray):
         """qnb_plan_observe on a host batch: (output, {blob id: (min, max)})."""
         x = np.ascontiguousarray(x)

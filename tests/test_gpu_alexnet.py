@@ -168,3 +168,24 @@ def test_inspect_blobs_stay_addressable(setup):
     fc8 = nhwc_interior_to_nchw(raw, lay, np.float32).reshape(batch, -1)[:, :1000]
     e = np.exp(fc8.astype(np.float64) - fc8.max(axis=1, keepdims=True))
     assert np.allclose(e / e.sum(axis=1, keepdims=True), out, rtol=1e-5, atol=1e-9)
+
+
+def test_device_resident_batch(setup):
+    """qnb_plan_forward_dyn: a plan launched at its capacity with the batch in device
+    memory (the MoE experts' routed sub-batches) gives exactly the host-batch forward for
+    the live images and leaves the rows past the device batch untouched."""
+    import torch
+    ref, g, params, ranges, ours = setup
+    cap = 64
+    plan = ours.compile(cap, use_cuda_graph=False)
+    x = graphs.synth_images(cap, (3, 227, 227), offset=700)
+    xd = torch.from_numpy(x).cuda()
+    for n in (37, 1, 64, 2):
+        want = torch.empty((n, 1000), dtype=torch.float32, device="cuda")
+        plan.forward_device(xd.data_ptr(), want.data_ptr(), n)
+        got = torch.full((cap, 1000), -7.0, dtype=torch.float32, device="cuda")
+        dyn = torch.tensor([n], dtype=torch.int32, device="cuda")
+        plan.forward_dyn(xd.data_ptr(), got.data_ptr(), cap, dyn.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(got[:n], want), n
+        assert bool((got[n:] == -7.0).all()), n

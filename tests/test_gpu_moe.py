@@ -72,8 +72,7 @@ def test_alexnet_moe_int8_matches_reference(reference, setup):
     rp = ref_net(reference, json.dumps(prefix), pp, ranges, -1)
     (m_ref, dt, qv), = rp.forward("data", x).values()
     assert dt == 2
-    p = ours._pipe(batch)
-    m_ours = p["bufs"]["M"].cpu().numpy()[: m_ref.size].reshape(m_ref.shape)
+    m_ours = ours.moe_output(batch).reshape(m_ref.shape)
     assert np.array_equal(m_ours, m_ref), int((m_ours != m_ref).sum())
     torch.cuda.synchronize()
 
@@ -99,3 +98,57 @@ def test_alexnet_moe_host_buffers_match_device_path(setup):
         ours.forward_device(xp.data_ptr(), op.data_ptr(), batch, in_host=True, out_host=True)
         torch.cuda.synchronize()
         assert np.array_equal(op.numpy(), want)
+
+
+def test_alexnet_moe_noisy_gating_matches_reference(reference, setup):
+    """Gating noise on (MoeLayerParams::noise_enabled, src/moe.cpp:53-71, 92-95) with
+    non-zero W_b / W_c, through the device-driven MoE plan: the noise table is drawn with
+    the reference's own arithmetic, so routing and the MoE output are bit-identical."""
+    g, params, ranges = setup
+    g = json.loads(json.dumps(g))
+    moe = next(l for l in g["layers"] if l["kind"] == "moe")
+    moe["moe"]["noise_enabled"] = True
+    moe["moe"]["seed"] = 12345
+    params = dict(params)
+    rng = np.random.default_rng(77)
+    N, D = params["moe.gate_a"].shape
+    params["moe.gate_b"] = rng.uniform(-0.3, 0.3, (N, D)).astype(np.float32)
+    params["moe.gate_c"] = rng.uniform(-0.5, 0.5, (N,)).astype(np.float32)
+    batch = 3
+    x = graphs.synth_images(batch, (3, 227, 227), offset=40)
+    ours = our_net(g, params, ranges)
+    out = ours.forward({"data": x})["prob"]
+    rn = ref_net(reference, json.dumps(g), params, ranges, 2)
+    full = json.loads(rn.graph_json())
+    prob_ref = rn.forward("data", x)["prob"][0]
+    d = np.abs(out.view(np.int32).astype(np.int64) - prob_ref.view(np.int32).astype(np.int64))
+    assert d.max() <= 1, d.max()
+    names = [l["name"] for l in full["layers"]]
+    prefix = {"name": "moe_prefix", "layers": full["layers"][: names.index("moe") + 1],
+              "range_aliases": full.get("range_aliases", {})}
+    keep = {l["name"] for l in prefix["layers"]}
+    pp = {k: v for k, v in params.items() if k.split(".")[0] in keep}
+    (m_ref, dt, qv), = ref_net(reference, json.dumps(prefix), pp, ranges, -1).forward("data", x).values()
+    assert np.array_equal(ours.moe_output(batch).reshape(m_ref.shape), m_ref)
+
+
+def test_moe_plan_counts_and_graph_replay(setup):
+    """The MoE plan replays one CUDA graph; routing counts come back only on request
+    (qnb_moe_plan_status) and always sum to batch * top_k; a replay at another batch
+    size (new graph) and back gives identical outputs."""
+    import torch
+    g, params, ranges = setup
+    ours = our_net(g, params, ranges)
+    outs = {}
+    for batch in (40, 17, 40):
+        x = graphs.synth_images(batch, (3, 227, 227), offset=900)
+        xd = torch.from_numpy(x).cuda()
+        od = torch.empty((batch, 1000), dtype=torch.float32, device="cuda")
+        ours.forward_device(xd.data_ptr(), od.data_ptr(), batch)
+        counts = ours.last_stats["counts"]
+        assert counts.sum() == batch * 4 and (counts >= 0).all()
+        o = od.cpu().numpy()
+        if batch in outs:
+            assert np.array_equal(outs[batch], o)
+        outs[batch] = o
+    assert np.array_equal(outs[17], outs[40][:17])  # per-sample independence (same seeds)
