@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], (p.a_tma2d ? 1u : 128u + (stream ? 1u : 0u)) + (rank == 0 ? 1u : 0u));
+      mbar_init(&full[i], ((p.a_tma2d || p.a_planes) ? 1u : 128u + (stream ? 1u : 0u)) + (rank == 0 ? 1u : 0u));
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -958,7 +958,49 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   const uint32_t tmem = *tmem_slot;
 
   if (warp != 4) griddep_wait();  // warp 4 first issues the resident weights (independent of it)
-  if (warp < 4 && p.a_tma2d) {
+  if (warp < 4 && p.a_planes) {
+    // ---------------------------------------------------------- TMA chunk-plane producer
+    // one thread: per stage, one im2col load (128 output pixels x 16 B) per real K chunk
+    // into its 2 KB plane, plus this CTA's half of the B stage when streamed; chunks past
+    // the last tap are left as they are (their weights are zero)
+    if (threadIdx.x == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_a)) : "memory");
+      uint32_t st_ph = 0;
+      int st_s = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        const TileCoord c = tile_of(ct, m_pairs, ntk);
+        const int64_t mt = c.mt * 2 + rank;
+        const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
+        const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+        const uint8_t* bsrc =
+            p.b + ((int64_t)(c.g * p.n_tiles + ntile) * p.num_kb) * (p.n_rows * 128) + (int64_t)rank * bh;
+        const uint32_t row0 = (uint32_t)(mt * kBM);
+        const uint32_t img = row0 / (uint32_t)pix_per_img;
+        const uint32_t rem = row0 - img * (uint32_t)pix_per_img;
+        const uint32_t oy = rem / (uint32_t)p.ow, ox = rem - oy * (uint32_t)p.ow;
+        const int w0 = (int)(ox * p.stride_w), h0 = (int)(oy * p.stride_h);
+        const int cg0 = c.g * (int)p.a_group;  // group channel offset (elements)
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int s = st_s;
+          mbar_wait(&empty[s], st_ph ^ 1);
+          if (++st_s == S) {
+            st_s = 0;
+            st_ph ^= 1;
+          }
+          const int k0 = kb * 8, nreal = max(0, min(8, p.pl_chunks - k0));
+          mbar_arrive_expect_tx(&full[s], (uint32_t)(nreal * 2048 + (stream ? bh : 0)));
+          for (int j = 0; j < nreal; ++j) {
+            const int k = k0 + j, tap = k / p.pl_cpt, cc = k - tap * p.pl_cpt;
+            const int r = tap / p.pl_kw, sx = tap - r * p.pl_kw;
+            tma_im2col_4d(sA + (size_t)s * a_stage + j * 2048, &p.tmap_a, cg0 + cc * 16, w0, h0, (int)img,
+                          (uint16_t)sx, (uint16_t)r, &full[s]);
+          }
+          if (stream) bulk_g2s(sB + (size_t)s * bh, bsrc + (int64_t)kb * p.n_rows * 128, (uint32_t)bh, &full[s]);
+        }
+      }
+    }
+  } else if (warp < 4 && p.a_tma2d) {
     // ---------------------------------------------------------------- TMA producer
     // one thread: per stage a 128 x 128 B tile of the samples' contiguous K bytes (2-D
     // tensor map, hardware 128B swizzle; rows past the batch and K past the sample are
@@ -1113,11 +1155,16 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
             st_ph ^= 1;
           }
           tc_fence_after();
-          const uint64_t ad = smem_desc_sw(sA + (size_t)s * a_stage, 128);
+          // chunk planes: non-swizzled K-major (LBO = next 2 KB plane, SBO = 8 rows of 16 B);
+          // one K step of 32 bytes = two planes = +4096 B (256 descriptor units)
+          const uint64_t ad = p.a_planes ? smem_desc_none(sA + (size_t)s * a_stage, 2048, 128)
+                                         : smem_desc_sw(sA + (size_t)s * a_stage, 128);
+          const uint32_t astep = p.a_planes ? 256u : 2u;
           const uint64_t bd = smem_desc_sw(sB + (size_t)(stream ? s : kb) * bh, 128);
           if (elect_one()) {
             if (mma_on)
-              for (int k = 0; k < 4; ++k) umma2_i8(dt, ad + 2 * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                umma2_i8(dt, ad + astep * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
             tc_commit2_multicast(&empty[s], 3);
           }
           __syncwarp();
@@ -1356,6 +1403,40 @@ qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const u
                             (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(QNB_E_CUDA, "cuTensorMapEncodeIm2col failed: " + std::to_string((int)r));
+  return QNB_OK;
+}
+
+bool igemm_planes_eligible(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk) {
+  if (g.kind != KIND_I8 || g.q16 || g.is_fc || !igemm_tma_eligible(g, in) || in.es() != 1) return false;
+  const int64_t cpt = g.cg / 16, taps = g.kh * g.kw;
+  if (g.cg % 16 != 0 || (int64_t)pk.chunk_off.size() < taps * cpt) return false;
+  for (int64_t k = 0; k < taps * cpt; ++k) {  // the chunk table must be tap-major (r, s, cc)
+    const int64_t tap = k / cpt, cc = k % cpt, r = tap / g.kw, sx = tap % g.kw;
+    if (pk.chunk_off[(size_t)k] != r * in.row() + sx * in.pix() + cc * 16) return false;
+  }
+  return true;
+}
+
+qnb_status igemm_encode_tma_planes(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base,
+                                   CUtensorMap* map) {
+  const uint8_t* base = a_base + (in.hh - g.ph) * in.row() + (in.hw - g.pw) * in.pix();
+  const int64_t W = in.w + 2 * g.pw, H = in.h + 2 * g.ph;
+  const cuuint64_t dims[4] = {(cuuint64_t)in.c_phys, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)in.n};
+  const cuuint64_t strides[3] = {(cuuint64_t)in.pix(), (cuuint64_t)in.row(), (cuuint64_t)in.img()};
+  const int lower[2] = {0, 0};
+  const int upper[2] = {(int)-(g.kw - 1), (int)-(g.kh - 1)};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g.sw, (cuuint32_t)g.sh, 1};
+  using EncodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static const EncodeIm2col encode = driver_fn<EncodeIm2col>("cuTensorMapEncodeIm2col");
+  if (!encode) return fail(QNB_E_CUDA, "cuTensorMapEncodeIm2col unavailable (driver too old?)");
+  // 16 channels (bytes) per pixel, 128 pixels per box, no swizzle: a dense 2 KB chunk plane
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, (void*)base, dims, strides, lower, upper, 16,
+                            (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(QNB_E_CUDA, "cuTensorMapEncodeIm2col (planes) failed: " + std::to_string((int)r));
   return QNB_OK;
 }
 

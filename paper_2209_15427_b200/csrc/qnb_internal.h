@@ -147,6 +147,14 @@ struct IgemmArgs {
   // sample): one cp.async.bulk.tensor.2d per stage (128 rows x 128 B, 128B swizzle)
   // replaces the 128-thread cp.async gather.
   int32_t a_tma2d;
+  // TMA im2col chunk planes (a_planes = 1; CTA-pair kernel, INT8): the K order is
+  // (tap, 16-byte channel chunk) -- the gather's tap-major chunk table -- and every chunk
+  // of a stage is one cp.async.bulk.tensor.im2col of 128 output pixels x 16 bytes into its
+  // own 2 KB plane; the MMA reads the stage through a non-swizzled K-major descriptor
+  // (core-matrix rows 16 B apart, SBO = 128, next chunk plane LBO = 2048).  Replaces the
+  // 16-byte cp.async gather for taps that are not whole 128-byte stages (AlexNet conv2:
+  // 48 channels per group and tap).  tmap_a holds the 16-byte-channel im2col map.
+  int32_t a_planes, pl_cpt, pl_kw, pl_chunks;  // chunks per tap, filter width, real chunks
   // device-resident batch (nullable): only output rows below *dyn_n * dyn_rows are
   // live; cluster / pair tiles starting past them are skipped by every warp role
   const int32_t* dyn_n;
@@ -275,6 +283,11 @@ qnb_status plan_prepare_host_io(qnb_plan* P, bool input_on_host, bool output_on_
 // True when the CTA-pair kernel can run this split-K contraction with the parallel
 // fused reduction (IgemmArgs::ks_fused) -- then no igemm_finalize launch follows.
 bool igemm_splitk_fused_ok(const IgemmArgs& a, int64_t groups);
+// True when the tap-major chunk table of `pk` can be served by TMA im2col chunk planes;
+// encodes the 16-byte-channel im2col tensor map.
+bool igemm_planes_eligible(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk);
+qnb_status igemm_encode_tma_planes(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base,
+                                   CUtensorMap* map);
 // 2-D tensor map over `rows` samples of `kbytes` contiguous bytes, `row_stride` apart.
 qnb_status igemm_encode_tma2d(const uint8_t* base, int64_t rows, int64_t kbytes, int64_t row_stride, CUtensorMap* map);
 qnb_status igemm_plan_tma(const IgemmGeometry& g, const ActLayout& in, IgemmPacked* pk);
