@@ -438,10 +438,18 @@ def run_qnb(a):
     B = wl.B
     stream = torch.cuda.current_stream()
     # N > 1: every rank classifies its own batch shard; the final logits are gathered
-    # over NCCL (the path's only data-path collective besides the MoE all-to-all)
+    # over NCCL (the path's only data-path collective besides the MoE all-to-all).  Chain
+    # nets run through the C-ABI group (qnb_group_forward: plan + in-place ncclAllGather).
     gathered = torch.empty((ws * B, wl.n_out), dtype=torch.float32, device="cuda") if ws > 1 else None
+    group = None
+    if ws > 1 and not wl.moe:
+        from paper_2209_15427_b200.group import Group
+        group = Group.from_torch(rank, ws, local)
 
     def step():
+        if group is not None:
+            group.forward(wl.plan, wl.x_dev.data_ptr(), B, gathered.data_ptr(), wl.n_out * 4, wl.sp)
+            return
         wl.step()
         if ws > 1:
             import torch.distributed as dist
@@ -580,7 +588,8 @@ def run_qnb(a):
                 "config": {"workload": f"{a.model} {a.precision} forward, batch {B} per GPU, {res}x{res} "
                                        f"(BASELINE configs[{CONFIG_IDX.get(a.model, '?')}])",
                            "model": a.model, "global_batch": B * ws,
-                           "parallelism": (f"dp{ws}: batch shard per GPU, NCCL all-gather of the logits"
+                           "parallelism": (f"dp{ws}: batch shard per GPU, NCCL all-gather of the logits "
+                                           f"(qnb_group_forward)"
                                            + (", expert-parallel all-to-all" if wl.moe else "")) if ws > 1
                            else "dp1 (single GPU)",
                            "l2": f"input batch {wl.x_host.nbytes / 1e6:.0f} MB "

@@ -61,7 +61,8 @@ typedef enum {
   QNB_E_CUDA = 8,        /* CUDA runtime/driver error or no sm_100 device */
   QNB_E_OOM = 9,         /* device allocation failed */
   QNB_E_UNSUPPORTED = 10, /* valid for the reference but not implemented here */
-  QNB_E_IO = 11           /* std::runtime_error: "not a model file", "truncated model file", "cannot read: ..." */
+  QNB_E_IO = 11,          /* std::runtime_error: "not a model file", "truncated model file", "cannot read: ..." */
+  QNB_E_NCCL = 12         /* NCCL failure or libnccl.so.2 unavailable (multi-GPU group calls) */
 } qnb_status;
 
 /* qnet::QuantizerValues (include/qnet/quantizer_values.hpp:32-42). */
@@ -369,6 +370,30 @@ qnb_status qnb_moe_plan_status(qnb_moe_plan* plan, int64_t* counts, qnb_stream s
 qnb_status qnb_moe_plan_moe_output(const qnb_moe_plan* plan, void** dev_ptr);
 qnb_status qnb_moe_plan_stats(const qnb_moe_plan* plan, int64_t* kernels_per_forward);
 qnb_status qnb_moe_plan_destroy(qnb_moe_plan* plan);
+
+/* ------------------------------------------------------------------ multi-GPU group
+ * Data parallelism over the GPUs of one node: one process per GPU, the
+ * batch sharded in contiguous slices, weights replicated, every layer per-sample.  The
+ * only data-path collectives are the logits all-gather and the MoE expert all-to-all,
+ * NCCL collectives on the caller's stream (NVLink / NVSwitch).  The reference has no
+ * multi-device placement; the hook it would have is Net::forward (include/qnet/net.hpp:85-86).
+ * The NCCL unique id is produced on one rank and distributed by the caller
+ * (torch.distributed / MPI / a file), exactly like ncclGetUniqueId. */
+typedef struct qnb_group qnb_group;
+qnb_status qnb_group_unique_id(uint8_t id[128]);
+qnb_status qnb_group_create(int32_t world, int32_t rank, const uint8_t id[128], int32_t device, qnb_group** out);
+/* This rank's shard through `plan` (input host or device), written to its slice of
+ * `gathered` (device, world * shard_batch * out_bytes_per_sample bytes), then an in-place
+ * ncclAllGather: every rank ends with the whole batch's outputs in rank order. */
+qnb_status qnb_group_forward(qnb_group* g, qnb_plan* plan, const void* input_shard, int64_t shard_batch,
+                             int32_t input_on_host, void* gathered, int64_t out_bytes_per_sample, qnb_stream s);
+qnb_status qnb_group_allgather(qnb_group* g, const void* send, void* recv, int64_t bytes, qnb_stream s);
+/* Expert all-to-all building block (ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd):
+ * bytes [send_off[p], +send_bytes[p]) go to rank p, rank p's bytes land at recv_off[p]. */
+qnb_status qnb_group_alltoallv(qnb_group* g, const void* send, const int64_t* send_off, const int64_t* send_bytes,
+                               void* recv, const int64_t* recv_off, const int64_t* recv_bytes, qnb_stream s);
+qnb_status qnb_group_info(const qnb_group* g, int32_t* world, int32_t* rank);
+qnb_status qnb_group_destroy(qnb_group* g);
 
 /* ---------------------------------------------------------------- QCNM model store
  * The reference's binary model file (QCNM v1, src/model_store.cpp:123-206;

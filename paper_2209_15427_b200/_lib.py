@@ -132,6 +132,15 @@ _PLAN_SIGS = {
     "qnb_moe_plan_moe_output": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "qnb_moe_plan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "qnb_moe_plan_destroy": (C.c_int, [C.c_void_p]),
+    "qnb_group_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "qnb_group_create": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_uint8), C.c_int32, C.POINTER(C.c_void_p)]),
+    "qnb_group_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+                                    C.c_void_p]),
+    "qnb_group_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "qnb_group_alltoallv": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p]),
+    "qnb_group_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "qnb_group_destroy": (C.c_int, [C.c_void_p]),
     "qnb_model_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "qnb_model_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "qnb_model_record": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(Record)]),

@@ -268,7 +268,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
   if (tma) {
     a.a_tma = 1;
     QNB_TRY(igemm_encode_tma(g, io.in, (const uint8_t*)xin, pk.kbytes, &a.tmap_a));
-  } else if (!hk && !patch && !std::getenv("QNB_NO_TMA") && !std::getenv("QNB_NO_PLANES") &&
+  } else if (!hk && !patch && !std::getenv("QNB_NO_TMA") && std::getenv("QNB_PLANES") &&
              igemm_planes_eligible(g, io.in, pk)) {
     QNB_TRY(igemm_encode_tma_planes(g, io.in, (const uint8_t*)xin, &a.tmap_a));
     a.a_planes = 1;

@@ -69,6 +69,7 @@ __device__ __forceinline__ TileCoord tile_of(int64_t t, int64_t m_tiles, int n_t
 // A (cluster) tile is live when its first output row is below m_valid.  Row-Hankel
 // tiles are (image pair q, output row): live when image 2q is inside the batch.
 __device__ __forceinline__ bool tile_live(const IgemmArgs& p, int64_t cmt, int cs, int64_t mv) {
+  if (p.patch) return true;  // padded-grid tiles (no device batch in patch mode)
   if (p.hk) return 2 * (cmt / p.oh) * (int64_t)p.oh * p.ow < mv;
   return cmt * cs * kBM < mv;
 }

@@ -634,9 +634,10 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   if (tma) {
     a.a_tma = 1;
     QNB_TRY(igemm_encode_tma(g, Lin, blob_ptr(P, op.in), pk.kbytes, &a.tmap_a));
-  } else if (!hk && !patch && !no_tma && !std::getenv("QNB_NO_PLANES") && igemm_planes_eligible(g, Lin, pk)) {
-    // taps narrower than a 128-byte stage: TMA im2col chunk planes for the CTA-pair kernel
-    // (the 16-byte cp.async gather is limited to ~25 GB/s per SM)
+  } else if (!hk && !patch && !no_tma && std::getenv("QNB_PLANES") && igemm_planes_eligible(g, Lin, pk)) {
+    // opt-in (QNB_PLANES=1): TMA im2col chunk planes for the CTA-pair kernel.  Measured
+    // 2-2.5x SLOWER than the cp.async gather on AlexNet conv2-5 (conv2 283 vs 135 us): a
+    // 16-byte-wide im2col box moves 16 B per pixel row through the TMA engine
     QNB_TRY(igemm_encode_tma_planes(g, Lin, blob_ptr(P, op.in), &a.tmap_a));
     a.a_planes = 1;
     a.pl_cpt = (int32_t)(g.cg / 16);

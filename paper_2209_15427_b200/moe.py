@@ -116,6 +116,26 @@ class ExpertExchange:
         grouped = self.gather(out, p) if len(perm) else out
         return grouped, local_counts
 
+    def run(self, rows, counts: np.ndarray, expert_fn):
+        """The expert-parallel step of one MoE forward: dispatch this rank's routed rows
+        (grouped by global expert, `counts` per expert) to the experts' owners, run
+        `expert_fn(e, rows_e) -> outputs` on the rows each local expert received, and return
+        the outputs to their home ranks in the original pair order."""
+        grouped, local_counts = self.dispatch(rows, counts)
+        outs, off = [], 0
+        for j in range(self.per_rank):
+            c = int(local_counts[j])
+            e = self.rank * self.per_rank + j
+            outs.append(expert_fn(e, grouped[off:off + c]) if c else grouped.new_empty((0,)))
+            off += c
+        y = [o for o in outs if o.numel()]
+        if y:
+            import torch
+            y_grouped = torch.cat(y, 0)
+        else:
+            y_grouped = grouped.new_empty((0,) + tuple(grouped.shape[1:]))
+        return self.combine(y_grouped)
+
     def combine(self, y_grouped):
         import torch
         import torch.distributed as dist
@@ -423,65 +443,31 @@ class MoeNet:
         check(lib.qnb_moe_gate_at(b["feats"].data_ptr(), B, p["D"], b["wa"].data_ptr(), b["wb"].data_ptr(),
                                   b["wc"].data_ptr(), self.n_experts, self.top_k, 1 if self.noise else 0,
                                   C.c_uint64(self.seed), self.rank * B, b["idx"].data_ptr(), b["w"].data_ptr(), sp))
-        # one rank: fixed per-expert segments (stride B + BUCKET rows) -> every expert's plan
-        # replays a cached CUDA graph at a bucketed batch size, concurrently on its own
-        # stream; N ranks: dense rows (the all-to-all splits count real pairs)
-        stride = B + self.BUCKET if self.world == 1 else 0
-        check(lib.qnb_moe_route(b["idx"].data_ptr(), B, self.top_k, self.n_experts, stride, b["counts"].data_ptr(),
+        # dense per-expert rows; the all-to-all splits count real pairs
+        check(lib.qnb_moe_route(b["idx"].data_ptr(), B, self.top_k, self.n_experts, 0, b["counts"].data_ptr(),
                                 b["pair_sample"].data_ptr(), b["pair_slot"].data_ptr(), sp))
-        P = self.n_experts * stride if stride else B * self.top_k
+        P = B * self.top_k
         es = b["S"].shape[1] // p["row_elems"]
         check(lib.qnb_gather_rows(b["T"].data_ptr(), p["row_elems"] * es, b["pair_sample"].data_ptr(), P,
                                   b["S"].data_ptr(), sp))
-        counts = b["counts"].cpu().numpy()  # the expert sub-batch sizes drive the launches
-        if self.world > 1:
-            rows, local_counts = p["xchg"].dispatch(b["S"], counts)
-        else:
-            rows, local_counts = b["S"], counts
-        nrows = int(local_counts.sum()) if not stride else self.n_experts * stride
+        counts = b["counts"].cpu().numpy()  # the all-to-all needs the split sizes on the host
+        xoff = [0]
 
-        def to_f32(src_ptr, dst_ptr, n_rows, st):
-            ne = n_rows * p["row_elems"]
+        def expert_fn(e, rows_e):
+            """Expert e (a local plan) on the rows it received: dequantize -> plan -> FP32."""
+            c = rows_e.shape[0]
+            x_dst = b["X"].data_ptr() + xoff[0] * p["row_elems"] * 4
+            ne = c * p["row_elems"]
             if p["qv_in"] is not None:
-                check(lib.qnb_dequantize(src_ptr, ne, p["in_dtype"], C.byref(p["qv_in"]), dst_ptr, C.c_void_p(st)))
+                check(lib.qnb_dequantize(rows_e.data_ptr(), ne, p["in_dtype"], C.byref(p["qv_in"]), x_dst, sp))
             else:
-                check(lib.qnb_cast_float(src_ptr, ne, p["in_dtype"], L.FP32, dst_ptr, C.c_void_p(st)))
+                check(lib.qnb_cast_float(rows_e.data_ptr(), ne, p["in_dtype"], L.FP32, x_dst, sp))
+            y = b["Y"][xoff[0]:xoff[0] + c]
+            p["experts"][e].forward_device(x_dst, y.data_ptr(), c, s)
+            xoff[0] += c
+            return y
 
-        if not stride:
-            to_f32(rows.data_ptr(), b["X"].data_ptr(), nrows, s)
-        off = 0
-        cap = p["experts"][next(iter(p["experts"]))].max_batch
-        main = torch.cuda.current_stream()
-        if "streams" not in p:
-            p["streams"] = [torch.cuda.Stream() for _ in range(4)]
-            p["events"] = [torch.cuda.Event() for _ in range(5)]
-        ready = p["events"][4]
-        ready.record(main)
-        used = []
-        for j, e in enumerate(sorted(p["experts"])):
-            c = int(local_counts[j])
-            if c:
-                if stride:
-                    # fixed segment, bucketed batch (graph cache hit), concurrent stream
-                    bk = min(cap, -(-c // self.BUCKET) * self.BUCKET)
-                    st = p["streams"][len(used) % len(p["streams"])]
-                    st.wait_event(ready)
-                    used.append(st)
-                    ss = st.cuda_stream
-                    to_f32(b["S"].data_ptr() + off * p["row_elems"] * es, b["X"].data_ptr() + off * p["row_elems"] * 4,
-                           c, ss)
-                else:
-                    bk, ss = c, s
-                p["experts"][e].forward_device(b["X"].data_ptr() + off * p["row_elems"] * 4,
-                                               b["Y"].data_ptr() + off * p["per"] * 4, bk, ss)
-            off += stride if stride else c
-        for i, st in enumerate({id(x): x for x in used}.values()):
-            ev = p["events"][i]
-            ev.record(st)
-            main.wait_event(ev)
-        y = b["Y"][:nrows]
-        if self.world > 1:
-            y = p["xchg"].combine(y)
+        y = p["xchg"].run(b["S"][:P], counts, expert_fn)
         qv = C.byref(p["qv_top"]) if p["qv_top"] is not None else None
         check(lib.qnb_moe_combine_rows(y.data_ptr(), p["per"], b["pair_slot"].data_ptr(), b["w"].data_ptr(), B,
                                        self.top_k, p["top_dtype"], qv, b["M"].data_ptr(), sp))

@@ -58,6 +58,47 @@ int main(int argc, char** argv) {
   std::string in_name;
   std::vector<int64_t> in_shape;
   uint64_t seed = 1234;
+  // seeded conv / inner-product parameters of graph `gs`, names prefixed for nested nets
+  auto set_params = [&](const GraphSpec& gs, const std::string& prefix) {
+    const auto bl = infer_blobs(gs);
+    for (const LayerSpec& l : gs.layers) {
+      if (l.kind != LayerKind::CONV && l.kind != LayerKind::INNER_PRODUCT) continue;
+      const auto& ish = bl.at(l.bottoms[0]).shape;
+      std::vector<int64_t> wshape;
+      int64_t fan = 0;
+      if (l.kind == LayerKind::CONV) {
+        const int64_t cg = ish[1] / l.conv.groups;
+        wshape = {l.conv.out_channels, cg, l.conv.kernel_h, l.conv.kernel_w};
+        fan = cg * l.conv.kernel_h * l.conv.kernel_w;
+      } else {
+        int64_t k = 1;
+        for (size_t i = 1; i < ish.size(); ++i) k *= ish[i];
+        wshape = {k, l.num_output};
+        fan = k;
+      }
+      const float a = 1.0f / std::sqrt((float)fan);
+      net.set_param(prefix + l.name + ".weight", uniform(wshape, -a, a, seed++));
+      if (l.bias_term)
+        net.set_param(prefix + l.name + ".bias", uniform({wshape[l.kind == LayerKind::CONV ? 0 : 1]}, -0.1f, 0.1f, seed++));
+    }
+  };
+  for (const LayerSpec& l : net.graph().layers) {
+    if (l.kind == LayerKind::MOE) {
+      // nested nets: "<moe>.gating.<p>", "<moe>.expert<k>.<p>" and the gate matrices
+      // "<moe>.gate_a/_b/_c" (include/qnet/net.hpp:36-40); W_b = W_c = 0 unless noise is on
+      set_params(*l.moe->gating_graph, l.name + ".gating.");
+      for (int64_t e = 0; e < l.moe->n_experts; ++e)
+        set_params(*l.moe->expert_graph, l.name + ".expert" + std::to_string(e) + ".");
+      const auto gb = infer_blobs(*l.moe->gating_graph);
+      int64_t D = 0;
+      for (const auto& kv : gb)
+        if (kv.second.consumers.empty()) D = kv.second.shape[1];
+      const float nb = l.moe->noise_enabled ? 0.3f : 0.0f;
+      net.set_param(l.name + ".gate_a", uniform({l.moe->n_experts, D}, -0.5f, 0.5f, seed++));
+      net.set_param(l.name + ".gate_b", uniform({l.moe->n_experts, D}, -nb, nb, seed++));
+      net.set_param(l.name + ".gate_c", uniform({l.moe->n_experts}, -nb, nb, seed++));
+    }
+  }
   for (const LayerSpec& l : net.graph().layers) {
     if (l.kind == LayerKind::INPUT) {
       in_name = l.tops[0];

@@ -43,6 +43,8 @@ def test_executor_fails_loudly_without_gpu():
     ("vgg16_32", "fp16", 4),
     ("alexnet", "int8", 3),
     ("alexnet", "int16", 1),
+    # Net::run_moe through qnb_moe_plan: trunk, gating, 16 expert nets, tail (configs[2])
+    ("alexnet_moe", "int8", 3),
 ])
 def test_executor_matches_reference_net(graph, precision, batch):
     r = run(graph, precision, batch)

@@ -152,3 +152,39 @@ def test_moe_plan_counts_and_graph_replay(setup):
             assert np.array_equal(outs[batch], o)
         outs[batch] = o
     assert np.array_equal(outs[17], outs[40][:17])  # per-sample independence (same seeds)
+
+
+def test_group_world1_forward_and_collectives(setup):
+    """qnb_group_* with one rank (NCCL communicator of size 1 on this GPU): the grouped
+    forward equals the plan's own forward, all-gather and all-to-all move the bytes."""
+    import torch
+    from paper_2209_15427_b200.group import Group
+    from paper_2209_15427_b200.net import QUANTIZED, Net
+    g = graphs.alexnet(1)
+    shapes = {b: v["shape"] for b, v in G.infer_blobs(g).items()}
+    params = graphs.synth_params(g, shapes)
+    with open(os.path.join(ROOT, "tests", "golden", "alexnet_int8_calib.json")) as f:
+        ranges = json.load(f)["ranges"]
+    net = Net(G.override_precision(g, "int8"))
+    for k, v in params.items():
+        net.set_param(k, v)
+    for k, (lo, hi) in ranges.items():
+        net.set_range(k, lo, hi)
+    net.finalize_quantizers()
+    net.set_quant_mode(QUANTIZED)
+    B = 8
+    plan = net.compile(B)
+    x = torch.from_numpy(graphs.synth_images(B, (3, 227, 227), offset=11)).cuda()
+    want = torch.empty((B, 1000), dtype=torch.float32, device="cuda")
+    plan.forward_device(x.data_ptr(), want.data_ptr(), B)
+    grp = Group(1, 0, Group.unique_id(), torch.cuda.current_device())
+    got = torch.zeros((B, 1000), dtype=torch.float32, device="cuda")
+    grp.forward(plan, x.data_ptr(), B, got.data_ptr(), 4000, torch.cuda.current_stream().cuda_stream)
+    src = torch.arange(64, dtype=torch.uint8, device="cuda")
+    dst = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    grp.alltoallv(src.data_ptr(), [0], [64], dst.data_ptr(), [0], [64], torch.cuda.current_stream().cuda_stream)
+    ag = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    grp.allgather(src.data_ptr(), ag.data_ptr(), 64, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert torch.equal(dst, src) and torch.equal(ag, src)
