@@ -69,7 +69,10 @@ __device__ __forceinline__ TileCoord tile_of(int64_t t, int64_t m_tiles, int n_t
 // A (cluster) tile is live when its first output row is below m_valid.  Row-Hankel
 // tiles are (image pair q, output row): live when image 2q is inside the batch.
 __device__ __forceinline__ bool tile_live(const IgemmArgs& p, int64_t cmt, int cs, int64_t mv) {
-  if (p.patch) return true;  // padded-grid tiles (no device batch in patch mode)
+  if (p.patch) {  // padded-grid tiles: live while the tile's first image is in the batch
+    if (!p.pt_pair) return true;  // (the single-CTA patch kernel takes no device batch)
+    return (cmt * cs * kBM) / ((int64_t)p.pt_hp * p.pt_wp) * p.oh * p.ow < mv;
+  }
   if (p.hk) return 2 * (cmt / p.oh) * (int64_t)p.oh * p.ow < mv;
   return cmt * cs * kBM < mv;
 }
@@ -1223,7 +1226,12 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
   uint8_t* sB = smem;
   uint8_t* sA = smem + ((b_bytes + 1023) & ~1023);
   const int a_tile = (p.hk_copy + 64 + 127) & ~127;  // + slack: the last pixels' K overrun meets zero weights
-  uint64_t* b_full = (uint64_t*)(sA + 2 * a_tile);
+  // hk_2copy: each tile's rows are copied twice, the second copy shifted by 16 bytes, so
+  // the two 16-byte K chunks of one MMA come from different buffers (LBO = buffer
+  // distance) instead of overlapping core matrices 16 B apart (LBO = 16), which ran the
+  // MMAs at about half the non-swizzled rate
+  const int ncopy = p.hk_2copy ? 2 : 1;
+  uint64_t* b_full = (uint64_t*)(sA + 2 * ncopy * a_tile);
   uint64_t* a_full = b_full + 1;
   uint64_t* a_empty = a_full + 2;
   uint64_t* acc_full = a_empty + 2;
@@ -1270,9 +1278,11 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
         const uint32_t buf = j & 1;
         mbar_wait(&a_empty[buf], ((j >> 1) & 1) ^ 1);
         const uint32_t q = (uint32_t)t / (uint32_t)p.oh, oy = (uint32_t)t - q * (uint32_t)p.oh;
-        mbar_arrive_expect_tx(&a_full[buf], (uint32_t)p.hk_copy);
-        bulk_g2s(sA + (size_t)buf * a_tile, p.a + (int64_t)q * p.a_img + p.a_origin + (int64_t)oy * p.stride_h * p.a_row,
-                 (uint32_t)p.hk_copy, &a_full[buf]);
+        const uint8_t* src = p.a + (int64_t)q * p.a_img + p.a_origin + (int64_t)oy * p.stride_h * p.a_row;
+        mbar_arrive_expect_tx(&a_full[buf], (uint32_t)(ncopy * p.hk_copy));
+        bulk_g2s(sA + (size_t)buf * ncopy * a_tile, src, (uint32_t)p.hk_copy, &a_full[buf]);
+        if (ncopy == 2)  // the same rows 16 bytes later (the arena keeps >= 1 KB past every blob)
+          bulk_g2s(sA + (size_t)buf * ncopy * a_tile + a_tile, src + 16, (uint32_t)p.hk_copy, &a_full[buf]);
       }
     }
     __syncwarp();
@@ -1294,7 +1304,7 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
         tc_fence_after();
         const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
         // M rows 0-63: image 2q, pixel m at 16 m; rows 64-127: image 2q+1 (+1024)
-        const uint64_t ad0 = smem_desc_none(sA + (size_t)buf * a_tile, 16, 128);
+        const uint64_t ad0 = smem_desc_none(sA + (size_t)buf * ncopy * a_tile, ncopy == 2 ? (uint32_t)a_tile : 16u, 128);
         if (elect_one()) {
           if (mma_on)
             for (int r = 0; r < p.hk_rows; ++r)
@@ -1672,6 +1682,216 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_patch_kernel(const __grid_c
   }
 }
 
+// ------------------------------------------------------------ CTA-pair patch kernel
+// Patch mode (see IgemmArgs::patch) on a cta_group::2 pair: a pair tile is 256 consecutive
+// pixels of the padded output grid, rank r owning pixels [P0_r, P0_r + 128), P0_r =
+// (2 * pair_tile + r) * 128.  Each CTA gathers the input SLAB of its pixels once per
+// channel chunk -- slab row q = padded-grid pixel P0_r + q, q < 128 + (kh-1)*wp + kw-1 --
+// so a filter tap (r, s) is an MMA whose A descriptor starts r*wp + s rows into the slab,
+// the same row offset in both CTAs (the 128B/64B/32B swizzle is absolute-address based).
+// A leaves L2 ~2x per tile instead of kh*kw times (the im2col gather's amplification),
+// and B of one (group, n-tile) stays resident, half in each CTA.  Synchronisation as in
+// igemm_pair_kernel: rank 1's warp 4 forwards each filled slab to rank 0's full barrier,
+// the pair commits multicast to both CTAs' empty / acc_full barriers.
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 1) igemm_ppatch_kernel(const __grid_constant__ IgemmArgs p) {
+  griddep_launch_dependents();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int kbA = p.pt_kb;                  // chunk width: the A swizzle span (128 / 64 / 32 bytes)
+  const int slab = p.pt_plane;              // bytes of one chunk slab (1024-aligned)
+  const int AST = p.pt_astg;                // slab ring depth
+  const int nb2 = p.n_rows >> 1;            // B rows held by this CTA
+  const int bh = nb2 * 128;                 // bytes of one K block of the B half
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)AST * slab;
+  uint64_t* full = (uint64_t*)(sB + (size_t)p.num_kb * bh);
+  uint64_t* empty = full + kPatchStages;
+  uint64_t* acc_full = empty + kPatchStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bfull = acc_empty + 2;
+  uint64_t* bpeer = bfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(bpeer + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int64_t grid_pix = (p.m_total / ((int64_t)p.oh * p.ow)) * p.pt_hp * p.pt_wp;
+  const int64_t m_tiles = (grid_pix + kBM - 1) / kBM;
+  const int64_t m_pairs = (m_tiles + 1) / 2;
+  const int taps = p.pt_kh * p.pt_kw;
+  const int nk = kbA >> 5;                  // K steps per (chunk, tap)
+  const int nchunk = p.pt_pairs;            // channel chunks per tap
+  // pairs split evenly over the (group, n-tile) combinations; each walks its m-pairs
+  const int combos = p.groups * p.n_tiles;
+  const int64_t pid = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int64_t ppc = npairs / combos;
+  const int64_t cmb = pid / ppc;
+  const bool idle = cmb >= combos;
+  const int64_t cid = idle ? 0 : cmb * m_pairs + (pid - cmb * ppc);
+  const int64_t ncl = ppc;
+  const int64_t total = idle ? 0 : (cmb + 1) * m_pairs;
+  const int g_ = idle ? 0 : (int)(cmb / p.n_tiles), nt_ = idle ? 0 : (int)(cmb % p.n_tiles);
+  const int64_t mv = m_valid(p);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < AST; ++i) {
+      mbar_init(&full[i], 128u + (rank == 0 ? 1u : 0u));
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 2 * kEpiWarps);
+    }
+    mbar_init(bfull, 1);
+    mbar_init(bpeer, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc2(tmem_slot, (uint32_t)(2 * p.tmem_cols));
+    tmem_relinquish2();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp != 4) griddep_wait();
+  if (warp < 4) {
+    // ------------------------------------------------------------------ slab producers
+    const int t = threadIdx.x;
+    const int64_t y_tot = (p.m_total / ((int64_t)p.oh * p.ow)) * p.pt_hp;  // rows of the merged N*H_p grid
+    const int nsub_sh = kbA == 128 ? 3 : (kbA == 64 ? 2 : 1);  // 16-byte sub-chunks per slab row
+    const int items = p.pt_slab_rows << nsub_sh;
+    const uint32_t wp = (uint32_t)p.pt_wp;
+    uint32_t ia = 0;
+    for (int64_t ct = cid; ct < total; ct += ncl) {
+      if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+      const int64_t mt = (ct % m_pairs) * 2 + rank;
+      const uint32_t P0 = (uint32_t)(mt * kBM);
+      for (int cc = 0; cc < nchunk; ++cc, ++ia) {
+        const int s = (int)(ia % AST);
+        mbar_wait(&empty[s], ((ia / AST) & 1) ^ 1);
+        const int64_t cbyte = (int64_t)g_ * p.a_group + (int64_t)cc * kbA;
+        uint8_t* dst = sA + (size_t)s * slab;
+        for (int i = t; i < items; i += 128) {
+          const uint32_t q = (uint32_t)i >> nsub_sh, jc = (uint32_t)i & ((1u << nsub_sh) - 1u);
+          const uint32_t G = P0 + q;
+          int64_t y = G / wp;
+          const uint32_t x = G - (uint32_t)y * wp;
+          y = y < y_tot ? y : y_tot - 1;  // pixels past the last image only feed discarded outputs
+          const uint32_t swz = nsub_sh == 3 ? (q & 7u) : (nsub_sh == 2 ? ((q >> 1) & 3u) : ((q >> 2) & 1u));
+          cp_async_16(dst + (size_t)q * kbA + ((jc ^ swz) << 4), p.a + y * p.a_row + (int64_t)x * p.a_pix + cbyte + jc * 16);
+        }
+        cp_async_arrive_noinc(&full[s]);
+      }
+    }
+  } else if (warp == 4) {
+    // resident B half of this pair's (group, n-tile): rows [rank * nb2, +nb2) of every K block
+    if (!idle && elect_one()) {
+      mbar_arrive_expect_tx(bfull, (uint32_t)(p.num_kb * bh));
+      const uint8_t* bg = p.b + (int64_t)(g_ * p.n_tiles + nt_) * p.num_kb * (p.n_rows * 128);
+      for (int kb = 0; kb < p.num_kb; ++kb)
+        bulk_g2s(sB + (size_t)kb * bh, bg + (int64_t)kb * p.n_rows * 128 + (int64_t)rank * bh, (uint32_t)bh, bfull);
+    }
+    __syncwarp();
+    griddep_wait();
+    if (!idle) mbar_wait(bfull, 0);
+    if (rank == 1) {
+      // ------------------------------------------------------- forwarder (rank 1)
+      if (!idle && elect_one()) mbar_arrive_cluster(bpeer, 0);
+      __syncwarp();
+      uint32_t ia = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        for (int cc = 0; cc < nchunk; ++cc, ++ia) {
+          const int s = (int)(ia % AST);
+          mbar_wait(&full[s], (ia / AST) & 1);
+          if (elect_one()) {
+            fence_proxy_async_smem();
+            mbar_arrive_cluster(&full[s], 0);
+          }
+          __syncwarp();
+        }
+      }
+    } else if (!idle) {
+      // ------------------------------------------------------- MMA issuer (rank 0)
+      mbar_wait_cluster(bpeer, 0);
+      uint32_t idesc = make_idesc<KIND>(p.n_rows);
+      idesc = (idesc & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24);  // M = 256 (pair)
+      const bool mma_on = !(p.dbg & 2);
+      const uint64_t bd0 = smem_desc_sw128(sB);
+      const uint32_t b_units = (uint32_t)(bh >> 4);
+      const uint32_t row_units = (uint32_t)(kbA >> 4);
+      const uint32_t wp = (uint32_t)p.pt_wp;
+      uint32_t ia = 0, jn = 0;
+      for (int64_t ct = cid; ct < total; ct += ncl) {
+        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        const uint32_t j = jn++;
+        const uint32_t buf = j & 1;
+        mbar_wait_cluster(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + buf * (uint32_t)p.tmem_cols;
+        int kk = 0;
+        for (int cc = 0; cc < nchunk; ++cc, ++ia) {
+          const int s = (int)(ia % AST);
+          mbar_wait_cluster(&full[s], (ia / AST) & 1);
+          tc_fence_after();
+          const uint64_t ad0 = smem_desc_sw(sA + (size_t)s * slab, kbA);
+          if (elect_one()) {
+            if (mma_on)
+              for (int r = 0; r < p.pt_kh; ++r)
+                for (int tt = 0; tt < p.pt_kw; ++tt)
+                  for (int q = 0; q < nk; ++q) {
+                    const int k2 = kk + (r * p.pt_kw + tt) * nk + q;
+                    umma2_i8(dt, ad0 + (uint32_t)(r * wp + tt) * row_units + 2 * q,
+                             bd0 + (uint32_t)(k2 >> 2) * b_units + 2 * (k2 & 3), idesc, k2 != 0);
+                  }
+            tc_commit2_multicast(&empty[s], 3);
+          }
+          __syncwarp();
+          kk += taps * nk;
+        }
+        if (elect_one()) tc_commit2_multicast(&acc_full[buf], 3);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    run_epilogue(p, tmem, acc_full, acc_empty, m_pairs, total, cid, ncl, 2, rank, warp, lane, nullptr, (warp - 5) >> 2,
+                 2);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, (uint32_t)(2 * p.tmem_cols));
+  }
+}
+
+static size_t igemm_ppatch_smem_bytes(const IgemmArgs& a) {
+  return 1024 + (size_t)a.pt_astg * a.pt_plane + (size_t)a.num_kb * (a.n_rows / 2) * 128 + (2 * kPatchStages + 6) * 8 +
+         16;
+}
+
+// Pair-patch configuration: the widest n-tile whose B half stays resident next to a slab
+// ring of >= 2 stages.  Returns false when none fits.
+bool igemm_ppatch_config(const IgemmGeometry& g, int64_t num_kb, int32_t slab, int* npt_out, int* astg_out) {
+  const size_t budget = 220 * 1024;
+  for (int npt : {240, 192, 128, 112, 96, 64, 48, 32}) {
+    if (npt > round_up(g.og, 16) && npt != 32) continue;
+    const int64_t n_rows = round_up(npt + 1, 16);
+    if ((n_rows / 2) % 8 != 0) continue;  // each CTA's B half must be whole 8-row SW128 atoms
+    const size_t b = (size_t)num_kb * (n_rows / 2) * 128;
+    if (b + 2 * (size_t)slab + 2048 > budget) continue;
+    *npt_out = npt;
+    *astg_out = (int)std::min<size_t>(kPatchStages, (budget - b - 2048) / (size_t)slab);
+    return true;
+  }
+  return false;
+}
+
 static size_t igemm_patch_smem_bytes(const IgemmArgs& a, int sb) {
   return 1024 + (size_t)a.pt_astg * a.pt_ppst * a.pt_plane + (size_t)sb * a.n_rows * 128 +
          (2 * kPatchStages + 2 * kMaxStages + 4) * 8 + 16 + 256;
@@ -1754,7 +1974,8 @@ bool igemm_patch_config(const IgemmGeometry& g, int64_t num_kb, int32_t plane, i
 }
 
 static size_t igemm_hk_smem_bytes(const IgemmArgs& a) {
-  return 1024 + (size_t)(((a.num_kb * a.n_rows * 128) + 1023) & ~1023) + 2 * (size_t)((a.hk_copy + 64 + 127) & ~127) +
+  return 1024 + (size_t)(((a.num_kb * a.n_rows * 128) + 1023) & ~1023) +
+         2 * (a.hk_2copy ? 2 : 1) * (size_t)((a.hk_copy + 64 + 127) & ~127) +
          9 * 8 + 16 + 256;
 }
 
@@ -2228,8 +2449,46 @@ static qnb_status launch_hk(const IgemmArgs& a, cudaStream_t s) {
   return QNB_OK;
 }
 
+static qnb_status launch_ppatch(const IgemmArgs& a0, int64_t groups, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    QNB_CUDA(cudaFuncSetAttribute(igemm_ppatch_kernel<KIND_I8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr_set = true;
+  }
+  IgemmArgs a = a0;
+  a.groups = (int32_t)groups;
+  a.pair = 1;
+  const size_t smem = igemm_ppatch_smem_bytes(a);
+  if (smem > 227 * 1024) return fail(QNB_E_UNSUPPORTED, "pair patch tile exceeds shared memory");
+  const int64_t combos = (int64_t)a.n_tiles * groups;
+  const int64_t grid_pix = (a.m_total / ((int64_t)a.oh * a.ow)) * a.pt_hp * a.pt_wp;
+  const int64_t m_pairs = ceil_div(ceil_div(grid_pix, kBM), 2);
+  const int64_t ppc = std::max<int64_t>(1, std::min<int64_t>(num_sms() / 2 / combos, m_pairs));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * ppc * combos));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  set_pdl(attr[1]);
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_on() ? 2 : 1;
+  QNB_CUDA(cudaLaunchKernelEx(&cfg, igemm_ppatch_kernel<KIND_I8>, a));
+  count_launch();
+  QNB_CUDA(cudaGetLastError());
+  return QNB_OK;
+}
+
 template <int KIND>
 static qnb_status launch_patch(const IgemmArgs& a0, int64_t groups, cudaStream_t s) {
+  if constexpr (KIND == KIND_I8) {
+    if (a0.pt_pair) return launch_ppatch(a0, groups, s);
+  }
   static bool attr_set = false;
   if (!attr_set) {
     QNB_CUDA(cudaFuncSetAttribute(igemm_patch_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));

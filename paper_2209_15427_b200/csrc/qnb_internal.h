@@ -190,6 +190,7 @@ struct IgemmArgs {
   // output pixel m's K bytes start at byte 16*m = m*stride_w*pixel of the input row,
   // so no im2col is ever materialised.  B (weights) stays resident in smem.
   int32_t hk, hk_rows, hk_kpr, hk_copy, hk_pairs;  // hk_copy: bytes per tile; hk_pairs: image pairs
+  int32_t hk_2copy;  // A rows copied twice (second shifted 16 B): non-overlapping MMA operand
   int32_t dbg;  // profiling probes (env QNB_IGEMM_DBG): 1 epilogue skips its math, 2 no MMAs
   // Patch mode (patch = 1; stride-1 convs over NHWC): output pixels live on the padded
   // grid of the input (row pitch pt_wp, pt_hp rows per image; rows/columns outside the
@@ -203,6 +204,11 @@ struct IgemmArgs {
   // owns one such combination and walks its pixel tiles (weights leave L2 once per CTA).
   int32_t pt_bstat;
   int32_t pt_ppst, pt_astg;  // channel chunks per A stage, A stages in the ring (<= 4)
+  // pt_pair = 1: patch mode on a CTA pair (igemm_ppatch_kernel): M = 256 tiles of the
+  // padded grid (cta_group::2), each CTA gathers the slab of its own 128 pixels (the slab
+  // starts AT the tile's first pixel, so one descriptor serves both CTAs), B of one
+  // (group, n-tile) resident as halves across the pair
+  int32_t pt_pair, pt_slab_rows;
   int32_t pt_kb;             // channel-chunk width in bytes (128 / 64 / 32 = the A swizzle span)
 };
 // Row-Hankel mode: the input is image-pair interleaved with 1024-byte row slots, so
@@ -285,6 +291,7 @@ qnb_status plan_prepare_host_io(qnb_plan* P, bool input_on_host, bool output_on_
 bool igemm_splitk_fused_ok(const IgemmArgs& a, int64_t groups);
 // True when the tap-major chunk table of `pk` can be served by TMA im2col chunk planes;
 // encodes the 16-byte-channel im2col tensor map.
+bool igemm_ppatch_config(const IgemmGeometry& g, int64_t num_kb, int32_t slab, int* npt_out, int* astg_out);
 bool igemm_planes_eligible(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk);
 qnb_status igemm_encode_tma_planes(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base,
                                    CUtensorMap* map);

@@ -560,17 +560,43 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   // Patch mode is opt-in (QNB_PATCH=1) until it beats the cp.async gather; TMA im2col
   // is used where a tap's channels fill whole 128-byte stages (measured faster there).
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
-  const bool patch = !hk && use_patch && igemm_patch_eligible(g, Lin);
+  // Pair patch (default for INT8 stride-1 convs whose halo is their padding): the CTA
+  // pair gathers each tile's input slab once instead of kh*kw im2col rows
+  static const bool no_ppatch = std::getenv("QNB_NO_PPATCH") != nullptr;
+  const bool ppatch_try = !hk && !no_ppatch && quant && dtype == QNB_INT8Q && !g.is_fc &&
+                          igemm_patch_eligible(g, Lin);
+  bool ppatch = false;
+  int32_t pp_slab = 0, pp_astg = 0, pp_rows = 0;
+  const bool patch0 = !hk && (use_patch || ppatch_try) && igemm_patch_eligible(g, Lin);
   static const int tma_align = std::getenv("QNB_TMA64") ? 64 : 128;  // A/B: 64-byte (SW64) im2col stages
   // TMA im2col boxes are 128 consecutive output pixels: on narrow outputs (AlexNet conv3,
   // 13 wide) one box wraps ~10 rows and the CTA-pair gather measured faster (+0.6 %)
+  bool patch = patch0;
   const bool tma = !hk && !patch && !no_tma && igemm_tma_eligible(g, Lin) && (g.cg * Lin.es()) % tma_align == 0 &&
                    g.ow >= 16;
   int32_t pt_pairs = 0, pt_kb = 128;
   if (hk)
     QNB_TRY(igemm_plan_hk(g, Lin, &pk, &hk_kpr));
-  else if (patch)
+  else if (patch) {
     QNB_TRY(igemm_plan_patch(g, Lin, &pk, &pt_pairs, &pt_kb));
+    if (ppatch_try) {
+      const int64_t wp = Lin.w + 2 * g.pw;
+      const int64_t srows = 128 + (g.kh - 1) * wp + (g.kw - 1);  // the tile's 128 pixels + the filter reach
+      const int32_t slab = (int32_t)round_up(srows * pt_kb, 1024);
+      int npt = 0, astg = 0;
+      if (igemm_ppatch_config(g, pk.num_kb, slab, &npt, &astg)) {
+        ppatch = true;
+        pk.n_per_tile = npt;
+        pp_slab = slab;
+        pp_astg = astg;
+        pp_rows = (int32_t)srows;
+      } else if (!use_patch) {  // no resident-B pair configuration: the usual engines
+        patch = false;
+        pk = IgemmPacked();
+        QNB_TRY(igemm_plan_k(g, Lin, &pk));
+      }
+    }
+  }
   else if (tma)
     QNB_TRY(igemm_plan_tma(g, Lin, &pk));
   else
@@ -588,7 +614,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   }
   int32_t pt_bstat_npt = 0;
   int pt_ppst = 1, pt_astg = 2;
-  if (patch) {
+  if (patch && !ppatch) {
     const int64_t wp = Lin.w + 2 * g.pw;
     const int64_t rows = (wp + 125 + g.kw) / wp + g.kh;
     int npt = 0;
@@ -630,6 +656,14 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     a.pt_bstat = pt_bstat_npt > 0 ? 1 : 0;
     a.pt_ppst = pt_ppst;
     a.pt_astg = pt_astg;
+    if (ppatch) {  // CTA-pair patch: one slab per (tile, chunk), starting at the tile's pixel
+      a.pt_pair = 1;
+      a.pt_plane = pp_slab;
+      a.pt_astg = pp_astg;
+      a.pt_slab_rows = pp_rows;
+      a.pt_bstat = 0;
+      a.pt_ppst = 1;
+    }
   }
   if (tma) {
     a.a_tma = 1;
@@ -650,6 +684,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     a.hk_kpr = hk_kpr;
     a.hk_copy = (int32_t)(g.kh * Lin.row());           // kh rows of one image pair
     a.hk_pairs = (int32_t)ceil_div(Lin.n, 2);
+    a.hk_2copy = std::getenv("QNB_HK_1COPY") ? 0 : 1;
   }
   a.n_rows = pk.n_rows;
   a.n_tiles = pk.n_tiles;
@@ -1290,7 +1325,8 @@ qnb_status qnb_plan_forward_dyn(qnb_plan* P, const void* input, int64_t batch_ca
     if (batch_cap < 1 || batch_cap > P->max_batch) return fail(QNB_E_SHAPE, "shape mismatch");
     if (P->flags & QNB_PLAN_OBSERVE) return fail(QNB_E_UNSUPPORTED, "device batch with an OBSERVE plan");
     for (const Step& st : P->steps)
-      if (st.kind == OP_IGEMM && st.ig.patch) return fail(QNB_E_UNSUPPORTED, "device batch with patch-mode GEMMs");
+      if (st.kind == OP_IGEMM && st.ig.patch && !st.ig.pt_pair)
+        return fail(QNB_E_UNSUPPORTED, "device batch with single-CTA patch-mode GEMMs");
     P->dyn_n = dyn_batch;
     const qnb_status st = launch_steps(*P, batch_cap, input, output, as_stream(s_));
     P->dyn_n = nullptr;
