@@ -282,7 +282,7 @@ qnb_status run_contraction(const IgemmGeometry& g, int dtype, const ContractionI
     a.hk_kpr = hk_kpr;
     a.hk_copy = (int32_t)(g.kh * io.in.row());           // kh rows of one image pair
     a.hk_pairs = (int32_t)ceil_div(io.in.n, 2);
-    a.hk_2copy = std::getenv("QNB_HK_1COPY") ? 0 : 1;
+    a.hk_2copy = std::getenv("QNB_HK_2COPY") ? 1 : 0;
   }
   a.n_rows = pk.n_rows;
   a.n_tiles = pk.n_tiles;

@@ -560,10 +560,13 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   // Patch mode is opt-in (QNB_PATCH=1) until it beats the cp.async gather; TMA im2col
   // is used where a tap's channels fill whole 128-byte stages (measured faster there).
   static const bool use_patch = std::getenv("QNB_PATCH") != nullptr;
-  // Pair patch (default for INT8 stride-1 convs whose halo is their padding): the CTA
-  // pair gathers each tile's input slab once instead of kh*kw im2col rows
-  static const bool no_ppatch = std::getenv("QNB_NO_PPATCH") != nullptr;
-  const bool ppatch_try = !hk && !no_ppatch && quant && dtype == QNB_INT8Q && !g.is_fc &&
+  // Pair patch (opt-in, QNB_PPATCH=1): the CTA pair gathers each tile's input slab once
+  // instead of kh*kw im2col rows.  Bit-exact, but measured SLOWER on AlexNet conv2-5
+  // (155 / 64 / 61 / 55 us vs 136 / 58 / 51 / 43 us for the gather): the tap MMAs start at
+  // row offsets that are not multiples of the 8-row swizzle atom and ran at ~230 cycles
+  // (vs 72 for the gather's aligned stages)
+  static const bool want_ppatch = std::getenv("QNB_PPATCH") != nullptr;
+  const bool ppatch_try = !hk && want_ppatch && quant && dtype == QNB_INT8Q && !g.is_fc &&
                           igemm_patch_eligible(g, Lin);
   bool ppatch = false;
   int32_t pp_slab = 0, pp_astg = 0, pp_rows = 0;
@@ -684,7 +687,7 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     a.hk_kpr = hk_kpr;
     a.hk_copy = (int32_t)(g.kh * Lin.row());           // kh rows of one image pair
     a.hk_pairs = (int32_t)ceil_div(Lin.n, 2);
-    a.hk_2copy = std::getenv("QNB_HK_1COPY") ? 0 : 1;
+    a.hk_2copy = std::getenv("QNB_HK_2COPY") ? 1 : 0;  // measured neutral (142 vs 143 us): opt-in
   }
   a.n_rows = pk.n_rows;
   a.n_tiles = pk.n_tiles;
