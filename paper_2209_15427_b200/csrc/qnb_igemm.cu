@@ -57,12 +57,26 @@ struct TileCoord {
   int nt, g;
 };
 // Tile order: m fastest, so the CTAs resident at any moment share one B tile in L2.
+// Tile indices stay below 2^31 (host-checked m_total < 2^31): 32-bit unsigned divisions,
+// and none when there is a single (n-tile, group) column (the row-Hankel kernel).
 __device__ __forceinline__ TileCoord tile_of(int64_t t, int64_t m_tiles, int n_tiles) {
   TileCoord c;
-  c.mt = t % m_tiles;
-  const int64_t r = t / m_tiles;
-  c.nt = (int)(r % n_tiles);
-  c.g = (int)(r / n_tiles);
+  const uint32_t tt = (uint32_t)t, mm = (uint32_t)m_tiles;
+  if (tt < mm) {
+    c.mt = tt;
+    c.nt = 0;
+    c.g = 0;
+    return c;
+  }
+  const uint32_t r = tt / mm;
+  c.mt = tt - r * mm;
+  if (n_tiles == 1) {
+    c.nt = 0;
+    c.g = (int)r;
+  } else {
+    c.nt = (int)(r % (uint32_t)n_tiles);
+    c.g = (int)(r / (uint32_t)n_tiles);
+  }
   return c;
 }
 
@@ -73,7 +87,7 @@ __device__ __forceinline__ bool tile_live(const IgemmArgs& p, int64_t cmt, int c
     if (!p.pt_pair) return true;  // (the single-CTA patch kernel takes no device batch)
     return (cmt * cs * kBM) / ((int64_t)p.pt_hp * p.pt_wp) * p.oh * p.ow < mv;
   }
-  if (p.hk) return 2 * (cmt / p.oh) * (int64_t)p.oh * p.ow < mv;
+  if (p.hk) return 2 * (int64_t)((uint32_t)cmt / (uint32_t)p.oh) * p.oh * p.ow < mv;
   return cmt * cs * kBM < mv;
 }
 
@@ -358,9 +372,9 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
   const int64_t mv = m_valid(p);
   uint32_t jn = 0;
   for (int64_t ct = cid; ct < total; ct += ncl) {
-    if (!tile_live(p, ct % m_groups, cs, mv)) continue;
-    const uint32_t j = jn++;
     const TileCoord c0 = tile_of(ct, m_groups, n_tiles * p.ksplit);
+    if (!tile_live(p, c0.mt, cs, mv)) continue;
+    const uint32_t j = jn++;
     const int ks = c0.nt % p.ksplit;
     TileCoord c = c0;
     c.nt = c0.nt / p.ksplit;
@@ -731,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_a)) : "memory");
       uint32_t it = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_groups, cs, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_groups), cs, mv)) continue;
         const TileCoord c = tile_of(ct, m_groups, p.n_tiles * p.ksplit);
         const int64_t mt = c.mt * cs + rank;
         const uint32_t row0 = (uint32_t)(mt * kBM);
@@ -766,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
     const int jc = lane & 7, rr = lane >> 3;
     uint32_t it = 0, par = 0;
     for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
-      if (!tile_live(p, ct % m_groups, cs, mv)) continue;
+      if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_groups), cs, mv)) continue;
       const TileCoord c = tile_of(ct, m_groups, p.n_tiles * p.ksplit);
       const int64_t mt = c.mt * cs + rank;
       {  // one row decomposition per thread, shared through smem
@@ -832,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
       const int nk = kbytes >> 5;
       uint32_t it = 0, jn = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_groups, cs, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_groups), cs, mv)) continue;
         const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
@@ -909,10 +923,9 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   uint32_t* tmem_slot = (uint32_t*)(bpeer + 1);
   int64_t* rowoff = (int64_t*)(tmem_slot + 4);   // [2][128]
   int32_t* chunk_s = (int32_t*)(rowoff + 256);
-  uint8_t* slabs = (uint8_t*)(((uintptr_t)(chunk_s + kMaxChunkSmem) + 127) & ~(uintptr_t)127);  // a_slab
   const int n_chunks = p.num_kb * 8;
   const bool chunks_in_smem = n_chunks <= kMaxChunkSmem;
-  const int32_t* ctab_g = p.a_slab ? p.sl_tab : p.chunk_off;
+  const int32_t* ctab_g = p.chunk_off;
   if (chunks_in_smem)
     for (int i = threadIdx.x; i < n_chunks; i += blockDim.x) chunk_s[i] = __ldg(ctab_g + i);
   const int32_t* chunk_tab = chunks_in_smem ? chunk_s : ctab_g;
@@ -974,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       uint32_t st_ph = 0;
       int st_s = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
         const TileCoord c = tile_of(ct, m_pairs, ntk);
         const int64_t mt = c.mt * 2 + rank;
         const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
@@ -1016,7 +1029,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       uint32_t st_ph = 0;
       int st_s = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
         const TileCoord c = tile_of(ct, m_pairs, ntk);
         const int64_t mt = c.mt * 2 + rank;
         const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
@@ -1036,113 +1049,6 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
         }
       }
     }
-  } else if (warp < 4 && p.a_slab) {
-    // ------------------------------------------------------- slab-staged producers
-    // Per tile: (1) cp.async the tile's input slab (group channels of the merged padded
-    // rows it touches) into slab buffer b -- issued one tile AHEAD when two buffers fit;
-    // (2) every A stage is built from the slab with 16-byte ld.shared / st.shared into the
-    // 128B-swizzled layout, fenced for the async proxy, then the stage's barrier arrival.
-    const int t = threadIdx.x;
-    const int jc = lane & 7, rr = lane >> 3;
-    const int spb = p.sl_spb, cps = p.sl_spb >> 4, wp = p.sl_wp;
-    const int64_t hp = p.sl_hp;
-    uint32_t st_ph = 0;
-    int st_s = 0;
-    // merged padded row of output row `row` (image-major, hp rows per image)
-    auto ymerged = [&](int64_t row) -> int64_t {
-      const uint32_t img = (uint32_t)row / (uint32_t)pix_per_img;
-      const uint32_t rem = (uint32_t)row - img * (uint32_t)pix_per_img;
-      return (int64_t)img * hp + rem / (uint32_t)p.ow;
-    };
-    // cp.async of tile ct's slab into buffer `buf` (one commit group per call)
-    auto fetch = [&](int64_t ct, int buf) {
-      const TileCoord c = tile_of(ct, m_pairs, ntk);
-      const int64_t r0 = (c.mt * 2 + rank) * kBM;
-      if (r0 < p.m_total) {
-        const int64_t r1 = min(p.m_total, r0 + kBM) - 1;
-        const int64_t y0 = ymerged(r0);
-        const int nrows = (int)(ymerged(r1) + p.pt_kh - y0);
-        const int items = nrows * wp * cps;
-        const uint8_t* src0 = p.a + p.a_origin + y0 * p.a_row + (int64_t)c.g * p.a_group;
-        uint8_t* dst0 = slabs + (size_t)buf * p.sl_bytes;
-        for (int i = t; i < items; i += 128) {
-          const int px = i / cps, cc = i - px * cps;
-          const int sy = px / wp, sx = px - sy * wp;
-          cp_async_16(dst0 + (size_t)px * spb + cc * 16, src0 + (int64_t)sy * p.a_row + (int64_t)sx * p.a_pix + cc * 16);
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    auto next_live = [&](int64_t ct) -> int64_t {
-      for (; ct < total; ct += ncl)
-        if (tile_live(p, ct % m_pairs, 2, mv)) return ct;
-      return total;
-    };
-    int64_t ct = next_live(cid);
-    if (ct < total) fetch(ct, 0);
-    for (int j = 0; ct < total; ++j) {
-      const int b = p.sl_nbuf == 2 ? (j & 1) : 0;
-      const int64_t nxt = next_live(ct + ncl);
-      if (p.sl_nbuf == 2 && nxt < total) fetch(nxt, b ^ 1);  // the next slab under this tile's stages
-      else asm volatile("cp.async.commit_group;" ::: "memory");
-      const TileCoord c = tile_of(ct, m_pairs, ntk);
-      const int64_t mt = c.mt * 2 + rank;
-      const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
-      const int kb0 = ks * p.kb_per_split, kb1 = min(p.num_kb, kb0 + p.kb_per_split);
-      const uint8_t* bsrc = p.b + ((int64_t)(c.g * p.n_tiles + ntile) * p.num_kb) * (p.n_rows * 128) + (int64_t)rank * bh;
-      {  // this thread's pixel: its window origin inside the slab
-        const int64_t row = mt * kBM + t;
-        int64_t off = -1;
-        if (row < p.m_total) {
-          const int64_t y0 = ymerged(mt * kBM);
-          const uint32_t img = (uint32_t)row / (uint32_t)pix_per_img;
-          const uint32_t rem = (uint32_t)row - img * (uint32_t)pix_per_img;
-          const uint32_t oy = rem / (uint32_t)p.ow, ox = rem - oy * (uint32_t)p.ow;
-          off = (((int64_t)img * hp + oy - y0) * wp + ox) * spb;
-        }
-        rowoff[(j & 1) * 128 + t] = off;
-      }
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this thread's copies of slab b landed
-      asm volatile("bar.sync 2, 128;" ::: "memory");          // ... and every producer's
-      const uint8_t* slab = slabs + (size_t)b * p.sl_bytes;
-      int32_t soff[8];
-      uint32_t valid = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t off = rowoff[(j & 1) * 128 + warp * 32 + rr + 4 * i];
-        soff[i] = (int32_t)(off < 0 ? 0 : off);
-        valid |= (off >= 0 ? 1u : 0u) << i;
-      }
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int s = st_s;
-        mbar_wait(&empty[s], st_ph ^ 1);
-        if (++st_s == S) {
-          st_s = 0;
-          st_ph ^= 1;
-        }
-        if (stream && t == 0) {
-          mbar_arrive_expect_tx(&full[s], (uint32_t)bh);
-          bulk_g2s(sB + (size_t)s * bh, bsrc + (int64_t)kb * p.n_rows * 128, (uint32_t)bh, &full[s]);
-        }
-        const int32_t off = chunk_tab[kb * 8 + jc];
-        uint8_t* dst = sA + (size_t)s * a_stage;
-        uint4 v[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (valid & (1u << i)) v[i] = *reinterpret_cast<const uint4*>(slab + soff[i] + off);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = warp * 32 + rr + 4 * i;
-          if (valid & (1u << i)) *reinterpret_cast<uint4*>(dst + row * 128 + ((jc ^ (row & 7)) << 4)) = v[i];
-        }
-        fence_proxy_async_smem();  // generic-proxy stores -> the tensor core's async-proxy reads
-        mbar_arrive(&full[s]);
-      }
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // slab b fully read before it is refilled
-      if (p.sl_nbuf != 2 && nxt < total) fetch(nxt, 0);
-      ct = nxt;
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else if (warp < 4) {
     // ---------------------------------------------------------------- producers
     const int t = threadIdx.x;
@@ -1150,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
     uint32_t par = 0, st_ph = 0;
     int st_s = 0;
     for (int64_t ct = cid; ct < total; ct += ncl, par ^= 1) {
-      if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+      if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
       const TileCoord c = tile_of(ct, m_pairs, ntk);
       const int64_t mt = c.mt * 2 + rank;
       const int ntile = c.nt / p.ksplit, ks = c.nt - ntile * p.ksplit;
@@ -1224,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       int st_s = 0;
       uint32_t st_ph = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
         const TileCoord c = tile_of(ct, m_pairs, ntk);
         const int ks = c.nt % p.ksplit;
         const int nkb = min(p.num_kb, (ks + 1) * p.kb_per_split) - ks * p.kb_per_split;
@@ -1251,7 +1157,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
       uint32_t jn = 0, st_ph = 0;
       int st_s = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
         const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait_cluster(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
@@ -1524,38 +1430,6 @@ qnb_status igemm_encode_tma(const IgemmGeometry& g, const ActLayout& in, const u
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(QNB_E_CUDA, "cuTensorMapEncodeIm2col failed: " + std::to_string((int)r));
   return QNB_OK;
-}
-
-bool igemm_slab_plan(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk, int64_t max_batch,
-                     std::vector<int32_t>* tab, int32_t* spb_out, int32_t* wp_out, int32_t* bytes_out) {
-  if (g.kind != KIND_I8 || g.q16 || g.is_fc || in.pair_slot != 0 || in.es() != 1) return false;
-  if (g.sh != 1 || g.sw != 1 || in.hh != g.ph || in.hw != g.pw || in.img() != in.hp() * in.row()) return false;
-  if (in.pix() % 16 != 0 || in.row() % 16 != 0 || in.interior_offset() % 16 != 0) return false;
-  const int64_t spb = pk.all_groups || g.groups == 1 ? in.pix() : g.cg * in.es();
-  if (spb % 16 != 0 || (g.groups > 1 && pk.all_groups)) return false;
-  const int64_t wp = in.w + 2 * in.hw, hp = in.hp();
-  // chunk table -> slab byte offsets: (r, s, channel byte) relative to the window origin
-  tab->assign(pk.chunk_off.size(), 0);
-  for (size_t k = 0; k < pk.chunk_off.size(); ++k) {
-    const int64_t o = pk.chunk_off[k];
-    const int64_t r = o / in.row(), rem = o - r * in.row(), sx = rem / in.pix(), cb = rem - sx * in.pix();
-    if (cb % 16 != 0 || cb + 16 > spb || r >= g.kh || sx >= wp) return false;
-    (*tab)[k] = (int32_t)((r * wp + sx) * spb + cb);
-  }
-  // slab rows of a tile: merged padded rows [y(first pixel), y(last pixel) + kh)
-  const int64_t ppi = g.oh * g.ow, m_total = max_batch * ppi;
-  int64_t rmax = 0;
-  for (int64_t r0 = 0; r0 < m_total; r0 += kBM) {
-    const int64_t r1 = std::min(m_total, r0 + kBM) - 1;
-    const int64_t y0 = (r0 / ppi) * hp + (r0 % ppi) / g.ow, y1 = (r1 / ppi) * hp + (r1 % ppi) / g.ow;
-    rmax = std::max(rmax, y1 + g.kh - y0);
-  }
-  const int64_t bytes = round_up(rmax * wp * spb, 128);
-  if (bytes > 96 * 1024) return false;
-  *spb_out = (int32_t)spb;
-  *wp_out = (int32_t)wp;
-  *bytes_out = (int32_t)bytes;
-  return true;
 }
 
 bool igemm_planes_eligible(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk) {
@@ -1906,7 +1780,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_ppatch_kernel(const __grid_
     const uint32_t wp = (uint32_t)p.pt_wp;
     uint32_t ia = 0;
     for (int64_t ct = cid; ct < total; ct += ncl) {
-      if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+      if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
       const int64_t mt = (ct % m_pairs) * 2 + rank;
       const uint32_t P0 = (uint32_t)(mt * kBM);
       for (int cc = 0; cc < nchunk; ++cc, ++ia) {
@@ -1943,7 +1817,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_ppatch_kernel(const __grid_
       __syncwarp();
       uint32_t ia = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
         for (int cc = 0; cc < nchunk; ++cc, ++ia) {
           const int s = (int)(ia % AST);
           mbar_wait(&full[s], (ia / AST) & 1);
@@ -1966,7 +1840,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_ppatch_kernel(const __grid_
       const uint32_t wp = (uint32_t)p.pt_wp;
       uint32_t ia = 0, jn = 0;
       for (int64_t ct = cid; ct < total; ct += ncl) {
-        if (!tile_live(p, ct % m_pairs, 2, mv)) continue;
+        if (!tile_live(p, (int64_t)((uint32_t)ct % (uint32_t)m_pairs), 2, mv)) continue;
         const uint32_t j = jn++;
         const uint32_t buf = j & 1;
         mbar_wait_cluster(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
@@ -2701,22 +2575,11 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     static const bool no_pair = std::getenv("QNB_NO_PAIR") != nullptr;
     const int64_t npairs = (num_sms() / 2 / std::max<int64_t>(groups, 1)) * groups;
     const size_t cap = 227 * 1024;
-    // slab-staged gather: two slab buffers when >= 4 A stages still fit, else one, else off
-    auto slab_extra = [&](int nbuf) -> size_t { return a.a_slab ? (size_t)nbuf * a.sl_bytes + 128 : 0; };
-    auto res_stages = [&](int nbuf) -> int {
-      const size_t fx = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0) + slab_extra(nbuf);
-      return fx < cap ? (int)std::min<size_t>(kMaxStages, (cap - fx) / (kBM * 128)) : 0;
-    };
-    auto str_stages = [&](int nbuf) -> int {
-      const size_t fx = igemm_pair_stream_smem_bytes(a.n_rows, 0) + slab_extra(nbuf);
+    auto str_stages = [&]() -> int {
+      const size_t fx = igemm_pair_stream_smem_bytes(a.n_rows, 0);
       return fx < cap ? (int)std::min<size_t>(6, (cap - fx) / ((size_t)(kBM + a.n_rows / 2) * 128)) : 0;
     };
-    if (a.a_slab) {
-      const bool res_ok2 = res_stages(2) >= 4, str_ok2 = str_stages(2) >= 4;
-      a.sl_nbuf = (res_ok2 || str_ok2) ? 2 : 1;
-      if (res_stages(a.sl_nbuf) < 3 && str_stages(a.sl_nbuf) < 3) a.a_slab = 0;
-    }
-    const size_t fixed = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0) + slab_extra(a.sl_nbuf);
+    const size_t fixed = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0);
     int stages = fixed < cap ? (int)std::min<size_t>(kMaxStages, (cap - fixed) / (kBM * 128)) : 0;
     static const int env_st = [] {
       const char* e = std::getenv("QNB_PAIR_STAGES");
@@ -2725,20 +2588,19 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     if (env_st >= 2 && env_st < stages) stages = env_st;
     const bool shape_ok = !no_pair && !a.a_tma && a.kbytes == 128 && a.n_rows % 16 == 0 && a.n_rows <= 256 &&
                           2 * a.tmem_cols <= 512 && m_tiles >= 2;
-    const bool resident = shape_ok && a.ksplit == 1 && a.n_tiles == 1 && npairs >= groups &&
-                          stages >= (a.a_slab ? 3 : 4) && a.epi_mode != EPIM_RAW32;
+    const bool resident = shape_ok && a.ksplit == 1 && a.n_tiles == 1 && npairs >= groups && stages >= 4 &&
+                          a.epi_mode != EPIM_RAW32;
     static const bool no_stream = std::getenv("QNB_NO_PAIR_STREAM") != nullptr;
-    int sstages = str_stages(a.sl_nbuf);
-    const bool streamed = shape_ok && !resident && !no_stream && sstages >= (a.a_slab ? 3 : 4);
+    int sstages = str_stages();
+    const bool streamed = shape_ok && !resident && !no_stream && sstages >= 4;
     if (a.ks_fused && !(streamed && a.epi_mode == EPIM_RAW32 && pair_fused_fits(a, groups, sstages)))
       a.ks_fused = 0;  // plan asked for it but this launch cannot guarantee co-residency
     if (resident || streamed) {
       a.pair = resident ? stages : sstages;
       a.pair_stream = resident ? 0 : 1;
       a.cluster = 2;
-      const size_t smem = (resident ? igemm_pair_smem_bytes(a.n_rows, a.num_kb, stages)
-                                    : igemm_pair_stream_smem_bytes(a.n_rows, sstages)) +
-                          slab_extra(a.sl_nbuf);
+      const size_t smem = resident ? igemm_pair_smem_bytes(a.n_rows, a.num_kb, stages)
+                                   : igemm_pair_stream_smem_bytes(a.n_rows, sstages);
       const int64_t ptiles = ceil_div(m_tiles, 2) * a.n_tiles * a.ksplit * groups;
       const int64_t np = resident ? npairs : std::min<int64_t>(num_sms() / 2, ptiles);
       // the attribute is per function, not per launch: set it once to the maximum so that a
@@ -2770,7 +2632,6 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     }
   }
   a.pair = 0;
-  a.a_slab = 0;  // the slab-staged gather is a CTA-pair producer mode
   a.cluster = (m_tiles >= 2 && a.cluster != 1) ? 2 : 1;
   const int64_t ctiles = ceil_div(m_tiles, a.cluster) * a.n_tiles * a.ksplit * groups;
   const int64_t nclusters = std::min<int64_t>(ctiles, num_sms() / a.cluster);

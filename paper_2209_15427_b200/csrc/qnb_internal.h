@@ -155,14 +155,6 @@ struct IgemmArgs {
   // 16-byte cp.async gather for taps that are not whole 128-byte stages (AlexNet conv2:
   // 48 channels per group and tap).  tmap_a holds the 16-byte-channel im2col map.
   int32_t a_planes, pl_cpt, pl_kw, pl_chunks;  // chunks per tap, filter width, real chunks
-  // Slab-staged gather (a_slab = 1; CTA-pair kernel, stride-1 convs whose halo is their
-  // padding): per tile the producers cp.async the tile's input SLAB once (the merged padded
-  // rows [y0, y_last + kh) x sl_wp pixels x sl_spb bytes of this group's channels) into
-  // shared memory, then build each SW128 A stage from the slab with 16-byte ld/st.shared
-  // (sl_tab: the chunk table as slab byte offsets).  L2 -> SM traffic drops from kh*kw*K
-  // bytes per pixel (the im2col gather) to ~1 slab per tile; sl_nbuf slabs double-buffer.
-  int32_t a_slab, sl_spb, sl_wp, sl_hp, sl_bytes, sl_nbuf;
-  const int32_t* sl_tab;
   // device-resident batch (nullable): only output rows below *dyn_n * dyn_rows are
   // live; cluster / pair tiles starting past them are skipped by every warp role
   const int32_t* dyn_n;
@@ -299,11 +291,6 @@ qnb_status plan_prepare_host_io(qnb_plan* P, bool input_on_host, bool output_on_
 bool igemm_splitk_fused_ok(const IgemmArgs& a, int64_t groups);
 // True when the tap-major chunk table of `pk` can be served by TMA im2col chunk planes;
 // encodes the 16-byte-channel im2col tensor map.
-// Slab-staged gather eligibility (stride 1, halo == padding, contiguous images) and its
-// host tables: the chunk table as slab offsets, the slab bytes (max over the tiles of a
-// batch of max_batch).
-bool igemm_slab_plan(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk, int64_t max_batch,
-                     std::vector<int32_t>* tab, int32_t* spb, int32_t* wp, int32_t* bytes);
 bool igemm_ppatch_config(const IgemmGeometry& g, int64_t num_kb, int32_t slab, int* npt_out, int* astg_out);
 bool igemm_planes_eligible(const IgemmGeometry& g, const ActLayout& in, const IgemmPacked& pk);
 qnb_status igemm_encode_tma_planes(const IgemmGeometry& g, const ActLayout& in, const uint8_t* a_base,

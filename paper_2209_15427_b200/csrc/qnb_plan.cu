@@ -668,20 +668,6 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
       a.pt_ppst = 1;
     }
   }
-  std::vector<int32_t> sl_tab;
-  int32_t sl_spb = 0, sl_wp = 0, sl_bytes = 0;
-  if (!hk && !patch && !tma && !g.is_fc && !std::getenv("QNB_NO_SLAB") &&
-      igemm_slab_plan(g, Lin, pk, P.max_batch, &sl_tab, &sl_spb, &sl_wp, &sl_bytes)) {
-    // slab-staged gather for the CTA-pair kernel (decided per launch; falls back to the
-    // direct cp.async gather when the slabs do not fit next to the A stages)
-    QNB_TRY(upload(P, sl_tab, const_cast<int32_t**>(&a.sl_tab)));
-    a.a_slab = 1;
-    a.sl_spb = sl_spb;
-    a.sl_wp = sl_wp;
-    a.sl_hp = (int32_t)Lin.hp();
-    a.sl_bytes = sl_bytes;
-    a.pt_kh = (int32_t)g.kh;
-  }
   if (tma) {
     a.a_tma = 1;
     QNB_TRY(igemm_encode_tma(g, Lin, blob_ptr(P, op.in), pk.kbytes, &a.tmap_a));

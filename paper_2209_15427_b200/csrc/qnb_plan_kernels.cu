@@ -178,6 +178,20 @@ __global__ void pack_input_kernel(const uint8_t* __restrict__ src, int src_dtype
     for (int w4 = 0; w4 < (L.c_phys >> 2); ++w4) reinterpret_cast<uint32_t*>(o)[w4] = words[w4];
     return;
   }
+  if (dst_dtype == QNB_FP16 && src_dtype == QNB_FP32 && (L.c_phys == 4 || L.c_phys == 8) && op != PACK_COPY) {
+    // FP16 graphs: the pixel's channels narrowed (RNE, NaN payload kept) and stored as
+    // one 8- or 16-byte vector instead of c_phys 2-byte stores
+    uint32_t h[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c >= L.c_phys) break;
+      const uint32_t v = c < C ? (uint32_t)f2h_bits(reinterpret_cast<const float*>(s)[c * plane]) : 0u;
+      h[c >> 1] |= v << (16 * (c & 1));
+    }
+    if (L.c_phys == 8) *reinterpret_cast<uint4*>(o) = make_uint4(h[0], h[1], h[2], h[3]);
+    else *reinterpret_cast<uint2*>(o) = make_uint2(h[0], h[1]);
+    return;
+  }
   for (int64_t c = 0; c < L.c_phys; ++c) {
     uint8_t* oc = o + c * L.es;
     if (c >= C) {
