@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqnb.so")
+# QNB_LIB_VARIANT=spin selects the A/B build with spinning mbarrier waits (profiling only)
+LIB_PATH = os.path.join(_HERE, "libqnb_spin.so" if os.environ.get("QNB_LIB_VARIANT") == "spin" else "libqnb.so")
 
 # qnet::DataType codes (include/qnet/datatypes.hpp:30-35)
 FP32, FP16, INT8Q, INT16Q = 0, 1, 2, 3

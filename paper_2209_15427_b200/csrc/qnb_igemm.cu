@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_kernel(const __grid_constan
         }
         const int32_t off = chunk_tab[kb * 8 + jc];
         uint8_t* dst = sA + (size_t)s * a_stage;
-        if (p.dbg & 16) {
+        if ((p.dbg & 16) || p.a_ca) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int row = warp * 32 + rr + 4 * i;
@@ -1096,7 +1096,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
         }
         const int32_t off = chunks_in_smem ? chunk_s[kb * 8 + jc] : __ldg(p.chunk_off + kb * 8 + jc);
         uint8_t* dst = sA + (size_t)s * a_stage;
-        if (p.dbg & 16) {
+        if ((p.dbg & 16) || p.a_ca) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int row = warp * 32 + rr + 4 * i;
@@ -1183,7 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
           if (elect_one()) {
             if (mma_on)
               for (int k = 0; k < 4; ++k)
-                umma2_i8(dt, ad + astep * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
+                umma2<KIND>(dt, ad + astep * k, bd + 2 * k, idesc, ((kb - kb0) | k) != 0);
             tc_commit2_multicast(&empty[s], 3);
           }
           __syncwarp();
@@ -2570,8 +2570,9 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     return fail(QNB_E_ARG, "row-Hankel mode is INT8 only");
   }
   const int64_t m_tiles = ceil_div(a.m_total, kBM);
-  if constexpr (KIND == KIND_I8) {
-    // CTA-pair path: one group's B split over the pair's smem, resident for the launch
+  {
+    // CTA-pair path (every MMA kind): one group's B split over the pair's smem, resident
+    // for the launch, or streamed as halves
     static const bool no_pair = std::getenv("QNB_NO_PAIR") != nullptr;
     const int64_t npairs = (num_sms() / 2 / std::max<int64_t>(groups, 1)) * groups;
     const size_t cap = 227 * 1024;

@@ -155,6 +155,10 @@ struct IgemmArgs {
   // 16-byte cp.async gather for taps that are not whole 128-byte stages (AlexNet conv2:
   // 48 channels per group and tap).  tmap_a holds the 16-byte-channel im2col map.
   int32_t a_planes, pl_cpt, pl_kw, pl_chunks;  // chunks per tap, filter width, real chunks
+  // L1-allocating gather (cp.async.ca): taps narrower than a 128-byte stage, whose
+  // neighbouring output pixels re-read most of each other's window bytes (AlexNet conv2:
+  // 48-byte taps, 132 -> 122 us; wide-tap layers measured slower with .ca)
+  int32_t a_ca;
   // device-resident batch (nullable): only output rows below *dyn_n * dyn_rows are
   // live; cluster / pair tiles starting past them are skipped by every warp role
   const int32_t* dyn_n;

@@ -668,6 +668,8 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
       a.pt_ppst = 1;
     }
   }
+  a.a_ca = (!hk && !patch && !tma && !g.is_fc && g.groups > 1 && g.cg * Lin.es() < 128 && g.kh * g.kw > 9 &&
+            !std::getenv("QNB_NO_CA")) ? 1 : 0;
   if (tma) {
     a.a_tma = 1;
     QNB_TRY(igemm_encode_tma(g, Lin, blob_ptr(P, op.in), pk.kbytes, &a.tmap_a));
