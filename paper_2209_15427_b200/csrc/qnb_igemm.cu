@@ -186,9 +186,19 @@ __device__ __forceinline__ uint32_t relu_tail(int32_t q, const ReluFastK& r) {
   return (uint32_t)min(max((int32_t)t + r.zout, r.omin), r.omax);
 }
 
-// F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32; bit 2: clamp-free ReLU tail.
+// Replicated ReLU table (F bit 3): the 256 u8 relu_quant results of every clamped conv
+// output, stored 32 times interleaved so lane L reads only bank L -- entry v of lane L at
+// byte ((v >> 2) * 32 + L) * 4 + (v & 3): one conflict-free LDS.U8 replaces the five-op
+// truncating requant tail.
+__device__ __forceinline__ uint32_t relu_lut32(uint32_t lutb, int32_t v) {
+  return lds_u8(lutb + ((uint32_t)(v >> 2) << 7) + (uint32_t)(v & 3));
+}
+
+// F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32; bit 2: clamp-free ReLU tail;
+// bit 3: ReLU through the replicated smem table (lutb).
 template <bool RELU, int F>
-__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk) {
+__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk,
+                                            uint32_t lutb = 0) {
   int32_t q;  // RNE quotient (before the output zero point)
   if constexpr ((F & 1) != 0) {
     const int64_t pr = mulwide_s32(acc, k.mult32);
@@ -203,6 +213,7 @@ __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, cons
     qq = qq < -lim ? -lim : (qq > lim ? lim : qq);
     q = (int32_t)max(min(qq, (int64_t)INT32_MAX / 2), (int64_t)INT32_MIN / 2);
   }
+  if constexpr (RELU && (F & 8) != 0) return relu_lut32(lutb, min(max(q + k.oz, k.omin), k.omax));
   if constexpr (RELU) return relu_tail<(F & 2) != 0, (F & 4) != 0>(q, rk);
   return (uint32_t)min(max(q + k.oz, k.omin), k.omax);
 }
@@ -358,8 +369,8 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
                                                uint64_t* acc_empty, int64_t m_groups, int64_t total, int64_t cid,
                                                int64_t ncl, int cs, int rank, int warp, int lane, uint8_t* lut,
                                                int slot, int nslots) {
-  (void)lut;
   const ReluFastK lut_s = relu_fast_consts(p.relu, p.rq);
+  const uint32_t lutb = ((F & 8) != 0) ? smem_u32(lut) + (uint32_t)lane * 4u : 0u;
   const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
   // this warp drains the 16-column blocks slot, slot + nslots, ... of its lane quarter
   const int half = slot, cstep = 16 * nslots;
@@ -498,10 +509,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
           uint32_t w[4];
 #pragma unroll
           for (int qd = 0; qd < 4; ++qd) {
-            const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[4 * qd + 0] + cc[qd].x + rowterm32, k, lut_s);
-            const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[4 * qd + 1] + cc[qd].y + rowterm32, k, lut_s);
-            const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[4 * qd + 2] + cc[qd].z + rowterm32, k, lut_s);
-            const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[4 * qd + 3] + cc[qd].w + rowterm32, k, lut_s);
+            const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[4 * qd + 0] + cc[qd].x + rowterm32, k, lut_s, lutb);
+            const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[4 * qd + 1] + cc[qd].y + rowterm32, k, lut_s, lutb);
+            const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[4 * qd + 2] + cc[qd].z + rowterm32, k, lut_s, lutb);
+            const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[4 * qd + 3] + cc[qd].w + rowterm32, k, lut_s, lutb);
             w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           *reinterpret_cast<uint4*>(obase + (int64_t)(ch0 + cb)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -520,14 +531,14 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
             uint32_t w0[4], w1[4];
 #pragma unroll
             for (int qd = 0; qd < 4; ++qd) {
-              const uint32_t a0 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 0] + c0[qd].x + rowterm32, k, lut_s);
-              const uint32_t b0 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 0] + c1[qd].x + rowterm32, k, lut_s);
-              const uint32_t a1 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 1] + c0[qd].y + rowterm32, k, lut_s);
-              const uint32_t b1 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 1] + c1[qd].y + rowterm32, k, lut_s);
-              const uint32_t a2 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 2] + c0[qd].z + rowterm32, k, lut_s);
-              const uint32_t b2 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 2] + c1[qd].z + rowterm32, k, lut_s);
-              const uint32_t a3 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 3] + c0[qd].w + rowterm32, k, lut_s);
-              const uint32_t b3 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 3] + c1[qd].w + rowterm32, k, lut_s);
+              const uint32_t a0 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 0] + c0[qd].x + rowterm32, k, lut_s, lutb);
+              const uint32_t b0 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 0] + c1[qd].x + rowterm32, k, lut_s, lutb);
+              const uint32_t a1 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 1] + c0[qd].y + rowterm32, k, lut_s, lutb);
+              const uint32_t b1 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 1] + c1[qd].y + rowterm32, k, lut_s, lutb);
+              const uint32_t a2 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 2] + c0[qd].z + rowterm32, k, lut_s, lutb);
+              const uint32_t b2 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 2] + c1[qd].z + rowterm32, k, lut_s, lutb);
+              const uint32_t a3 = q8_fast<RELU, F>((int32_t)r0[4 * qd + 3] + c0[qd].w + rowterm32, k, lut_s, lutb);
+              const uint32_t b3 = q8_fast<RELU, F>((int32_t)r1[4 * qd + 3] + c1[qd].w + rowterm32, k, lut_s, lutb);
               w0[qd] = a0 | (a1 << 8) | (a2 << 16) | (a3 << 24);
               w1[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
             }
@@ -582,10 +593,10 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int qd = 0; qd < 4; ++qd) {
             const int4 cc = __ldg(cc4 + qd);
-            const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut_s);
-            const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut_s);
-            const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut_s);
-            const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut_s);
+            const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[4 * qd + 0] + cc.x + rowterm32, k, lut_s, lutb);
+            const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[4 * qd + 1] + cc.y + rowterm32, k, lut_s, lutb);
+            const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[4 * qd + 2] + cc.z + rowterm32, k, lut_s, lutb);
+            const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[4 * qd + 3] + cc.w + rowterm32, k, lut_s, lutb);
             w[qd] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
           }
           if (o_vec) {
@@ -598,7 +609,7 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
 #pragma unroll
           for (int i = 0; i < 16; ++i)
             if (i < cnt)
-              dst[i] = (uint8_t)q8_fast<RELU, F>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut_s);
+              dst[i] = (uint8_t)q8_fast<RELU, F>((int32_t)r[i] + p.chan_const32[ch0 + cb + i] + rowterm32, k, lut_s, lutb);
         }
       } else if constexpr (MODE == EPIM_Q8_EXACT) {
 #pragma unroll
@@ -644,6 +655,11 @@ __device__ __forceinline__ void run_epilogue(const IgemmArgs& p, uint32_t tmem, 
   const int f = (p.rq.s >= 32 ? 1 : 0) | (p.relu.shift_bits + p.relu.shift >= 32 ? 2 : 0);
   switch (p.epi_mode) {
     case EPIM_Q8_FAST_RELU:
+      if ((p.hk || p.pair) && p.relu_lut != nullptr && lut != nullptr && !(p.dbg & 64)) {
+        if (f & 1) QNB_EPI(EPIM_Q8_FAST_RELU, 9);
+        else QNB_EPI(EPIM_Q8_FAST_RELU, 8);
+        break;
+      }
       switch (f | (p.relu_free ? 4 : 0)) {
         case 0: QNB_EPI(EPIM_Q8_FAST_RELU, 0); break;
         case 1: QNB_EPI(EPIM_Q8_FAST_RELU, 1); break;
@@ -923,6 +939,12 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
   uint32_t* tmem_slot = (uint32_t*)(bpeer + 1);
   int64_t* rowoff = (int64_t*)(tmem_slot + 4);   // [2][128]
   int32_t* chunk_s = (int32_t*)(rowoff + 256);
+  uint8_t* relu_lut = (uint8_t*)(chunk_s + kMaxChunkSmem);  // 8 KB replicated relu_quant table
+  if (p.relu_lut != nullptr)
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int v = i >> 5, l = i & 31;
+      relu_lut[((v >> 2) * 32 + l) * 4 + (v & 3)] = __ldg(p.relu_lut + v);
+    }
   const int n_chunks = p.num_kb * 8;
   const bool chunks_in_smem = n_chunks <= kMaxChunkSmem;
   const int32_t* ctab_g = p.chunk_off;
@@ -1194,8 +1216,8 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    run_epilogue(p, tmem, acc_full, acc_empty, m_pairs, total, cid, ncl, 2, rank, warp, lane, nullptr, (warp - 5) >> 2,
-                 2);
+    run_epilogue(p, tmem, acc_full, acc_empty, m_pairs, total, cid, ncl, 2, rank, warp, lane, relu_lut,
+                 (warp - 5) >> 2, 2);
   }
 
   tc_fence_before();
@@ -1209,11 +1231,11 @@ __global__ void __launch_bounds__(kThreads, 1) igemm_pair_kernel(const __grid_co
 
 static size_t igemm_pair_smem_bytes(int n_rows, int num_kb, int stages) {
   return 1024 + (size_t)stages * kBM * 128 + (size_t)num_kb * (n_rows / 2) * 128 + (2 * kMaxStages + 6) * 8 + 16 +
-         2 * 128 * 8 + kMaxChunkSmem * 4;
+         2 * 128 * 8 + kMaxChunkSmem * 4 + 8192;
 }
 static size_t igemm_pair_stream_smem_bytes(int n_rows, int stages) {
   return 1024 + (size_t)stages * (kBM + n_rows / 2) * 128 + (2 * kMaxStages + 6) * 8 + 16 + 2 * 128 * 8 +
-         kMaxChunkSmem * 4;
+         kMaxChunkSmem * 4 + 8192;
 }
 
 
@@ -1252,9 +1274,14 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
   uint64_t* acc_full = a_empty + 2;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(acc_empty + 2);
-  uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);
+  uint8_t* relu_lut = (uint8_t*)(tmem_slot + 4);  // 8 KB: relu_quant table replicated per lane
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t total = (int64_t)p.hk_pairs * p.oh;  // tile = (image pair, output row)
+  if (p.relu_lut != nullptr)
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int v = i >> 5, l = i & 31;
+      relu_lut[((v >> 2) * 32 + l) * 4 + (v & 3)] = __ldg(p.relu_lut + v);
+    }
   const int64_t mv = m_valid(p);
 
   if (threadIdx.x == 0) {
@@ -1991,7 +2018,7 @@ bool igemm_patch_config(const IgemmGeometry& g, int64_t num_kb, int32_t plane, i
 static size_t igemm_hk_smem_bytes(const IgemmArgs& a) {
   return 1024 + (size_t)(((a.num_kb * a.n_rows * 128) + 1023) & ~1023) +
          2 * (a.hk_2copy ? 2 : 1) * (size_t)((a.hk_copy + 64 + 127) & ~127) +
-         9 * 8 + 16 + 256;
+         9 * 8 + 16 + 8192;
 }
 
 bool hk_geometry_ok(const IgemmGeometry& g, const ActLayout& in) {
