@@ -492,6 +492,42 @@ __device__ __forceinline__ void epilogue_tiles(const IgemmArgs& p, uint32_t tmem
     const int n_here = min(npt, n_real - n0);
     const int ch0 = c.g * n_real + n0;
     if constexpr (MODE == EPIM_Q8_FAST || MODE == EPIM_Q8_FAST_RELU) {
+      if (nslots == 4 && o_vec && n_here == 96 && !(p.dbg & 8)) {
+        // 16 epilogue warps (row-Hankel): 12 blocks of 8 columns, three per warp -- all
+        // three TMEM loads in flight, one wait, 24 independent requant chains
+        constexpr bool RELU = MODE == EPIM_Q8_FAST_RELU;
+        const int4* ccp = reinterpret_cast<const int4*>(p.chan_const32 + ch0);
+        uint32_t r[3][8];
+        int4 cc[3][2];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int col = slot * 8 + b * 32;
+          cc[b][0] = __ldg(ccp + (col >> 2));
+          cc[b][1] = __ldg(ccp + (col >> 2) + 1);
+          tmem_ld8(trow + (uint32_t)col, r[b]);
+        }
+        tmem_ld_wait3x8(r);
+        if (ok) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            uint32_t w[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int4 c4 = cc[b][h];
+              const uint32_t b0 = q8_fast<RELU, F>((int32_t)r[b][4 * h + 0] + c4.x + rowterm32, k, lut_s, lutb);
+              const uint32_t b1 = q8_fast<RELU, F>((int32_t)r[b][4 * h + 1] + c4.y + rowterm32, k, lut_s, lutb);
+              const uint32_t b2 = q8_fast<RELU, F>((int32_t)r[b][4 * h + 2] + c4.z + rowterm32, k, lut_s, lutb);
+              const uint32_t b3 = q8_fast<RELU, F>((int32_t)r[b][4 * h + 3] + c4.w + rowterm32, k, lut_s, lutb);
+              w[h] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+            }
+            *reinterpret_cast<uint2*>(obase + (int64_t)(ch0 + slot * 8 + b * 32)) = make_uint2(w[0], w[1]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) epi_release(p, &acc_empty[buf]);
+        continue;
+      }
       if (o_vec && (n_here & 15) == 0 && !(p.dbg & 8)) {
         // Software-pipelined drain: the TMEM load and the per-channel constants of the
         // next 16-column block are in flight while this block is requantized.
@@ -1251,8 +1287,9 @@ static size_t igemm_pair_stream_smem_bytes(int n_rows, int stages) {
 //   warp 0 (lane 0)  producer: B once, then per tile the 2 x kh input rows
 //   warp 4           TMEM allocator + MMA issuer
 //   warps 5-12       epilogue (shared with the general kernel)
-constexpr int kHkThreads = 14 * 32;  // warps 0-3, 5-12 epilogue (3 per TMEM lane quarter), 4 MMA, 13 producer
-constexpr int kHkEpiWarps = 12;
+constexpr int kHkThreads = 18 * 32;  // warps 0-3, 5-16 epilogue (4 per TMEM lane quarter), 4 MMA, 17 producer
+constexpr int kHkEpiWarps = 16;
+constexpr int kHkProducer = 17;
 template <int KIND>
 __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_constant__ IgemmArgs p) {
   griddep_launch_dependents();
@@ -1303,8 +1340,8 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp != 13) griddep_wait();  // warp 13 first issues the resident weights
-  if (warp == 13) {
+  if (warp != kHkProducer) griddep_wait();  // the producer warp first issues the resident weights
+  if (warp == kHkProducer) {
     if (lane == 0) {
       mbar_arrive_expect_tx(b_full, (uint32_t)b_bytes);
       for (int kb = 0; kb < p.num_kb; ++kb)
@@ -1361,9 +1398,9 @@ __global__ void __launch_bounds__(kHkThreads, 1) igemm_hk_kernel(const __grid_co
         __syncwarp();
       }
     }
-  } else if (warp != 4) {  // epilogue warps 0-3, 5-12
+  } else if (warp != 4) {  // epilogue warps 0-3, 5-16: slot = which 8-column blocks of the lane quarter
     run_epilogue(p, tmem, acc_full, acc_empty, total, total, blockIdx.x, gridDim.x, 1, 0, warp, lane, relu_lut,
-                 warp < 4 ? 0 : 1 + ((warp - 5) >> 2), 3);
+                 warp < 4 ? 0 : 1 + ((warp - 5) >> 2), 4);
   }
   tc_fence_before();
   __syncthreads();
