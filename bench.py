@@ -525,17 +525,17 @@ def run_qnb(a):
                               "ms": round(t, 4),
                               "tops": round(ops_ / (t * 1e-3) / 1e12, 1) if ops_ else None,
                               "gbs": round(by / (t * 1e-3) / 1e9, 1)})
-            if kind == "igemm" and names[li].startswith("conv"):
+            if kind in ("igemm", "conv_pool") and names[li].startswith("conv"):
                 conv_ops += ops_
                 conv_ms += t
         dom = int(np.argmax(ms_steps))
         li, kind, ops_, by = steps_info[dom]
         t = ms_steps[dom]
-        if kind == "igemm":
+        if kind in ("igemm", "conv_pool"):  # conv_pool: conv + ReLU + max-pool fused (qnb_front.cu)
             roof = {"bound": "tensor", "achieved": ops_ / (t * 1e-3) / 1e12, "peak": mma_peak, "unit": "TFLOP/s",
                     "op_type": ("int8 tensor ops (2 per u8 x u8 MAC), i.e. TOPS" if a.precision in ("int8", "int16")
                                 else f"{a.precision} flops (2 per MAC)"),
-                    "kernel": f"igemm {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
+                    "kernel": f"{kind} {names[li]}", "algorithmic_ops": ops_, "launch_ms": t}
         else:
             roof = {"bound": "hbm", "achieved": by / (t * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "kernel": f"{kind} {names[li]}", "algorithmic_bytes": by, "launch_ms": t}
@@ -554,7 +554,7 @@ def run_qnb(a):
         except Exception:
             pass
         roof["peak_source"] = ((int8_src if a.precision in ("int8", "int16") else f16_src)
-                               if kind == "igemm" else f"{peak_src}: hbm_gbs")
+                               if kind in ("igemm", "conv_pool") else f"{peak_src}: hbm_gbs")
         conv_tops = conv_ops / (conv_ms * 1e-3) / 1e12 if conv_ms else None
 
     cpu = parity = None

@@ -298,7 +298,7 @@ qnb_status qnb_plan_stats(const qnb_plan* plan, int64_t* kernels_per_forward,
                           int64_t* arena_bytes, int64_t* weight_bytes);
 /* Step `step` of the forward: reference layer index it implements (the first of a fused
  * group), step kind (0 pack_input, 1 implicit GEMM, 2 pool, 3 pool+LRN, 4 convert,
- * 5 softmax, 6 unpack) and its algorithmic work at max_batch (ops = 2 per MAC,
+ * 5 softmax, 6 unpack, 7 fused conv + ReLU + max-pool) and its algorithmic work at max_batch (ops = 2 per MAC,
  * bytes = logical input + output (+ weights) bytes). */
 qnb_status qnb_plan_step_info(const qnb_plan* plan, int32_t step, int32_t* layer, int32_t* kind,
                               double* ops, double* bytes);

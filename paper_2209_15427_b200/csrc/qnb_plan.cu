@@ -7,6 +7,7 @@
 //   2. lowering with fusion over single-consumer chains:
 //        INPUT -> QUANTIZER(fp->q|f16)       => pack_input (quantize + NCHW->NHWC)
 //        CONV|IP (-> RELU)                   => tcgen05 implicit GEMM, fused epilogue
+//        CONV(row-Hankel) -> RELU -> POOL    => front kernel (conv1 + relu1 + pool1, qnb_front.cu)
 //        POOL (-> Q2F) -> LRN (-> F2Q)       => pool_lrn, one HBM pass
 //        Q2F -> SOFTMAX                      => softmax_rows with fused dequantize
 //        DROPOUT                             => alias (no kernel)
@@ -42,7 +43,7 @@ int default_shift_bits(int dtype);
 
 namespace {
 
-enum OpKind { OP_PACK, OP_IGEMM, OP_POOL, OP_POOL_LRN, OP_CONVERT, OP_SOFTMAX, OP_ALIAS, OP_FEXACT };
+enum OpKind { OP_PACK, OP_IGEMM, OP_POOL, OP_POOL_LRN, OP_CONVERT, OP_SOFTMAX, OP_ALIAS, OP_FEXACT, OP_FRONT };
 
 struct Blob {
   bool defined = false;
@@ -67,7 +68,7 @@ struct Op {
   int in = -1, out = -1;
   int layer = -1;       // main layer
   int relu = -1;        // fused RELU layer (IGEMM)
-  int pool = -1, lrn = -1;  // POOL_LRN parts
+  int pool = -1, lrn = -1;  // POOL_LRN parts (pool: also the FRONT op's pool layer)
   int pack_op = PACK_COPY;
   int conv_op = CVT_CONVERT;
   int in_dtype = 0, out_dtype = 0;
@@ -89,6 +90,7 @@ struct Step {
   FExactArgs fx;
   PoolArgs pool;
   PoolLrnArgs plrn;
+  FrontArgs front;
   ConvertArgs cvt;
   const uint8_t* sm_src = nullptr;
   DevLayout sm_S;
@@ -221,9 +223,9 @@ IgemmGeometry geometry_of(const qnb_layer_desc& l, const Blob& in, const Blob& o
 
 // Layout the consumer op needs for its input blob.
 ActLayout required_input_layout(const qnb_plan& P, const Op& op, const Blob& b) {
-  if (op.kind == OP_IGEMM) {
+  if (op.kind == OP_IGEMM || op.kind == OP_FRONT) {
     const qnb_layer_desc& l = P.layers[op.layer];
-    const Blob& out = P.blobs[op.out];
+    const Blob& out = P.blobs[l.top];  // the contraction's own output (FRONT: before the pool)
     IgemmGeometry g = geometry_of(l, b, out);
     if (l.kind == QNB_LAYER_CONV) return choose_input_layout(g, b.dtype, P.max_batch, b.c, b.h, b.w);
     ActLayout L = plain_layout(b, P.max_batch);
@@ -348,6 +350,84 @@ bool is_f2x(const qnb_layer_desc& l) {
   return l.kind == QNB_LAYER_QUANTIZER && l.mi_type == QNB_FP32 && l.mo_type != QNB_FP32;
 }
 
+
+// Per-output-channel constant of the quantized contraction: K zx zW - zx sum_k(w) + bias
+// (src/ops.cpp:53-87 with bias_to_acc, src/quantizer.cpp:157-199).
+std::vector<int64_t> quant_chan_const(const qnb_layer_desc& l, const IgemmGeometry& g, const qnb_qvals& qx) {
+  const qnb_qvals& qw = l.weight_qv;
+  const qnb_qvals& qa = g.is_fc ? qx : qw;  // src/ops.cpp:303-306 vs 428-431
+  const qnb_qvals& qb = g.is_fc ? qw : qx;
+  const int64_t K = g.is_fc ? g.fc_c * g.fc_h * g.fc_w : g.cg * g.kh * g.kw;
+  const int64_t OC = g.groups * g.og;
+  std::vector<int64_t> cc((size_t)OC);
+  for (int64_t oc = 0; oc < OC; ++oc) {
+    int64_t wsum = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      const int64_t wi = g.is_fc ? k * OC + oc : oc * K + k;
+      wsum += l.d_type == QNB_INT16Q ? (int64_t)((const uint16_t*)l.weight)[wi] : (int64_t)((const uint8_t*)l.weight)[wi];
+    }
+    int64_t c = K * (int64_t)qx.zero * qw.zero - (int64_t)qx.zero * wsum;
+    if (l.bias_term && l.bias) c += bias_to_acc(l.bias[oc], qa.scale, qb.scale);
+    cc[(size_t)oc] = c;
+  }
+  return cc;
+}
+
+// The fused conv1 front's numeric preconditions (qnb_front.cu): INT8 throughout, the
+// host-proven 32-bit requant, and a monotone requant / ReLU chain so that max-pooling the
+// raw accumulators equals pooling the requantized outputs.
+struct FrontNumeric {
+  bool ok = false;
+  qnb_requant rq{}, relu{};
+  std::vector<int64_t> cc;
+  std::vector<uint8_t> lut;
+};
+FrontNumeric front_numeric(const qnb_plan& P, int conv, int relu) {
+  FrontNumeric f;
+  const qnb_layer_desc& l = P.layers[conv];
+  const qnb_layer_desc& lr = P.layers[relu];
+  const Blob& in = P.blobs[l.bottom];
+  const Blob& cout = P.blobs[l.top];
+  const Blob& rtop = P.blobs[lr.top];
+  if (l.d_type != QNB_INT8Q || l.mi_type != QNB_INT8Q || l.mo_type != QNB_INT8Q || lr.d_type != QNB_INT8Q) return f;
+  if (!l.weight || l.weight_dtype != QNB_INT8Q || !l.weight_has_qv || !in.has_qv || !cout.has_qv || !rtop.has_qv)
+    return f;
+  const IgemmGeometry g = geometry_of(l, in, cout);
+  if (requant_from_ratio(l.weight_qv.scale * in.qv.scale / cout.qv.scale, l.weight_qv.zero, cout.qv,
+                         default_shift_bits(QNB_INT8Q), &f.rq) != QNB_OK)
+    return f;
+  if (requant_from_ratio(cout.qv.scale / rtop.qv.scale, cout.qv.zero, rtop.qv, default_shift_bits(QNB_INT8Q),
+                         &f.relu) != QNB_OK)
+    return f;
+  if (f.rq.mult <= 0) return f;  // requant_round is monotone non-decreasing for mult > 0
+  f.cc = quant_chan_const(l, g, in.qv);
+  if (!igemm_fast_requant_ok(f.cc, g.cg * g.kh * g.kw, l.weight_qv.zero, to_dev(f.rq))) return f;
+  f.lut.resize(256);
+  for (int q = 0; q < 256; ++q) {
+    f.lut[(size_t)q] = (uint8_t)relu_requant_host(q, f.relu, QNB_INT8Q);
+    if (q > 0 && f.lut[(size_t)q] < f.lut[(size_t)q - 1]) return f;  // relu_quant must be monotone
+  }
+  f.ok = true;
+  return f;
+}
+
+// conv (+relu) -> pool that the front kernel can run as one step
+bool front_candidate(const qnb_plan& P, int conv, int relu, int pool) {
+  if (std::getenv("QNB_NO_FRONT")) return false;
+  const qnb_layer_desc& l = P.layers[conv];
+  const qnb_layer_desc& lp = P.layers[pool];
+  if (l.kind != QNB_LAYER_CONV || lp.kind != QNB_LAYER_POOL || lp.mi_type != QNB_INT8Q || lp.mo_type != QNB_INT8Q)
+    return false;
+  if (P.flags & QNB_PLAN_OBSERVE) return false;
+  const Blob& in = P.blobs[l.bottom];
+  const Blob& cout = P.blobs[l.top];
+  if (in.ndim != 4 || in.external) return false;
+  const IgemmGeometry g = geometry_of(l, in, cout);
+  const ActLayout Lin = choose_input_layout(g, in.dtype, P.max_batch, in.c, in.h, in.w);
+  if (!front_geometry_ok(g, Lin, lp.pool_kernel, lp.pool_stride)) return false;
+  return front_numeric(P, conv, relu).ok;
+}
+
 qnb_status lower(qnb_plan& P) {
   std::vector<bool> done(P.layers.size(), false);
   for (size_t i = 0; i < P.layers.size(); ++i) {
@@ -396,6 +476,13 @@ qnb_status lower(qnb_plan& P) {
           done[j] = true;
           op.relu = j;
           op.out = P.layers[j].top;
+          const int jp = sole_consumer(P, P.layers[j].top);
+          if (jp >= 0 && front_candidate(P, (int)i, j, jp)) {  // conv1 + relu1 + pool1
+            done[jp] = true;
+            op.kind = OP_FRONT;
+            op.pool = jp;
+            op.out = P.layers[jp].top;
+          }
         }
         break;
       }
@@ -819,6 +906,49 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   return QNB_OK;
 }
 
+
+// conv (row-Hankel) + relu + pool -> one front-kernel step (qnb_front.cu)
+qnb_status emit_front(qnb_plan& P, const Op& op, Step& st) {
+  const qnb_layer_desc& l = P.layers[op.layer];
+  const qnb_layer_desc& lp = P.layers[op.pool];
+  const Blob& in = P.blobs[op.in];
+  const Blob& cout = P.blobs[l.top];
+  const ActLayout& Lin = blob_layout(P, op.in);
+  const IgemmGeometry g = geometry_of(l, in, cout);
+  if (!front_geometry_ok(g, Lin, lp.pool_kernel, lp.pool_stride))
+    return fail(QNB_E_ARG, "internal: front step on an ineligible input layout");
+  FrontNumeric fn = front_numeric(P, op.layer, op.relu);
+  if (!fn.ok) return fail(QNB_E_ARG, "internal: front step without its numeric preconditions");
+  FrontArgs& a = st.front;
+  std::memset(&a, 0, sizeof(a));
+  std::vector<uint8_t> wpk;
+  QNB_TRY(front_pack_weights(g, Lin, (const uint8_t*)l.weight, l.weight_qv.zero, &wpk, &a.num_kb, &a.kpr, &a.signed_a));
+  QNB_TRY(upload(P, wpk, const_cast<uint8_t**>(&a.w)));
+  std::vector<int32_t> cc32(fn.cc.begin(), fn.cc.end());
+  QNB_TRY(upload(P, cc32, const_cast<int32_t**>(&a.chan_const)));
+  QNB_TRY(upload(P, fn.lut, const_cast<uint8_t**>(&a.relu_lut)));
+  a.rq = to_dev(fn.rq);
+  a.a = blob_ptr(P, op.in);
+  a.a_img = Lin.img();
+  a.a_row = Lin.row();
+  a.a_origin = (Lin.hh - g.ph) * Lin.row() + (Lin.hw - g.pw) * Lin.pix();
+  a.sh = (int32_t)g.sh;
+  a.kh = (int32_t)g.kh;
+  a.oh = (int32_t)g.oh;
+  a.ow = (int32_t)g.ow;
+  const Blob& pt = P.blobs[op.out];
+  a.ph = (int32_t)pt.h;
+  a.pw = (int32_t)pt.w;
+  a.oc = (int32_t)g.og;
+  a.cpq = (int32_t)(g.og / 4);
+  a.out = blob_ptr(P, op.out);
+  a.D = dev_layout(blob_layout(P, op.out));
+  a.batch = (int32_t)P.max_batch;
+  a.dyn_n = nullptr;
+  st.kind = OP_FRONT;
+  return QNB_OK;
+}
+
 qnb_status emit(qnb_plan& P) {
   for (const Op& op : P.ops) {
     if (op.kind == OP_ALIAS) continue;
@@ -832,13 +962,14 @@ qnb_status emit(qnb_plan& P) {
       const double in_b = (double)P.max_batch * bi.c * bi.h * bi.w * dtype_size(bi.dtype);
       const double out_b = (double)P.max_batch * bo.c * bo.h * bo.w * dtype_size(bo.dtype);
       st.bytes = in_b + out_b;
-      if (op.kind == OP_IGEMM) {
+      if (op.kind == OP_IGEMM || op.kind == OP_FRONT) {
         const qnb_layer_desc& l = P.layers[op.layer];
         const double K = l.kind == QNB_LAYER_CONV
                              ? (double)(bi.c / l.conv.groups) * l.conv.kernel_h * l.conv.kernel_w
                              : (double)bi.c * bi.h * bi.w;
-        const double M = (double)P.max_batch * bo.h * bo.w;
-        st.ops = 2.0 * M * bo.c * K;
+        const Blob& bc = P.blobs[l.top];  // the contraction's own output (FRONT: before the pool)
+        const double M = (double)P.max_batch * bc.h * bc.w;
+        st.ops = 2.0 * M * bc.c * K;
         st.bytes += (double)bo.c * K * dtype_size(l.d_type);
       }
     }
@@ -866,6 +997,9 @@ qnb_status emit(qnb_plan& P) {
       }
       case OP_IGEMM:
         QNB_TRY(emit_igemm(P, op, st));
+        break;
+      case OP_FRONT:
+        QNB_TRY(emit_front(P, op, st));
         break;
       case OP_FEXACT: {
         const qnb_layer_desc& l = P.layers[op.layer];
@@ -1031,6 +1165,9 @@ Step with_batch(const Step& s0, int64_t b, const void* in, void* out, const int3
     s.sm_out = (float*)out;
     s.up_dst = (uint8_t*)out;
   }
+  s.front.batch = (int32_t)b;
+  s.front.D.n = b;
+  if (dyn) s.front.dyn_n = dyn;
   s.ig.m_total = b * s.rows_per_img;
   if (s.ig.hk) s.ig.hk_pairs = (int32_t)((b + 1) / 2);  // row-Hankel tiles cover only this batch's image pairs
   s.pack.N = b;
@@ -1062,6 +1199,9 @@ qnb_status launch_one(const Step& s0, int64_t b, const void* in, void* out, cuda
           g_launches.fetch_sub(g_launches.load() - l0);  // counted below with the others
           break;
         }
+        case OP_FRONT:
+          QNB_TRY(launch_front(st.front, s));
+          break;
         case OP_FEXACT:
           launch_fexact(st.fx, s);
           break;
@@ -1101,7 +1241,8 @@ int step_kind_code(const Step& st) {
     case OP_POOL_LRN: return 3;
     case OP_CONVERT: return 4;
     case OP_SOFTMAX: return 5;
-    default: return 7;
+    case OP_FRONT: return 7;
+    default: return 8;
   }
 }
 

@@ -113,6 +113,36 @@ struct FExactArgs {
   int64_t in_c, in_h, in_w, out;           // IP: K = in_c * in_h * in_w in NCHW order
 };
 
+// Fused conv1 front (csrc/qnb_front.cu): row-Hankel INT8 convolution + truncating ReLU
+// requant + 3x3 / stride-2 max pool in one persistent kernel (AlexNet conv1 -> relu1 ->
+// pool1; src/ops.cpp:264-342, 156-181, 344-390).  Channels are the MMA's M rows (TMEM
+// lanes), pixels its N columns, so both pooling directions run in registers.
+struct FrontArgs {
+  const uint8_t* a;                // conv input, image-pair interleaved (1024-byte row slots)
+  int64_t a_img, a_row, a_origin;  // pair-image stride, pair-row stride (2048), window origin
+  int32_t sh, kh, kpr;             // stride_h, filter rows, K bytes per filter row (multiple of 32)
+  int32_t oh, ow, ph, pw;          // conv and pooled extents
+  int32_t oc, cpq;                 // output channels, channels per TMEM lane quarter (oc / 4)
+  const uint8_t* w;                // [num_kb][128 rows][128 B] SW128 A operand (channel rows + zW row)
+  int32_t num_kb;
+  int32_t signed_a;                // A holds w - zW as s8 (no zW * rowsum row)
+  const int32_t* chan_const;       // [oc]: K zx zW - zx sum(w) + bias (host-proven to fit int32)
+  Requant rq;                      // conv accumulator -> conv top grid (fast form, host-proven)
+  const uint8_t* relu_lut;         // [256] relu_quant of every conv top value (monotone)
+  uint8_t* out;                    // pool top, NHWC
+  DevLayout D;
+  int32_t batch;                   // images of this launch
+  const int32_t* dyn_n;            // device-resident batch clamp (nullable)
+  int32_t dbg;                     // profiling probes (env QNB_FRONT_DBG): 1 no epilogue math, 2 no MMAs
+};
+
+// Eligibility of conv (row-Hankel geometry on `in`) -> relu -> pool(k, s) for the front kernel.
+bool front_geometry_ok(const IgemmGeometry& g, const ActLayout& in, int64_t pool_k, int64_t pool_s);
+// Packs u8 weights (OC x Cg x KH x KW) into the front kernel's A operand.
+qnb_status front_pack_weights(const IgemmGeometry& g, const ActLayout& in, const uint8_t* w, int64_t zw,
+                              std::vector<uint8_t>* packed, int32_t* num_kb, int32_t* kpr, int32_t* signed_a);
+qnb_status launch_front(const FrontArgs& a, cudaStream_t s);
+
 void launch_pack_input(const PackArgs& p, cudaStream_t s);
 void launch_fexact(const FExactArgs& a, cudaStream_t s);
 void launch_pool(const PoolArgs& p, cudaStream_t s);

@@ -64,7 +64,7 @@ class Plan:
         check(_plan_lib().qnb_plan_stats(self.h, C.byref(k), C.byref(a), C.byref(w)))
         return {"kernels_per_forward": k.value, "arena_bytes": a.value, "weight_bytes": w.value}
 
-    STEP_KINDS = {0: "pack_input", 1: "igemm", 2: "pool", 3: "pool_lrn", 4: "convert", 5: "softmax",
+    STEP_KINDS = {0: "pack_input", 1: "igemm", 2: "pool", 3: "pool_lrn", 4: "convert", 5: "softmax", 7: "conv_pool",
                   6: "unpack"}
 
     def steps(self):

@@ -74,9 +74,11 @@ def test_finalize_matches_reference(setup):
             assert q.as_tuple() == rn.blob_qvals(b).as_tuple(), b
 
 
-def test_alexnet_int8_bit_exact(setup):
+@pytest.mark.parametrize("batch", [2, 7])
+def test_alexnet_int8_bit_exact(setup, batch):
+    """Checkpoints vs reference prefix nets.  pool1 is the front kernel's output (conv1 +
+    relu1 + pool1 fused); batch 7 leaves the last image quad with one and a half pairs."""
     ref, g, params, ranges, ours = setup
-    batch = 2
     x = graphs.synth_images(batch, (3, 227, 227), offset=0)
     out = ours.forward({"data": x})["prob"]
     plan = ours.plan(batch)
@@ -84,7 +86,8 @@ def test_alexnet_int8_bit_exact(setup):
     assert st["kernels_per_forward"] <= 16
     # checkpoints: reference prefix nets give the reference's blob at that point
     names = [l["name"] for l in g["layers"]]
-    for ck in ("relu1", "norm1", "relu2", "relu5", "pool5", "relu7", "fc8"):
+    assert "conv_pool" in [s[1] for s in plan.steps()]
+    for ck in ("pool1", "norm1", "relu2", "relu5", "pool5", "relu7", "fc8"):
         prefix = {"name": "alexnet_prefix", "layers": g["layers"][: names.index(ck) + 1]}
         pr = {k: v for k, v in params.items() if k.split(".")[0] in names[: names.index(ck) + 1]}
         rn = ref_net(ref, prefix, "int8", pr, ranges)
@@ -189,3 +192,27 @@ def test_device_resident_batch(setup):
         torch.cuda.synchronize()
         assert torch.equal(got[:n], want), n
         assert bool((got[n:] == -7.0).all()), n
+
+
+def test_front_zero_point_row_fallback(setup, monkeypatch):
+    """The conv1 front kernel runs its A operand as s8 (w - zW) when every weight fits;
+    otherwise an extra A row of zW gives zW * rowsum, which the lane quarter holding it
+    hands to the others through shared memory.  Both forms give the same pool1 bytes and
+    the same network output (the reference comparison is test_alexnet_int8_bit_exact)."""
+    ref, g, params, ranges, ours = setup
+    batch = 9
+    x = graphs.synth_images(batch, (3, 227, 227), offset=41)
+    pa = ours.plan(batch)
+    out_sa = ours.forward({"data": x})["prob"]
+    pool_sa = pa.blob("pool1")[0].copy()
+    monkeypatch.setenv("QNB_FRONT_NO_SA", "1")
+    net = Net(G.override_precision(g, "int8"))
+    for k, (arr, dt, qv) in ours.params.items():
+        net.set_param(k, arr, dt, qv)
+    net.blob_qv = dict(ours.blob_qv)
+    net.set_quant_mode(QUANTIZED)
+    out_row = net.forward({"data": x})["prob"]
+    pb = net.plan(batch)
+    assert "conv_pool" in [s[1] for s in pb.steps()]
+    assert np.array_equal(pb.blob("pool1")[0], pool_sa)
+    assert np.array_equal(out_row, out_sa)

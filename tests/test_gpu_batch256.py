@@ -3,9 +3,10 @@ compiled at max_batch=256 and run on the full 256-image batch, exactly as bench.
 it, and images {0-7, 248-255} are compared with the UNMODIFIED reference Net
 (`Net::forward`, /root/reference/proj/src/net.cpp:305-330) on the same images.
 
-At batch 256 every persistent GEMM CTA runs many tiles (AlexNet conv1's row-Hankel
-kernel: 6 930 tiles over 148 CTAs), so the double-buffered TMEM accumulator phases and the
-"both accumulators in flight" epilogue are exercised; at batch 2 they are not.  Integer
+At batch 256 every persistent GEMM CTA runs many tiles (AlexNet conv1 + relu1 + pool1 in
+the front kernel: 3 456 pool rows in bands over 148 CTAs, ~48 conv rows each), so the
+double-buffered TMEM accumulator phases, the input-row ring and the band hand-overs are
+exercised; at batch 2 they are not.  Integer
 checkpoints must be bit-identical; the FP32 softmax sink within 1 ulp."""
 import json
 import os
@@ -85,7 +86,7 @@ def alexnet256():
     return ref, g, params, ranges, ours, plan, x, od.cpu().numpy()
 
 
-@pytest.mark.parametrize("ck", ["relu1", "norm1", "relu2", "relu5", "pool5", "relu7", "fc8"])
+@pytest.mark.parametrize("ck", ["pool1", "norm1", "relu2", "relu5", "pool5", "relu7", "fc8"])
 def test_alexnet_int8_b256_checkpoints_bit_exact(alexnet256, ck):
     ref, g, params, ranges, ours, plan, x, _ = alexnet256
     names = [l["name"] for l in g["layers"]]
