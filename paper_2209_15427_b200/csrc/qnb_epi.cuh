@@ -102,11 +102,11 @@ __device__ __forceinline__ uint32_t relu_lut32(uint32_t lutb, int32_t v) {
 
 // F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32; bit 2: clamp-free ReLU tail;
 // bit 3: ReLU through the replicated smem table (lutb).
-template <bool RELU, int F>
-__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk,
-                                            uint32_t lutb = 0) {
-  int32_t q;  // RNE quotient (before the output zero point)
-  if constexpr ((F & 1) != 0) {
+// RNE quotient of q8_fast (before the output zero point and the clamp).
+template <bool HI>
+__device__ __forceinline__ int32_t q8_quot(int32_t acc, const Q8Consts& k) {
+  int32_t q;
+  if constexpr (HI) {
     const int64_t pr = mulwide_s32(acc, k.mult32);
     const uint32_t b = ((uint32_t)(pr >> 32) >> k.sh) & 1u;
     const int64_t t = pr + (k.halfm1 + (int64_t)b);
@@ -119,9 +119,20 @@ __device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, cons
     qq = qq < -lim ? -lim : (qq > lim ? lim : qq);
     q = (int32_t)max(min(qq, (int64_t)INT32_MAX / 2), (int64_t)INT32_MIN / 2);
   }
-  if constexpr (RELU && (F & 8) != 0) return relu_lut32(lutb, min(max(q + k.oz, k.omin), k.omax));
-  if constexpr (RELU) return relu_tail<(F & 2) != 0, (F & 4) != 0>(q, rk);
-  return (uint32_t)min(max(q + k.oz, k.omin), k.omax);
+  return q;
+}
+// requant_clamp's value (before any ReLU).
+template <bool HI>
+__device__ __forceinline__ int32_t q8_clamped(int32_t acc, const Q8Consts& k) {
+  return min(max(q8_quot<HI>(acc, k) + k.oz, k.omin), k.omax);
+}
+
+template <bool RELU, int F>
+__device__ __forceinline__ uint32_t q8_fast(int32_t acc, const Q8Consts& k, const ReluFastK& rk,
+                                            uint32_t lutb = 0) {
+  if constexpr (RELU && (F & 8) != 0) return relu_lut32(lutb, q8_clamped<(F & 1) != 0>(acc, k));
+  if constexpr (RELU) return relu_tail<(F & 2) != 0, (F & 4) != 0>(q8_quot<(F & 1) != 0>(acc, k), rk);
+  return (uint32_t)q8_clamped<(F & 1) != 0>(acc, k);
 }
 
 

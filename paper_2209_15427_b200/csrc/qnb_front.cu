@@ -53,7 +53,7 @@ namespace qnb {
 constexpr int kFrWarps = 18;
 constexpr int kFrThreads = kFrWarps * 32;
 constexpr int kFrMma = 16, kFrProducer = 17;
-constexpr int kFrRing = 20;            // input rows held in smem
+constexpr int kFrRing = 28;            // input rows held in smem (a tile needs kh = 11)
 constexpr int kFrRow = 4 * kHkSlot;    // one ring row: input row y of image pairs 2q and 2q+1
 constexpr int kFrN = 4 * 64;           // MMA N: 64 pixel columns per image
 constexpr int kFrCols = 56;            // pixel columns an epilogue thread drains (ow <= 56)
@@ -81,7 +81,7 @@ __device__ __forceinline__ void front_walk(int u0, int u1, int ph, int quads_liv
   }
 }
 
-template <bool HI, bool SA>
+template <bool HI, bool SA, int PIX_>
 __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_constant__ FrontArgs p) {
   griddep_launch_dependents();
   extern __shared__ uint8_t smem_raw[];
@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rt_full + 16);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // relu_quant table replicated per lane (entry v of lane L at ((v >> 2) * 32 + L) * 4 + (v & 3))
+  // relu_quant table replicated per lane (entry v of lane L at ((v >> 2) * 32 + L) * 4 + (v & 3)):
+  // a warp's lookups hit 32 distinct banks
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     const int v = i >> 5, l = i & 31;
     relu_tab[((v >> 2) * 32 + l) * 4 + (v & 3)] = __ldg(p.relu_lut + v);
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
         const bool two = 2 * quad + 1 < pairs;
         const uint8_t* src = p.a + (int64_t)(2 * quad) * p.a_img + p.a_origin;
         for (int y = y0; y < y1; ++y, ++seq) {
+          if ((p.dbg & 64) && seq >= kFrRing) continue;  // probe: no ring traffic after the first fill
           const uint32_t s = seq % kFrRing;
           mbar_wait(&row_empty[s], ((seq / kFrRing) & 1) ^ 1);
           mbar_arrive_expect_tx(&row_full[s], two ? 2 * 2 * kHkSlot : 2 * kHkSlot);
@@ -175,22 +177,23 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
         seq_next += (uint32_t)((R1 - R0) * p.sh + p.kh);
       }
       const uint32_t buf = j & 1;
-      mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+      if (!(p.dbg & 8)) mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
       const uint32_t need = seq_run + (uint32_t)((r - R0) * p.sh + p.kh);
-      for (; waited < need; ++waited) mbar_wait(&row_full[waited % kFrRing], (waited / kFrRing) & 1);
+      for (; waited < need; ++waited)
+        if (!(p.dbg & 4)) mbar_wait(&row_full[waited % kFrRing], (waited / kFrRing) & 1);
       tc_fence_after();
       const uint32_t dt = tmem + buf * (uint32_t)kFrN;
       const uint32_t row0 = seq_run + (uint32_t)((r - R0) * p.sh);  // ring sequence of input row r*sh
       if (elect_one()) {
         if (!(p.dbg & 2))
-        for (int kr = 0; kr < p.kh; ++kr) {
-          const uint32_t rs = (row0 + kr) % kFrRing;
-          for (int q = 0; q < ksteps; ++q) {
-            const uint32_t kk = (uint32_t)(kr * p.kpr + q * 32);  // K byte in the packed A order
-            umma<KIND_I8>(dt, wd0 + (kk >> 7) * (kFrABlock >> 4) + 2 * ((kk & 127) >> 5),
-                          rd0 + ((rs * kFrRow + q * 32) >> 4), idesc, (kr | q) != 0);
+          for (int kr = 0; kr < p.kh; ++kr) {
+            const uint32_t rs = (row0 + kr) % kFrRing;
+            for (int q = 0; q < ksteps; ++q) {
+              const uint32_t kk = (uint32_t)(kr * p.kpr + q * 32);  // K byte in the packed A order
+              umma<KIND_I8>(dt, wd0 + (kk >> 7) * (kFrABlock >> 4) + 2 * ((kk & 127) >> 5),
+                            rd0 + ((rs * kFrRow + q * 32) >> 4), idesc, (kr | q) != 0);
+            }
           }
-        }
         tc_commit(&acc_full[buf]);
         // ring rows the next tile of the run no longer reads (all of them after the last)
         const uint32_t nfree = r == R1 ? (uint32_t)p.kh : (uint32_t)p.sh;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
     const bool rs_lane = !SA && quarter == 3 && lane == p.cpq;  // TMEM lane 96 + cpq: zW * rowsum
     const Q8Consts k = q8_consts(p.rq);
     const uint32_t lutb = smem_u32(relu_tab) + (uint32_t)lane * 4u;
-    constexpr int F = 8 | (HI ? 1 : 0);  // q8_fast: table ReLU (+ high-word requant)
+    const int64_t PIX = PIX_ ? PIX_ : p.D.pix;  // pooled-blob pixel stride (compile-time for AlexNet)
     const int pw = p.pw;
     int32_t acc[kFrPW];
 #pragma unroll
@@ -235,8 +238,8 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
       const int n = 4 * quad + img;
       const bool store = ch_ok && n < n_live;
       uint8_t* dst = p.out + img_off(p.D, n) + (int64_t)((r >> 1) - 1) * p.D.row + p.D.origin + ch;
-      const int64_t dpix = p.D.pix;
-      // window maxima h[q] (q in [Q0, Q1), held in hv[q - Q0]) -> running max / requant + store
+      // window maxima h[q] (q in [Q0, Q1), held in hv[q - Q0]) -> running max / requant + store.
+      // SA: the channel constant is added once per pooled value (max commutes with + cc).
       auto pool_cols = [&](auto Q0c, auto Q1c, const uint32_t* hv) {
         constexpr int Q0 = decltype(Q0c)::value, Q1 = decltype(Q1c)::value;
         if (mode == 0) {
@@ -248,8 +251,11 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
         } else {
           if (store) {
 #pragma unroll
-            for (int q = Q0; q < Q1; ++q)
-              if (q < pw) dst[q * dpix] = (uint8_t)q8_fast<true, F>(max(acc[q], (int32_t)hv[q - Q0]), k, ReluFastK{}, lutb);
+            for (int q = Q0; q < Q1; ++q) {
+              if (q >= pw) break;
+              const int32_t a = max(acc[q], (int32_t)hv[q - Q0]) + (SA ? cc : 0);
+              dst[q * PIX] = (uint8_t)relu_lut32(lutb, q8_clamped<HI>(a, k));
+            }
           }
           if (mode == 2) {
 #pragma unroll
@@ -258,13 +264,11 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
         }
       };
       // acc = dot + chan_const - zW * rowsum (the reference's exact integer accumulator);
-      // SA: the A operand holds w - zW as s8, so dot already carries the correction
+      // SA: the A operand holds w - zW as s8, so dot already carries the zero-point term
       auto add_consts = [&](uint32_t* v, int n_cols, int col0) {
+        if constexpr (!SA) {
 #pragma unroll
-        for (int x = 0; x < n_cols; x += 4) {
-          if constexpr (SA) {
-            v[x] += (uint32_t)cc, v[x + 1] += (uint32_t)cc, v[x + 2] += (uint32_t)cc, v[x + 3] += (uint32_t)cc;
-          } else {
+          for (int x = 0; x < n_cols; x += 4) {
             const int4 t = lds_v4(rtb + 4u * (uint32_t)(col0 + x));
             v[x] = (uint32_t)((int32_t)v[x] + cc - t.x);
             v[x + 1] = (uint32_t)((int32_t)v[x + 1] + cc - t.y);
@@ -273,57 +277,55 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
           }
         }
       };
-      // Two halves of the row (18 warps leave 96 registers per thread): columns 0-31 (+32)
-      // give pooled columns 0-15, columns 32-55 pooled columns 16-26.  Without SA the
+      // The row in two halves (18 warps leave 96 registers per thread).  Without SA the
       // zW*rowsum lane publishes each half's columns first (rt_full[buf][img][half]).
-      {
-        uint32_t v[36];
-        tmem_ld32(ta, v);
-        tmem_ld1(ta + 32, v[32]);
-        tmem_ld_wait();
+      // columns 0-31 (+32) -> window maxima of pooled columns 0-15 (in place in v[0..15])
+      uint32_t v[36];
+      tmem_ld32(ta, v);
+      tmem_ld1(ta + 32, v[32]);
+      tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) reg_pin8(v + i);
-        reg_pin1(v[32]);
-        v[33] = v[34] = v[35] = 0;
-        if constexpr (!SA) {
-          if (rs_lane) {
+      for (int i = 0; i < 32; i += 8) reg_pin8(v + i);
+      reg_pin1(v[32]);
+      v[33] = v[34] = v[35] = 0;
+      if constexpr (!SA) {
+        if (rs_lane) {
 #pragma unroll
-            for (int x = 0; x < 36; x += 4) sts_v4(rtb + 4u * (uint32_t)x, v[x], v[x + 1], v[x + 2], v[x + 3]);
-            mbar_arrive(&rt_full[(buf * 4 + img) * 2]);
-          }
-          mbar_wait(&rt_full[(buf * 4 + img) * 2], par);
+          for (int x = 0; x < 36; x += 4) sts_v4(rtb + 4u * (uint32_t)x, v[x], v[x + 1], v[x + 2], v[x + 3]);
+          mbar_arrive(&rt_full[(buf * 4 + img) * 2]);
         }
-        add_consts(v, 36, 0);
-#pragma unroll
-        for (int q = 0; q < 16; ++q)  // in place: h[q] overwrites column q <= 2q
-          v[q] = (uint32_t)max(max((int32_t)v[2 * q], (int32_t)v[2 * q + 1]), (int32_t)v[2 * q + 2]);
-        pool_cols(std::integral_constant<int, 0>{}, std::integral_constant<int, 16>{}, v);
+        mbar_wait(&rt_full[(buf * 4 + img) * 2], par);
       }
-      {
-        uint32_t w[24];  // columns 32-55
-        tmem_ld16p(ta + 32, w);
-        tmem_ld8p(ta + 48, w + 16);
-        tmem_ld_wait();
+      add_consts(v, 36, 0);
 #pragma unroll
-        for (int i = 0; i < 24; i += 8) reg_pin8(w + i);
-        if constexpr (!SA) {
-          if (rs_lane) {
+      for (int q = 0; q < 16; ++q)  // h[q] overwrites column q <= 2q
+        v[q] = (uint32_t)max(max((int32_t)v[2 * q], (int32_t)v[2 * q + 1]), (int32_t)v[2 * q + 2]);
+      // columns 32-55 -> pooled columns 16-26 (h[q] in w[q - 16])
+      uint32_t w[24];
+      tmem_ld16p(ta + 32, w);
+      tmem_ld8p(ta + 48, w + 16);
+      tmem_ld_wait();
 #pragma unroll
-            for (int x = 0; x < 24; x += 4) sts_v4(rtb + 4u * (uint32_t)(32 + x), w[x], w[x + 1], w[x + 2], w[x + 3]);
-            mbar_arrive(&rt_full[(buf * 4 + img) * 2 + 1]);
-          }
-          mbar_wait(&rt_full[(buf * 4 + img) * 2 + 1], par);
+      for (int i = 0; i < 24; i += 8) reg_pin8(w + i);
+      if constexpr (!SA) {
+        if (rs_lane) {
+#pragma unroll
+          for (int x = 0; x < 24; x += 4) sts_v4(rtb + 4u * (uint32_t)(32 + x), w[x], w[x + 1], w[x + 2], w[x + 3]);
+          mbar_arrive(&rt_full[(buf * 4 + img) * 2 + 1]);
         }
-        add_consts(w, 24, 32);
-        // every read of this accumulator and of rt[buf] is done: hand both back
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
-#pragma unroll
-        for (int q = 16; q < kFrPW; ++q)  // column 32 + c lives in w[c]; h[q] -> w[q - 16]
-          w[q - 16] = (uint32_t)max(max((int32_t)w[2 * q - 32], (int32_t)w[2 * q - 31]), (int32_t)w[2 * q - 30]);
-        pool_cols(std::integral_constant<int, 16>{}, std::integral_constant<int, kFrPW>{}, w);
+        mbar_wait(&rt_full[(buf * 4 + img) * 2 + 1], par);
       }
+      add_consts(w, 24, 32);
+      // every read of this accumulator and of rt[buf] is done: hand both back before the
+      // running-max / requant work
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+#pragma unroll
+      for (int q = 16; q < kFrPW; ++q)
+        w[q - 16] = (uint32_t)max(max((int32_t)w[2 * q - 32], (int32_t)w[2 * q - 31]), (int32_t)w[2 * q - 30]);
+      pool_cols(std::integral_constant<int, 0>{}, std::integral_constant<int, 16>{}, v);
+      pool_cols(std::integral_constant<int, 16>{}, std::integral_constant<int, kFrPW>{}, w);
     });
   }
   tc_fence_before();
@@ -346,7 +348,7 @@ bool front_geometry_ok(const IgemmGeometry& g, const ActLayout& in, int64_t pool
   if (pw > kFrPW || 2 * pw + 1 > kFrCols) return false;
   if (g.sh > g.kh || g.kh + g.sh > kFrRing) return false;  // the ring holds a tile and the next rows
   const int64_t kpr = round_up(g.kw * in.pix(), 32);
-  if (round_up(g.kh * kpr, 128) / 128 * kFrABlock + (size_t)kFrRing * kFrRow > 200 * 1024) return false;
+  if (front_smem_bytes((int)(round_up(g.kh * kpr, 128) / 128)) > 227 * 1024) return false;
   return true;
 }
 
@@ -391,11 +393,11 @@ static int front_sms() {
   return n;
 }
 
-template <bool HI, bool SA>
+template <bool HI, bool SA, int PIX_>
 static qnb_status launch_front_t(const FrontArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    QNB_CUDA(cudaFuncSetAttribute(front_kernel<HI, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    QNB_CUDA(cudaFuncSetAttribute(front_kernel<HI, SA, PIX_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
   const size_t smem = front_smem_bytes(a.num_kb);
@@ -413,7 +415,7 @@ static qnb_status launch_front_t(const FrontArgs& a, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = std::getenv("QNB_NO_PDL") ? 0 : 1;
-  QNB_CUDA(cudaLaunchKernelEx(&cfg, front_kernel<HI, SA>, a));
+  QNB_CUDA(cudaLaunchKernelEx(&cfg, front_kernel<HI, SA, PIX_>, a));
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;
@@ -427,8 +429,13 @@ qnb_status launch_front(const FrontArgs& a0, cudaStream_t s) {
   }();
   FrontArgs a = a0;
   a.dbg |= dbg;
-  if (a.signed_a) return a.rq.s >= 32 ? launch_front_t<true, true>(a, s) : launch_front_t<false, true>(a, s);
-  return a.rq.s >= 32 ? launch_front_t<true, false>(a, s) : launch_front_t<false, false>(a, s);
+  const bool hi = a.rq.s >= 32;
+  if (a.D.pix == 96) {  // AlexNet pool1: 96 channels, compile-time store stride
+    if (a.signed_a) return hi ? launch_front_t<true, true, 96>(a, s) : launch_front_t<false, true, 96>(a, s);
+    return hi ? launch_front_t<true, false, 96>(a, s) : launch_front_t<false, false, 96>(a, s);
+  }
+  if (a.signed_a) return hi ? launch_front_t<true, true, 0>(a, s) : launch_front_t<false, true, 0>(a, s);
+  return hi ? launch_front_t<true, false, 0>(a, s) : launch_front_t<false, false, 0>(a, s);
 }
 
 }  // namespace qnb
