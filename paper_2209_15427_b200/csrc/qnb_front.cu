@@ -50,10 +50,9 @@
 
 namespace qnb {
 
+constexpr int kFrWarps = 18;
+constexpr int kFrThreads = kFrWarps * 32;
 constexpr int kFrMma = 16, kFrProducer = 17;
-constexpr int kFrConvWarps = 3;  // fused pack: warps 17-19 quantize the FP32 input rows into the ring
-constexpr int kFrConvTasks = 10; // (image, pixel) tasks per converter thread and batch of loads
-__host__ __device__ constexpr int front_threads(bool pack) { return (pack ? 17 + kFrConvWarps : 18) * 32; }
 constexpr int kFrRing = 28;            // input rows held in smem (a tile needs kh = 11)
 constexpr int kFrRow = 4 * kHkSlot;    // one ring row: input row y of image pairs 2q and 2q+1
 constexpr int kFrN = 4 * 64;           // MMA N: 64 pixel columns per image
@@ -82,8 +81,8 @@ __device__ __forceinline__ void front_walk(int u0, int u1, int ph, int quads_liv
   }
 }
 
-template <bool HI, bool SA, int PIX_, bool PACK>
-__global__ void __launch_bounds__(front_threads(PACK), 1) front_kernel(const __grid_constant__ FrontArgs p) {
+template <bool HI, bool SA, int PIX_>
+__global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_constant__ FrontArgs p) {
   griddep_launch_dependents();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(front_threads(PACK), 1) front_kernel(const __g
   if (threadIdx.x == 0) {
     mbar_init(w_full, 1);
     for (int i = 0; i < kFrRing; ++i) {
-      mbar_init(&row_full[i], PACK ? kFrConvWarps * 32 : 1);
+      mbar_init(&row_full[i], 1);
       mbar_init(&row_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -133,8 +132,8 @@ __global__ void __launch_bounds__(front_threads(PACK), 1) front_kernel(const __g
   const int u0 = (int)((int64_t)units * blockIdx.x / gridDim.x);
   const int u1 = (int)((int64_t)units * (blockIdx.x + 1) / gridDim.x);
 
-  if (warp >= kFrProducer) {
-    if (warp == kFrProducer && lane == 0) {  // the weights do not depend on the preceding grid
+  if (warp == kFrProducer) {
+    if (lane == 0) {  // the weights do not depend on the preceding grid
       mbar_arrive_expect_tx(w_full, (uint32_t)(p.num_kb * kFrABlock));
       for (int kb = 0; kb < p.num_kb; ++kb)
         bulk_g2s(sW + (size_t)kb * kFrABlock, p.w + (size_t)kb * kFrABlock, kFrABlock, w_full);
@@ -142,48 +141,7 @@ __global__ void __launch_bounds__(front_threads(PACK), 1) front_kernel(const __g
     __syncwarp();
     griddep_wait();
     const int n_live = p.dyn_n ? min(p.batch, __ldg(p.dyn_n)) : p.batch;
-    if constexpr (PACK) {
-      // Input rows straight from the FP32 NCHW batch: quantize_value (src/quantizer.cpp:
-      // 103-109, the pack kernel's qz8 contract) into the ring row's 1024-byte image slots,
-      // pixel x at byte 4x, channels 0..C-1 (the padding channel meets zero weights)
-      const int ct = threadIdx.x - kFrProducer * 32, W = p.x_w, C = p.x_c;
-      const int64_t plane = (int64_t)p.x_h * W;
-      const float invf = (float)p.xq.inv, zf = (float)p.xq.zero, lo = (float)p.xq.i_min, hi = (float)p.xq.i_max;
-      uint32_t seq = 0;
-      front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int quad, int r, int R0, int) {
-        const int y0 = r == R0 ? r * p.sh : (r - 1) * p.sh + p.kh, y1 = r * p.sh + p.kh;
-        for (int y = y0; y < y1; ++y, ++seq) {
-          const uint32_t s = seq % kFrRing;
-          mbar_wait(&row_empty[s], ((seq / kFrRing) & 1) ^ 1);
-          const uint32_t rowb = smem_u32(ring + (size_t)s * kFrRow);
-          for (int t0 = ct; t0 < 4 * W; t0 += kFrConvWarps * 32 * kFrConvTasks) {
-            float v[kFrConvTasks][4];
-#pragma unroll
-            for (int u = 0; u < kFrConvTasks; ++u) {
-              const int t = t0 + u * kFrConvWarps * 32;
-              const int i = (t >= W) + (t >= 2 * W) + (t >= 3 * W), x = t - i * W, n = 4 * quad + i;
-              const bool ok = t < 4 * W && n < p.batch;
-              const float* src = p.x + ((int64_t)n * C * plane + (int64_t)y * W + x);
-#pragma unroll
-              for (int c = 0; c < 4; ++c) v[u][c] = (ok && c < C) ? __ldg(src + c * plane) : 0.0f;
-            }
-#pragma unroll
-            for (int u = 0; u < kFrConvTasks; ++u) {
-              const int t = t0 + u * kFrConvWarps * 32;
-              if (t >= 4 * W) break;
-              const int i = (t >= W) + (t >= 2 * W) + (t >= 3 * W), x = t - i * W;
-              uint32_t word = 0;
-#pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (c < C) word |= (qz8(v[u][c], p.xq, invf, zf, lo, hi) & 0xFFu) << (8 * c);
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowb + (uint32_t)(i * kHkSlot + 4 * x)), "r"(word) : "memory");
-            }
-          }
-          fence_proxy_async_smem();  // generic-proxy writes -> the tensor core's async-proxy reads
-          mbar_arrive(&row_full[s]);
-        }
-      });
-    } else if (warp == kFrProducer && lane == 0) {
+    if (lane == 0) {
       uint32_t seq = 0;
       front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int quad, int r, int R0, int) {
         const int y0 = r == R0 ? r * p.sh : (r - 1) * p.sh + p.kh, y1 = r * p.sh + p.kh;
@@ -435,11 +393,11 @@ static int front_sms() {
   return n;
 }
 
-template <bool HI, bool SA, int PIX_, bool PACK>
+template <bool HI, bool SA, int PIX_>
 static qnb_status launch_front_t(const FrontArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    QNB_CUDA(cudaFuncSetAttribute(front_kernel<HI, SA, PIX_, PACK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    QNB_CUDA(cudaFuncSetAttribute(front_kernel<HI, SA, PIX_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
   const size_t smem = front_smem_bytes(a.num_kb);
@@ -449,7 +407,7 @@ static qnb_status launch_front_t(const FrontArgs& a, cudaStream_t s) {
   const int64_t grid = std::min<int64_t>(units, front_sms());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(front_threads(PACK));
+  cfg.blockDim = dim3(kFrThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -457,7 +415,7 @@ static qnb_status launch_front_t(const FrontArgs& a, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = std::getenv("QNB_NO_PDL") ? 0 : 1;
-  QNB_CUDA(cudaLaunchKernelEx(&cfg, front_kernel<HI, SA, PIX_, PACK>, a));
+  QNB_CUDA(cudaLaunchKernelEx(&cfg, front_kernel<HI, SA, PIX_>, a));
   count_launch();
   QNB_CUDA(cudaGetLastError());
   return QNB_OK;
@@ -471,21 +429,13 @@ qnb_status launch_front(const FrontArgs& a0, cudaStream_t s) {
   }();
   FrontArgs a = a0;
   a.dbg |= dbg;
-  const bool hi = a.rq.s >= 32, pk = a.x_c > 0;
-#define QNB_FRONT_L(PX, PK_)                                                                 \
-  if (a.signed_a) return hi ? launch_front_t<true, true, PX, PK_>(a, s) : launch_front_t<false, true, PX, PK_>(a, s); \
-  return hi ? launch_front_t<true, false, PX, PK_>(a, s) : launch_front_t<false, false, PX, PK_>(a, s)
+  const bool hi = a.rq.s >= 32;
   if (a.D.pix == 96) {  // AlexNet pool1: 96 channels, compile-time store stride
-    if (pk) {
-      QNB_FRONT_L(96, true);
-    }
-    QNB_FRONT_L(96, false);
+    if (a.signed_a) return hi ? launch_front_t<true, true, 96>(a, s) : launch_front_t<false, true, 96>(a, s);
+    return hi ? launch_front_t<true, false, 96>(a, s) : launch_front_t<false, false, 96>(a, s);
   }
-  if (pk) {
-    QNB_FRONT_L(0, true);
-  }
-  QNB_FRONT_L(0, false);
-#undef QNB_FRONT_L
+  if (a.signed_a) return hi ? launch_front_t<true, true, 0>(a, s) : launch_front_t<false, true, 0>(a, s);
+  return hi ? launch_front_t<true, false, 0>(a, s) : launch_front_t<false, false, 0>(a, s);
 }
 
 }  // namespace qnb

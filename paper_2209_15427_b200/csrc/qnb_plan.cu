@@ -72,7 +72,6 @@ struct Op {
   int pack_op = PACK_COPY;
   int conv_op = CVT_CONVERT;
   int in_dtype = 0, out_dtype = 0;
-  bool fuse_pack = false;  // FRONT: quantizes the FP32 NCHW network input itself (no pack step)
 };
 
 enum Sym { SYM_NONE = 0, SYM_INPUT = 1, SYM_OUTPUT = 2 };
@@ -429,23 +428,6 @@ bool front_candidate(const qnb_plan& P, int conv, int relu, int pool) {
   return front_numeric(P, conv, relu).ok;
 }
 
-
-// INPUT -> QUANTIZER(INT8) -> conv1 where the front kernel quantizes the FP32 NCHW input
-// rows itself (src/quantizer.cpp:103-126): 3-4 channels, no conv padding, nothing inspected.
-bool front_pack_fusable(const qnb_plan& P, const Op& pack, int conv) {
-  // opt-in until its producer keeps up: the register-load converter measured 600 us (latency
-  // bound) against 64 + 79 us for the pack kernel + front kernel
-  if (!std::getenv("QNB_FRONT_PACK")) return false;
-  const qnb_layer_desc& l = P.layers[conv];
-  const Blob& src = P.blobs[pack.in];
-  const Blob& q = P.blobs[pack.out];
-  if (pack.pack_op != PACK_QUANTIZE || !src.external || src.dtype != QNB_FP32 || src.ndim != 4) return false;
-  if (q.dtype != QNB_INT8Q || !q.has_qv || q.inspect || only_consumer(P, pack.out) != conv) return false;
-  if (src.c < 1 || src.c > 4 || l.conv.pad_h != 0 || l.conv.pad_w != 0) return false;
-  if (src.w * 4 > kHkSlot) return false;
-  return true;
-}
-
 qnb_status lower(qnb_plan& P) {
   std::vector<bool> done(P.layers.size(), false);
   for (size_t i = 0; i < P.layers.size(); ++i) {
@@ -500,13 +482,6 @@ qnb_status lower(qnb_plan& P) {
             op.kind = OP_FRONT;
             op.pool = jp;
             op.out = P.layers[jp].top;
-            // the INPUT -> QUANTIZER pack that feeds it folds into the front kernel's producer
-            if (!P.ops.empty() && P.ops.back().kind == OP_PACK && P.ops.back().out == l.bottom &&
-                front_pack_fusable(P, P.ops.back(), (int)i)) {
-              op.in = P.ops.back().in;  // the external FP32 NCHW input
-              op.fuse_pack = true;
-              P.ops.pop_back();
-            }
           }
         }
         break;
@@ -606,7 +581,7 @@ qnb_status lower(qnb_plan& P) {
 qnb_status assign_layouts(qnb_plan& P) {
   // Each op's input blob (through aliases) gets the layout the op requires.
   for (const Op& op : P.ops) {
-    if (op.kind == OP_ALIAS || op.kind == OP_PACK || (op.kind == OP_FRONT && op.fuse_pack)) continue;
+    if (op.kind == OP_ALIAS || op.kind == OP_PACK) continue;
     const int r = root_of(P, op.in);
     Blob& b = P.blobs[r];
     if (b.external) return fail(QNB_E_ARG, "internal: external blob consumed by a device op");
@@ -936,11 +911,10 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
 qnb_status emit_front(qnb_plan& P, const Op& op, Step& st) {
   const qnb_layer_desc& l = P.layers[op.layer];
   const qnb_layer_desc& lp = P.layers[op.pool];
-  const Blob& in = P.blobs[l.bottom];  // the quantized conv input (fuse_pack: never materialised)
+  const Blob& in = P.blobs[op.in];
   const Blob& cout = P.blobs[l.top];
+  const ActLayout& Lin = blob_layout(P, op.in);
   const IgemmGeometry g = geometry_of(l, in, cout);
-  const ActLayout Lin = op.fuse_pack ? choose_input_layout(g, in.dtype, P.max_batch, in.c, in.h, in.w)
-                                     : blob_layout(P, op.in);
   if (!front_geometry_ok(g, Lin, lp.pool_kernel, lp.pool_stride))
     return fail(QNB_E_ARG, "internal: front step on an ineligible input layout");
   FrontNumeric fn = front_numeric(P, op.layer, op.relu);
@@ -954,17 +928,7 @@ qnb_status emit_front(qnb_plan& P, const Op& op, Step& st) {
   QNB_TRY(upload(P, cc32, const_cast<int32_t**>(&a.chan_const)));
   QNB_TRY(upload(P, fn.lut, const_cast<uint8_t**>(&a.relu_lut)));
   a.rq = to_dev(fn.rq);
-  if (op.fuse_pack) {  // the user's FP32 NCHW batch, bound per forward (SYM_INPUT)
-    const Blob& x = P.blobs[op.in];
-    a.x = nullptr;
-    a.x_c = (int32_t)x.c;
-    a.x_h = (int32_t)x.h;
-    a.x_w = (int32_t)x.w;
-    a.xq = dev_q(in.qv);
-    st.src_sym = SYM_INPUT;
-  } else {
-    a.a = blob_ptr(P, op.in);
-  }
+  a.a = blob_ptr(P, op.in);
   a.a_img = Lin.img();
   a.a_row = Lin.row();
   a.a_origin = (Lin.hh - g.ph) * Lin.row() + (Lin.hw - g.pw) * Lin.pix();
@@ -1196,10 +1160,7 @@ Step with_batch(const Step& s0, int64_t b, const void* in, void* out, const int3
     s.sm_S.dyn_n = dyn;
     s.up_S.dyn_n = dyn;
   }
-  if (s.src_sym == SYM_INPUT) {
-    s.pack.src = (const uint8_t*)in;
-    s.front.x = (const float*)in;
-  }
+  if (s.src_sym == SYM_INPUT) s.pack.src = (const uint8_t*)in;
   if (s.dst_sym == SYM_OUTPUT) {
     s.sm_out = (float*)out;
     s.up_dst = (uint8_t*)out;

@@ -118,10 +118,7 @@ struct FExactArgs {
 // pool1; src/ops.cpp:264-342, 156-181, 344-390).  Channels are the MMA's M rows (TMEM
 // lanes), pixels its N columns, so both pooling directions run in registers.
 struct FrontArgs {
-  const uint8_t* a;                // conv input, image-pair interleaved (1024-byte row slots), or
-  const float* x;                  // (fused pack) the FP32 NCHW network input, quantized by the kernel
-  int32_t x_c, x_h, x_w;           //   its channels / rows / columns
-  DevQ xq;                         //   the input quantizer (src/quantizer.cpp:103-126)
+  const uint8_t* a;                // conv input, image-pair interleaved (1024-byte row slots)
   int64_t a_img, a_row, a_origin;  // pair-image stride, pair-row stride (2048), window origin
   int32_t sh, kh, kpr;             // stride_h, filter rows, K bytes per filter row (multiple of 32)
   int32_t oh, ow, ph, pw;          // conv and pooled extents
