@@ -34,7 +34,10 @@
 // Warp roles (18 warps):
 //   0-15  epilogue: quarter = warp % 4 (TMEM lanes), image = warp / 4 (64 columns)
 //   16    TMEM allocator (512 columns: two 256-column accumulators) + MMA issuer
-//   17    producer: resident weights, then the input-row ring
+//   17    producer: resident weights, then the input-row ring (one barrier per tile's rows)
+//   18    gate: rows resident + accumulator drained -> go[buf], so the MMA warp waits on a
+//         single barrier per tile (each wait in the issuing warp idles the tensor pipe for
+//         ~250 cycles, scripts/probe/umma_ring.cu)
 #include <cuda.h>
 
 #include <algorithm>
@@ -50,9 +53,10 @@
 
 namespace qnb {
 
-constexpr int kFrWarps = 18;
+constexpr int kFrWarps = 19;
 constexpr int kFrThreads = kFrWarps * 32;
-constexpr int kFrMma = 16, kFrProducer = 17;
+constexpr int kFrMma = 16, kFrProducer = 17, kFrGate = 18;
+constexpr int kFrGrp = 8;              // tile row-groups in flight (> ring rows / stride)
 constexpr int kFrRing = 28;            // input rows held in smem (a tile needs kh = 11)
 constexpr int kFrRow = 4 * kHkSlot;    // one ring row: input row y of image pairs 2q and 2q+1
 constexpr int kFrN = 4 * 64;           // MMA N: 64 pixel columns per image
@@ -64,7 +68,7 @@ static size_t front_smem_bytes(int num_kb) {
   return 1024 + (size_t)num_kb * kFrABlock + (size_t)kFrRing * kFrRow + 1024  // ring + K overrun slack
          + 2 * 4 * 64 * 4                                                     // zW*rowsum per column
          + 8192                                                                // replicated ReLU table
-         + (1 + 2 * kFrRing + 2 + 2 + 16) * 8 + 16;                             // barriers + TMEM slot
+         + (1 + kFrRing + 2 + 2 + 16 + kFrGrp + 2) * 8 + 16;                // barriers + TMEM slot
 }
 
 // The band of pool rows [u0, u1) of the flattened (image quad, pool row) space, as the
@@ -91,12 +95,13 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   int32_t* rt = reinterpret_cast<int32_t*>(ring + kFrRing * kFrRow + 1024);  // [2 buf][4 img][64]
   uint8_t* relu_tab = reinterpret_cast<uint8_t*>(rt + 2 * 4 * 64);
   uint64_t* w_full = reinterpret_cast<uint64_t*>(relu_tab + 8192);
-  uint64_t* row_full = w_full + 1;
-  uint64_t* row_empty = row_full + kFrRing;
+  uint64_t* row_empty = w_full + 1;
   uint64_t* acc_full = row_empty + kFrRing;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* rt_full = acc_empty + 2;  // [2 buf][4 img][2 halves]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rt_full + 16);
+  uint64_t* grp_full = rt_full + 16;  // [kFrGrp]: a tile's new input rows (one complete_tx group)
+  uint64_t* go = grp_full + kFrGrp;     // [2]: rows resident AND accumulator free -> the MMA warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // relu_quant table replicated per lane (entry v of lane L at ((v >> 2) * 32 + L) * 4 + (v & 3)):
@@ -107,15 +112,14 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   }
   if (threadIdx.x == 0) {
     mbar_init(w_full, 1);
-    for (int i = 0; i < kFrRing; ++i) {
-      mbar_init(&row_full[i], 1);
-      mbar_init(&row_empty[i], 1);
-    }
+    for (int i = 0; i < kFrRing; ++i) mbar_init(&row_empty[i], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 16);
     }
     for (int i = 0; i < 16; ++i) mbar_init(&rt_full[i], 1);
+    for (int i = 0; i < kFrGrp; ++i) mbar_init(&grp_full[i], 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&go[i], 1);
     fence_barrier_init();
   }
   if (warp == kFrMma) {
@@ -142,21 +146,37 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
     griddep_wait();
     const int n_live = p.dyn_n ? min(p.batch, __ldg(p.dyn_n)) : p.batch;
     if (lane == 0) {
-      uint32_t seq = 0;
+      uint32_t seq = 0, jt = 0;
       front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int quad, int r, int R0, int) {
         const int y0 = r == R0 ? r * p.sh : (r - 1) * p.sh + p.kh, y1 = r * p.sh + p.kh;
         const bool two = 2 * quad + 1 < pairs;
         const uint8_t* src = p.a + (int64_t)(2 * quad) * p.a_img + p.a_origin;
+        // all of this tile's new rows complete one group barrier (the MMA warp then waits
+        // once per tile: every mbarrier wait in the issuing warp idles the tensor pipe)
+        uint64_t* gb = &grp_full[jt % kFrGrp];
+        ++jt;
+        mbar_arrive_expect_tx(gb, (uint32_t)((y1 - y0) * (two ? 2 : 1) * 2 * kHkSlot));
         for (int y = y0; y < y1; ++y, ++seq) {
-          if ((p.dbg & 64) && seq >= kFrRing) continue;  // probe: no ring traffic after the first fill
           const uint32_t s = seq % kFrRing;
           mbar_wait(&row_empty[s], ((seq / kFrRing) & 1) ^ 1);
-          mbar_arrive_expect_tx(&row_full[s], two ? 2 * 2 * kHkSlot : 2 * kHkSlot);
-          bulk_g2s(ring + (size_t)s * kFrRow, src + (int64_t)y * p.a_row, 2 * kHkSlot, &row_full[s]);
+          bulk_g2s(ring + (size_t)s * kFrRow, src + (int64_t)y * p.a_row, 2 * kHkSlot, gb);
           if (two)
-            bulk_g2s(ring + (size_t)s * kFrRow + 2 * kHkSlot, src + p.a_img + (int64_t)y * p.a_row, 2 * kHkSlot,
-                     &row_full[s]);
+            bulk_g2s(ring + (size_t)s * kFrRow + 2 * kHkSlot, src + p.a_img + (int64_t)y * p.a_row, 2 * kHkSlot, gb);
         }
+      });
+    }
+    __syncwarp();
+  } else if (warp == kFrGate) {
+    // tile j may start when its rows are resident and its accumulator was drained
+    griddep_wait();
+    const int n_live = p.dyn_n ? min(p.batch, __ldg(p.dyn_n)) : p.batch;
+    if (lane == 0) {
+      uint32_t j = 0;
+      front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int, int, int, int) {
+        mbar_wait(&grp_full[j % kFrGrp], (j / kFrGrp) & 1);
+        mbar_wait(&acc_empty[j & 1], ((j >> 1) & 1) ^ 1);
+        mbar_arrive(&go[j & 1]);
+        ++j;
       });
     }
     __syncwarp();
@@ -170,17 +190,14 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
     const uint64_t wd0 = smem_desc_sw128(sW);
     const uint64_t rd0 = smem_desc_none(ring, 16, 128);
     const int ksteps = p.kpr / 32;
-    uint32_t j = 0, waited = 0, seq_next = 0, seq_run = 0;
+    uint32_t j = 0, seq_next = 0, seq_run = 0;
     front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int, int r, int R0, int R1) {
       if (r == R0) {  // a run loads rows [R0 sh, R1 sh + kh) contiguously in the ring sequence
         seq_run = seq_next;
         seq_next += (uint32_t)((R1 - R0) * p.sh + p.kh);
       }
       const uint32_t buf = j & 1;
-      if (!(p.dbg & 8)) mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
-      const uint32_t need = seq_run + (uint32_t)((r - R0) * p.sh + p.kh);
-      for (; waited < need; ++waited)
-        if (!(p.dbg & 4)) mbar_wait(&row_full[waited % kFrRing], (waited / kFrRing) & 1);
+      mbar_wait(&go[buf], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t dt = tmem + buf * (uint32_t)kFrN;
       const uint32_t row0 = seq_run + (uint32_t)((r - R0) * p.sh);  // ring sequence of input row r*sh

@@ -133,8 +133,7 @@ struct FrontArgs {
   DevLayout D;
   int32_t batch;                   // images of this launch
   const int32_t* dyn_n;            // device-resident batch clamp (nullable)
-  int32_t dbg;                     // profiling probes (env QNB_FRONT_DBG): 1 no epilogue math, 2 no MMAs,
-                                   // 4 MMAs skip the ring waits, 8 MMAs skip the accumulator waits
+  int32_t dbg;                     // profiling probes (env QNB_FRONT_DBG): 1 no epilogue math, 2 no MMAs
 };
 
 // Eligibility of conv (row-Hankel geometry on `in`) -> relu -> pool(k, s) for the front kernel.
