@@ -102,17 +102,16 @@ __device__ __forceinline__ uint32_t relu_lut32(uint32_t lutb, int32_t v) {
 
 // F bit 0: HI (requant shift s >= 32); bit 1: ReLU RN32; bit 2: clamp-free ReLU tail;
 // bit 3: ReLU through the replicated smem table (lutb).
-// RNE quotient of q8_fast (before the output zero point and the clamp).
+// RNE quotient of q8_fast (before the output zero point and the clamp), from the 64-bit
+// product P = acc * mult.
 template <bool HI>
-__device__ __forceinline__ int32_t q8_quot(int32_t acc, const Q8Consts& k) {
+__device__ __forceinline__ int32_t q8_quot_p(int64_t pr, const Q8Consts& k) {
   int32_t q;
   if constexpr (HI) {
-    const int64_t pr = mulwide_s32(acc, k.mult32);
     const uint32_t b = ((uint32_t)(pr >> 32) >> k.sh) & 1u;
     const int64_t t = pr + (k.halfm1 + (int64_t)b);
     q = (int32_t)(t >> 32) >> k.sh;
   } else {
-    const int64_t pr = mulwide_s32(acc, k.mult32);
     const int64_t b = (pr >> k.s) & 1;
     int64_t qq = (pr + k.halfm1 + b) >> k.s;
     const int64_t lim = (int64_t)1 << 40;  // keep the int32 add below exact (clamped right after)
@@ -120,6 +119,10 @@ __device__ __forceinline__ int32_t q8_quot(int32_t acc, const Q8Consts& k) {
     q = (int32_t)max(min(qq, (int64_t)INT32_MAX / 2), (int64_t)INT32_MIN / 2);
   }
   return q;
+}
+template <bool HI>
+__device__ __forceinline__ int32_t q8_quot(int32_t acc, const Q8Consts& k) {
+  return q8_quot_p<HI>(mulwide_s32(acc, k.mult32), k);
 }
 // requant_clamp's value (before any ReLU).
 template <bool HI>

@@ -57,7 +57,7 @@ constexpr int kFrWarps = 19;
 constexpr int kFrThreads = kFrWarps * 32;
 constexpr int kFrMma = 16, kFrProducer = 17, kFrGate = 18;
 constexpr int kFrGrp = 8;              // tile row-groups in flight (> ring rows / stride)
-constexpr int kFrRing = 28;            // input rows held in smem (a tile needs kh = 11)
+constexpr int kFrRing = 20;            // input rows held in smem (a tile needs kh = 11)
 constexpr int kFrRow = 4 * kHkSlot;    // one ring row: input row y of image pairs 2q and 2q+1
 constexpr int kFrN = 4 * 64;           // MMA N: 64 pixel columns per image
 constexpr int kFrCols = 56;            // pixel columns an epilogue thread drains (ow <= 56)
@@ -67,7 +67,7 @@ constexpr int kFrABlock = 128 * 128;   // one 128-byte K block of the 128-row A 
 static size_t front_smem_bytes(int num_kb) {
   return 1024 + (size_t)num_kb * kFrABlock + (size_t)kFrRing * kFrRow + 1024  // ring + K overrun slack
          + 2 * 4 * 64 * 4                                                     // zW*rowsum per column
-         + 8192                                                                // replicated ReLU table
+         + 256 * 128                                                           // ReLU table, 128 B per entry
          + (1 + kFrRing + 2 + 2 + 16 + kFrGrp + 2) * 8 + 16;                // barriers + TMEM slot
 }
 
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   uint8_t* ring = sW + (size_t)p.num_kb * kFrABlock;
   int32_t* rt = reinterpret_cast<int32_t*>(ring + kFrRing * kFrRow + 1024);  // [2 buf][4 img][64]
   uint8_t* relu_tab = reinterpret_cast<uint8_t*>(rt + 2 * 4 * 64);
-  uint64_t* w_full = reinterpret_cast<uint64_t*>(relu_tab + 8192);
+  uint64_t* w_full = reinterpret_cast<uint64_t*>(relu_tab + 256 * 128);
   uint64_t* row_empty = w_full + 1;
   uint64_t* acc_full = row_empty + kFrRing;
   uint64_t* acc_empty = acc_full + 2;
@@ -104,11 +104,11 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // relu_quant table replicated per lane (entry v of lane L at ((v >> 2) * 32 + L) * 4 + (v & 3)):
-  // a warp's lookups hit 32 distinct banks
+  // relu_quant table replicated per lane: entry v of lane L at byte 128 v + 4 L, so a warp's
+  // lookups hit 32 distinct banks and the address is one shift-add of v
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     const int v = i >> 5, l = i & 31;
-    relu_tab[((v >> 2) * 32 + l) * 4 + (v & 3)] = __ldg(p.relu_lut + v);
+    relu_tab[v * 128 + l * 4] = __ldg(p.relu_lut + v);
   }
   if (threadIdx.x == 0) {
     mbar_init(w_full, 1);
@@ -230,8 +230,11 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
     const bool rs_lane = !SA && quarter == 3 && lane == p.cpq;  // TMEM lane 96 + cpq: zW * rowsum
     const Q8Consts k = q8_consts(p.rq);
     const uint32_t lutb = smem_u32(relu_tab) + (uint32_t)lane * 4u;
-    const int64_t PIX = PIX_ ? PIX_ : p.D.pix;  // pooled-blob pixel stride (compile-time for AlexNet)
-    const int pw = p.pw;
+    // AlexNet specialisation (PIX_ = 96): pooled-blob pixel stride and row width compile-time
+    const int64_t PIX = PIX_ ? PIX_ : p.D.pix;
+    const int pw = PIX_ ? kFrPW : p.pw;
+    // SA: chan_const folds into the requant product, P = max * mult + cc * mult
+    const int64_t ccm = SA ? (int64_t)cc * k.mult32 : 0;
     int32_t acc[kFrPW];
 #pragma unroll
     for (int i = 0; i < kFrPW; ++i) acc[i] = 0;
@@ -270,8 +273,9 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
 #pragma unroll
             for (int q = Q0; q < Q1; ++q) {
               if (q >= pw) break;
-              const int32_t a = max(acc[q], (int32_t)hv[q - Q0]) + (SA ? cc : 0);
-              dst[q * PIX] = (uint8_t)relu_lut32(lutb, q8_clamped<HI>(a, k));
+              const int64_t P = (int64_t)max(acc[q], (int32_t)hv[q - Q0]) * k.mult32 + ccm;
+              const int32_t v = min(max(q8_quot_p<HI>(P, k) + k.oz, k.omin), k.omax);
+              dst[q * PIX] = (uint8_t)lds_u8(lutb + ((uint32_t)v << 7));
             }
           }
           if (mode == 2) {
@@ -447,7 +451,7 @@ qnb_status launch_front(const FrontArgs& a0, cudaStream_t s) {
   FrontArgs a = a0;
   a.dbg |= dbg;
   const bool hi = a.rq.s >= 32;
-  if (a.D.pix == 96) {  // AlexNet pool1: 96 channels, compile-time store stride
+  if (a.D.pix == 96 && a.pw == kFrPW) {  // AlexNet pool1: 96 channels x 27 columns, compile-time
     if (a.signed_a) return hi ? launch_front_t<true, true, 96>(a, s) : launch_front_t<false, true, 96>(a, s);
     return hi ? launch_front_t<true, false, 96>(a, s) : launch_front_t<false, false, 96>(a, s);
   }
