@@ -35,9 +35,10 @@
 //   0-15  epilogue: quarter = warp % 4 (TMEM lanes), image = warp / 4 (64 columns)
 //   16    TMEM allocator (512 columns: two 256-column accumulators) + MMA issuer
 //   17    producer: resident weights, then the input-row ring (one barrier per tile's rows)
-//   18    gate: rows resident + accumulator drained -> go[buf], so the MMA warp waits on a
-//         single barrier per tile (each wait in the issuing warp idles the tensor pipe for
-//         ~250 cycles, scripts/probe/umma_ring.cu)
+// Tile j may start when its new input rows landed AND the epilogue drained tile j - 2's
+// accumulator: both signals go to one barrier go[j % kFrGrp] (the producer's expect_tx +
+// TMA complete_tx, and the 16 epilogue warps' arrivals), so the MMA warp waits once per
+// tile (each wait in the issuing warp idles the tensor pipe, scripts/probe/umma_ring.cu).
 #include <cuda.h>
 
 #include <algorithm>
@@ -53,9 +54,9 @@
 
 namespace qnb {
 
-constexpr int kFrWarps = 19;
+constexpr int kFrWarps = 18;
 constexpr int kFrThreads = kFrWarps * 32;
-constexpr int kFrMma = 16, kFrProducer = 17, kFrGate = 18;
+constexpr int kFrMma = 16, kFrProducer = 17;
 constexpr int kFrGrp = 8;              // tile row-groups in flight (> ring rows / stride)
 constexpr int kFrRing = 20;            // input rows held in smem (a tile needs kh = 11)
 constexpr int kFrRow = 4 * kHkSlot;    // one ring row: input row y of image pairs 2q and 2q+1
@@ -68,7 +69,7 @@ static size_t front_smem_bytes(int num_kb) {
   return 1024 + (size_t)num_kb * kFrABlock + (size_t)kFrRing * kFrRow + 1024  // ring + K overrun slack
          + 2 * 4 * 64 * 4                                                     // zW*rowsum per column
          + 256 * 128                                                           // ReLU table, 128 B per entry
-         + (1 + kFrRing + 2 + 2 + 16 + kFrGrp + 2) * 8 + 16;                // barriers + TMEM slot
+         + (1 + kFrRing + 2 + 16 + kFrGrp) * 8 + 16;                // barriers + TMEM slot
 }
 
 // The band of pool rows [u0, u1) of the flattened (image quad, pool row) space, as the
@@ -97,11 +98,9 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   uint64_t* w_full = reinterpret_cast<uint64_t*>(relu_tab + 256 * 128);
   uint64_t* row_empty = w_full + 1;
   uint64_t* acc_full = row_empty + kFrRing;
-  uint64_t* acc_empty = acc_full + 2;
-  uint64_t* rt_full = acc_empty + 2;  // [2 buf][4 img][2 halves]
-  uint64_t* grp_full = rt_full + 16;  // [kFrGrp]: a tile's new input rows (one complete_tx group)
-  uint64_t* go = grp_full + kFrGrp;     // [2]: rows resident AND accumulator free -> the MMA warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + 2);
+  uint64_t* rt_full = acc_full + 2;  // [2 buf][4 img][2 halves]
+  uint64_t* go = rt_full + 16;  // [kFrGrp]: tile j's rows landed and its accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + kFrGrp);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // relu_quant table replicated per lane: entry v of lane L at byte 128 v + 4 L, so a warp's
@@ -113,13 +112,9 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
   if (threadIdx.x == 0) {
     mbar_init(w_full, 1);
     for (int i = 0; i < kFrRing; ++i) mbar_init(&row_empty[i], 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 16);
-    }
+    for (int i = 0; i < 2; ++i) mbar_init(&acc_full[i], 1);
     for (int i = 0; i < 16; ++i) mbar_init(&rt_full[i], 1);
-    for (int i = 0; i < kFrGrp; ++i) mbar_init(&grp_full[i], 1);
-    for (int i = 0; i < 2; ++i) mbar_init(&go[i], 1);
+    for (int i = 0; i < kFrGrp; ++i) mbar_init(&go[i], 1 + 16);  // producer + 16 epilogue warps
     fence_barrier_init();
   }
   if (warp == kFrMma) {
@@ -153,7 +148,7 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
         const uint8_t* src = p.a + (int64_t)(2 * quad) * p.a_img + p.a_origin;
         // all of this tile's new rows complete one group barrier (the MMA warp then waits
         // once per tile: every mbarrier wait in the issuing warp idles the tensor pipe)
-        uint64_t* gb = &grp_full[jt % kFrGrp];
+        uint64_t* gb = &go[jt % kFrGrp];
         ++jt;
         mbar_arrive_expect_tx(gb, (uint32_t)((y1 - y0) * (two ? 2 : 1) * 2 * kHkSlot));
         for (int y = y0; y < y1; ++y, ++seq) {
@@ -163,20 +158,6 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
           if (two)
             bulk_g2s(ring + (size_t)s * kFrRow + 2 * kHkSlot, src + p.a_img + (int64_t)y * p.a_row, 2 * kHkSlot, gb);
         }
-      });
-    }
-    __syncwarp();
-  } else if (warp == kFrGate) {
-    // tile j may start when its rows are resident and its accumulator was drained
-    griddep_wait();
-    const int n_live = p.dyn_n ? min(p.batch, __ldg(p.dyn_n)) : p.batch;
-    if (lane == 0) {
-      uint32_t j = 0;
-      front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int, int, int, int) {
-        mbar_wait(&grp_full[j % kFrGrp], (j / kFrGrp) & 1);
-        mbar_wait(&acc_empty[j & 1], ((j >> 1) & 1) ^ 1);
-        mbar_arrive(&go[j & 1]);
-        ++j;
       });
     }
     __syncwarp();
@@ -197,7 +178,7 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
         seq_next += (uint32_t)((R1 - R0) * p.sh + p.kh);
       }
       const uint32_t buf = j & 1;
-      mbar_wait(&go[buf], (j >> 1) & 1);
+      mbar_wait(&go[j % kFrGrp], (j / kFrGrp) & 1);
       tc_fence_after();
       const uint32_t dt = tmem + buf * (uint32_t)kFrN;
       const uint32_t row0 = seq_run + (uint32_t)((r - R0) * p.sh);  // ring sequence of input row r*sh
@@ -238,16 +219,20 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
     int32_t acc[kFrPW];
 #pragma unroll
     for (int i = 0; i < kFrPW; ++i) acc[i] = 0;
+    if (lane == 0) {  // both accumulators start drained: tiles 0 and 1 need no epilogue release
+      mbar_arrive(&go[0]);
+      mbar_arrive(&go[1]);
+    }
     uint32_t j = 0;
     front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int quad, int r, int R0, int R1) {
-      const uint32_t buf = j & 1, par = (j >> 1) & 1;
-      ++j;
+      const uint32_t jc = j++, buf = jc & 1, par = (jc >> 1) & 1;
+      uint64_t* release = &go[(jc + 2) % kFrGrp];  // this accumulator is next written by tile jc + 2
       mbar_wait(&acc_full[buf], par);
       tc_fence_after();
       if (p.dbg & 1) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        if (lane == 0) mbar_arrive(release);
         return;
       }
       const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + buf * (uint32_t)kFrN + 64u * (uint32_t)img;
@@ -341,7 +326,7 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
       // running-max / requant work
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) mbar_arrive(release);
 #pragma unroll
       for (int q = 16; q < kFrPW; ++q)
         w[q - 16] = (uint32_t)max(max((int32_t)w[2 * q - 32], (int32_t)w[2 * q - 31]), (int32_t)w[2 * q - 30]);

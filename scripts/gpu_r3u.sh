@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out
+for D in 0 1 3; do QNB_FRONT_DBG=$D timeout 300 python bench.py --no-cpu-baseline --steps 20 --warmup 5 > $O/r3u_dbg$D.json 2>/dev/null; done
