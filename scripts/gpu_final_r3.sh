@@ -1,7 +1,7 @@
-# Round-2 verification pass: full GPU tests, smoke, every bench line, the reference arm,
+# Round-2 (session 3) verification pass: full GPU tests, smoke, every bench line, the reference arm,
 # ncu launch list + one --set full forward capture (with the tcgen05 UMMA counters).
 cd $GRAFT_REPO_ROOT
-TAG=${1:-r2s}
+TAG=${1:-r3z}
 O=gpurun_out
 UM=sm__ops_path_tensor_op_utcimma_src_int8_realtime.avg.pct_of_peak_sustained_elapsed,sm__ops_path_tensor_op_utcimma_src_int8_realtime.sum
 timeout 1800 python -m pytest tests -m gpu -q -x -p no:hypothesispytest > $O/${TAG}_tests.log 2>&1
@@ -20,3 +20,5 @@ timeout 900 ncu --set full --metrics $UM --clock-control none --import-source on
 ncu -i $O/${TAG}_full.ncu-rep --page raw --csv > $O/${TAG}_full_raw.csv 2>/dev/null
 ncu -i $O/${TAG}_full.ncu-rep --page details > $O/${TAG}_full_details.txt 2>/dev/null
 rm -f $O/${TAG}_full.ncu-rep
+bash scripts/gpu_ncu_kernel.sh ${TAG}_front front_kernel
+rm -f $O/${TAG}_front_sass.csv.gz; gzip -f $O/${TAG}_front_sass.csv
