@@ -16,7 +16,7 @@ timeout 900 python bench.py --model alexnet_moe --steps 30 --warmup 5 > $O/${TAG
 timeout 900 python bench.py --model vgg16 --batch 128 --steps 10 --warmup 3 --no-cpu-baseline > $O/${TAG}_vgg.json 2> $O/${TAG}_vgg.err
 timeout 1500 python bench.py --model convsweep --batch 128 --no-cpu-baseline > $O/${TAG}_sweep.json 2> $O/${TAG}_sweep.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --profile-reps 1 > /dev/null 2> $O/${TAG}_ncu.err
-timeout 900 ncu --set full --metrics $UM --clock-control none --import-source on -k "regex:igemm|pack|pool|softmax" -c 14 -o $O/${TAG}_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline --profile-reps 1 > $O/${TAG}_full_ncu.log 2>&1
+timeout 900 ncu --set full --metrics $UM --clock-control none --import-source on -k "regex:igemm|pack|pool|softmax|front" -c 14 -o $O/${TAG}_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline --profile-reps 1 > $O/${TAG}_full_ncu.log 2>&1
 ncu -i $O/${TAG}_full.ncu-rep --page raw --csv > $O/${TAG}_full_raw.csv 2>/dev/null
 ncu -i $O/${TAG}_full.ncu-rep --page details > $O/${TAG}_full_details.txt 2>/dev/null
 rm -f $O/${TAG}_full.ncu-rep

@@ -1,5 +1,5 @@
 """Summarises an ncu --set full capture of one AlexNet INT8 forward (16 launches, see
-scripts/gpu_final.sh): writes profiles/ncu/<tag>_forward_table.md and the per-launch DRAM
+scripts/gpu_final_r3.sh): writes profiles/ncu/<tag>_forward_table.md and the per-launch DRAM
 traffic bench.py reports as roofline.traffic (profiles/ncu/traffic_alexnet_int8.json).
 usage: python scripts/ncu_table.py gpurun_out/<tag>_full.ncu-rep <tag> [layer,names,...]"""
 import csv
@@ -26,10 +26,10 @@ def get(r, k):
         return float("nan")
 
 
-# layer of each launch, in plan order (argv[3] overrides; the round-2 default plan splits K
-# only for fc8, so one finalize launch follows it)
+# layer of each launch, in plan order (argv[3] overrides; conv1 + relu1 + pool1 run in the
+# front kernel, norm1 as an LRN-only pool_lrn pass; fc8 splits K, so a finalize follows it)
 names = (sys.argv[3].split(",") if len(sys.argv) > 3 else
-         ["data", "conv1", "pool1", "conv2", "pool2", "conv3", "conv4", "conv5", "pool5", "fc6", "fc7", "fc8",
+         ["data", "conv1", "norm1", "conv2", "pool2", "conv3", "conv4", "conv5", "pool5", "fc6", "fc7", "fc8",
           "fc8_finalize", "fc8_to_fp32"])
 lines = ["| layer | kernel | us | dram read MB | dram write MB | UMMA dense % | dram % | SM % |",
          "|---|---|---|---|---|---|---|---|"]
