@@ -2528,7 +2528,11 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     const size_t cap = 227 * 1024;
     auto str_stages = [&]() -> int {
       const size_t fx = igemm_pair_stream_smem_bytes(a.n_rows, 0);
-      return fx < cap ? (int)std::min<size_t>(6, (cap - fx) / ((size_t)(kBM + a.n_rows / 2) * 128)) : 0;
+      static const size_t ss_cap = [] {
+        const char* e = std::getenv("QNB_PAIR_SSTAGES");
+        return (size_t)(e ? std::max(2, std::min(kMaxStages, atoi(e))) : 8);
+      }();
+      return fx < cap ? (int)std::min<size_t>(ss_cap, (cap - fx) / ((size_t)(kBM + a.n_rows / 2) * 128)) : 0;
     };
     const size_t fixed = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0);
     int stages = fixed < cap ? (int)std::min<size_t>(kMaxStages, (cap - fixed) / (kBM * 128)) : 0;

@@ -658,7 +658,10 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
   bool ppatch = false;
   int32_t pp_slab = 0, pp_astg = 0, pp_rows = 0;
   const bool patch0 = !hk && (use_patch || ppatch_try) && igemm_patch_eligible(g, Lin);
-  static const int tma_align = std::getenv("QNB_TMA64") ? 64 : 128;  // A/B: 64-byte (SW64) im2col stages
+  static const int tma_align = [] {  // A/B: QNB_TMA_ALIGN=64 / 16 admits narrower channel runs per tap
+    const char* e = std::getenv("QNB_TMA_ALIGN");
+    return e ? std::max(16, atoi(e)) : (std::getenv("QNB_TMA64") ? 64 : 128);
+  }();
   // TMA im2col boxes are 128 consecutive output pixels: on narrow outputs (AlexNet conv3,
   // 13 wide) one box wraps ~10 rows and the CTA-pair gather measured faster (+0.6 %)
   bool patch = patch0;
@@ -849,9 +852,10 @@ qnb_status emit_igemm(qnb_plan& P, const Op& op, Step& st) {
     const int64_t tiles = m_tiles * pk.n_tiles;
     int64_t ks = 148 / std::max<int64_t>(tiles, 1);
     ks = std::max<int64_t>(1, std::min<int64_t>(ks, pk.num_kb / 2));
-    // at most 2 splits with 64-column tiles: more splits only multiply the s32 partial
-    // traffic the finalize re-reads (fc8: 11 splits wrote 3.5x its 4 MB of weights)
-    int64_t ks_max = 2;
+    // at most 4 splits with 64-column tiles: more splits only multiply the s32 partial
+    // traffic the finalize re-reads (fc8: 11 splits wrote 3.5x its 4 MB of weights; 4 splits
+    // measured 21.5 vs 23.6 us for 2; fc6 / fc7 have enough tiles for 1)
+    int64_t ks_max = 4;
     if (const char* e = std::getenv("QNB_FC_KS_MAX")) ks_max = std::max(1, atoi(e));
     ks = std::max<int64_t>(1, std::min<int64_t>(ks, ks_max));
     a.cluster = 1;

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) pack_rgb_u8_kernel(const float* __restric
 // mask and redone by the exact path afterwards, so the common case carries no
 // divergent branches.
 template <int C>
-__global__ void __launch_bounds__(256) pack_rgb_c_kernel(const float* __restrict__ src, int H, int W,
+__global__ void __launch_bounds__(256, 6) pack_rgb_c_kernel(const float* __restrict__ src, int H, int W,
                                                          uint8_t* __restrict__ dst, DevLayout L, DevQ q,
                                                          uint32_t fill) {
   const int ry = threadIdx.x / kPackLanes, l = threadIdx.x % kPackLanes;
