@@ -170,7 +170,10 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
     mbar_wait(w_full, 0);
     const uint64_t wd0 = smem_desc_sw128(sW);
     const uint64_t rd0 = smem_desc_none(ring, 16, 128);
-    const int ksteps = p.kpr / 32;
+    // AlexNet specialisation: 11 filter rows x 2 K steps unrolled with compile-time
+    // descriptor offsets (a run-time loop measured as a slower issue stream)
+    const int ksteps = PIX_ ? 2 : p.kpr / 32;
+    const int kh = PIX_ ? 11 : p.kh;
     uint32_t j = 0, seq_next = 0, seq_run = 0;
     front_walk(u0, u1, p.ph, (n_live + 3) >> 2, [&](int, int r, int R0, int R1) {
       if (r == R0) {  // a run loads rows [R0 sh, R1 sh + kh) contiguously in the ring sequence
@@ -183,15 +186,19 @@ __global__ void __launch_bounds__(kFrThreads, 1) front_kernel(const __grid_const
       const uint32_t dt = tmem + buf * (uint32_t)kFrN;
       const uint32_t row0 = seq_run + (uint32_t)((r - R0) * p.sh);  // ring sequence of input row r*sh
       if (elect_one()) {
-        if (!(p.dbg & 2))
-          for (int kr = 0; kr < p.kh; ++kr) {
-            const uint32_t rs = (row0 + kr) % kFrRing;
+        if (!(p.dbg & 2)) {
+          const uint32_t rs0 = row0 % kFrRing;
+#pragma unroll
+          for (int kr = 0; kr < kh; ++kr) {
+            const uint32_t rs = rs0 + kr < kFrRing ? rs0 + kr : rs0 + kr - kFrRing;
+#pragma unroll
             for (int q = 0; q < ksteps; ++q) {
-              const uint32_t kk = (uint32_t)(kr * p.kpr + q * 32);  // K byte in the packed A order
+              const uint32_t kk = (uint32_t)(kr * (PIX_ ? 64 : p.kpr) + q * 32);  // K byte in the packed A order
               umma<KIND_I8>(dt, wd0 + (kk >> 7) * (kFrABlock >> 4) + 2 * ((kk & 127) >> 5),
                             rd0 + ((rs * kFrRow + q * 32) >> 4), idesc, (kr | q) != 0);
             }
           }
+        }
         tc_commit(&acc_full[buf]);
         // ring rows the next tile of the run no longer reads (all of them after the last)
         const uint32_t nfree = r == R1 ? (uint32_t)p.kh : (uint32_t)p.sh;
@@ -436,7 +443,7 @@ qnb_status launch_front(const FrontArgs& a0, cudaStream_t s) {
   FrontArgs a = a0;
   a.dbg |= dbg;
   const bool hi = a.rq.s >= 32;
-  if (a.D.pix == 96 && a.pw == kFrPW) {  // AlexNet pool1: 96 channels x 27 columns, compile-time
+  if (a.D.pix == 96 && a.pw == kFrPW && a.kh == 11 && a.kpr == 64) {  // AlexNet conv1/pool1: compile-time shape
     if (a.signed_a) return hi ? launch_front_t<true, true, 96>(a, s) : launch_front_t<false, true, 96>(a, s);
     return hi ? launch_front_t<true, false, 96>(a, s) : launch_front_t<false, false, 96>(a, s);
   }
