@@ -143,6 +143,10 @@ template <int C>
 __global__ void __launch_bounds__(256, 6) pack_rgb_c_kernel(const float* __restrict__ src, int H, int W,
                                                          uint8_t* __restrict__ dst, DevLayout L, DevQ q,
                                                          uint32_t fill) {
+  // the next kernel (the conv1 front kernel, launched with programmatic stream
+  // serialization) may start its weight loads as SMs drain; it waits on this grid's
+  // completion (griddepcontrol.wait) before reading the packed rows
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ry = threadIdx.x / kPackLanes, l = threadIdx.x % kPackLanes;
   const int y = blockIdx.x * (256 / kPackLanes) + ry;
   if (y >= H) return;
