@@ -657,7 +657,8 @@ __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_
     const bool ok = lane_on && pix < total_pix;
     float x[16];
     if (ok) {
-      const int n = pix / Dhw, rem = pix - n * Dhw, oy = rem / Dw, ox = rem - oy * Dw;
+      const int n = (int)(((uint64_t)(uint32_t)pix * a.m_hw) >> a.sh_hw), rem = pix - n * Dhw;
+      const int oy = (int)(((uint64_t)(uint32_t)rem * a.m_w) >> a.sh_w), ox = rem - oy * Dw;
       const uint8_t* wp = at(a.src, a.S, n, (int64_t)oy * st, (int64_t)ox * st) + ch * 16 * LrnIo<IT>::es;
       constexpr int W = PK > 0 ? PK * PK : 1;
       uint4 v[W][IV];
@@ -783,7 +784,8 @@ __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_
         }
       }
     }
-    const int n = pix / Dhw, rem = pix - n * Dhw, oy = rem / Dw, ox = rem - oy * Dw;
+    const int n = (int)(((uint64_t)(uint32_t)pix * a.m_hw) >> a.sh_hw), rem = pix - n * Dhw;
+    const int oy = (int)(((uint64_t)(uint32_t)rem * a.m_w) >> a.sh_w), ox = rem - oy * Dw;
     uint4* dst = reinterpret_cast<uint4*>(at(a.dst, a.D, n, oy, ox) + ch * 16 * LrnIo<OT>::es);
 #pragma unroll
     for (int u = 0; u < OV; ++u)
@@ -1044,7 +1046,16 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
     const int32_t total = (int32_t)(a.D.n * a.D.h * a.D.w);
     const int64_t ppb = 8 * (32 / CH);
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(total, ppb), 148 * 3);
-#define QNB_PLV2_T(PK, C_, IT, OT) pool_lrn5_kernel<PK, C_, IT, OT><<<blocks, 256, 0, s>>>(a, total)
+    PoolLrnArgs ar = a;
+    auto magic = [](int64_t d, uint32_t* m, int32_t* sh) {  // exact for numerators < 2^31
+      int l = 0;
+      while ((int64_t(1) << l) < d) ++l;
+      *sh = 31 + l;
+      *m = (uint32_t)(((uint64_t)1 << *sh) / (uint64_t)d + 1);
+    };
+    magic(a.D.h * a.D.w, &ar.m_hw, &ar.sh_hw);
+    magic(a.D.w, &ar.m_w, &ar.sh_w);
+#define QNB_PLV2_T(PK, C_, IT, OT) pool_lrn5_kernel<PK, C_, IT, OT><<<blocks, 256, 0, s>>>(ar, total)
 #define QNB_PLV2_IO(PK, C_)                                                                         \
   do {                                                                                              \
     if (a.in_dtype == QNB_INT8Q && a.out_dtype == QNB_INT8Q) QNB_PLV2_T(PK, C_, QNB_INT8Q, QNB_INT8Q); \

@@ -80,6 +80,10 @@ struct PoolLrnArgs {
   double a_n, beta, k;
   int32_t pix;  // output pixels per block (pool_lrn_q8); set by launch_pool_lrn
   int32_t exact_float;  // float outputs must carry the reference's exact FP32 bits
+  // pixel -> (image, row, column) by multiply-shift (set by launch_pool_lrn): for x < 2^31,
+  // x / d == (x * m) >> sh with sh = 31 + ceil(log2 d), m = floor(2^sh / d) + 1
+  uint32_t m_hw, m_w;
+  int32_t sh_hw, sh_w;
 };
 
 enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3, CVT_PSEUDO = 4 };
