@@ -2528,10 +2528,13 @@ static qnb_status launch_kind(const IgemmArgs& a0, int64_t groups, cudaStream_t 
     const size_t cap = 227 * 1024;
     auto str_stages = [&]() -> int {
       const size_t fx = igemm_pair_stream_smem_bytes(a.n_rows, 0);
-      static const size_t ss_cap = [] {
+      // 8 stages for the INT8 inner products (fc6 34.9 -> 32.8 us), 6 elsewhere (8 made the
+      // FP16 / INT16 convolutions 5-15 % slower)
+      static const int ss_env = [] {
         const char* e = std::getenv("QNB_PAIR_SSTAGES");
-        return (size_t)(e ? std::max(2, std::min(kMaxStages, atoi(e))) : 8);
+        return e ? std::max(2, std::min(kMaxStages, atoi(e))) : 0;
       }();
+      const size_t ss_cap = (size_t)(ss_env ? ss_env : (a.a_tma2d ? 8 : 6));
       return fx < cap ? (int)std::min<size_t>(ss_cap, (cap - fx) / ((size_t)(kBM + a.n_rows / 2) * 128)) : 0;
     };
     const size_t fixed = igemm_pair_smem_bytes(a.n_rows, a.num_kb, 0);
