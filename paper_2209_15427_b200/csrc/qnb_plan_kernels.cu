@@ -262,6 +262,8 @@ __global__ void pool_u8_kernel(const uint8_t* __restrict__ src, DevLayout S, uin
 template <int K>
 __global__ void __launch_bounds__(256) pool_u8_k_kernel(const uint8_t* __restrict__ src, DevLayout S,
                                                         uint8_t* __restrict__ dst, DevLayout D, int st) {
+  // the next kernel (a PDL-launched GEMM) may start its prologue as this grid drains
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int chunks = (int)(S.c_phys / 16);
   const int total = (int)(eff_n(D) * D.h * D.w * chunks);  // host checks < 2^31
   const int Dw = (int)D.w, Dh = (int)D.h;
@@ -633,6 +635,8 @@ struct LrnIo {
 
 template <int PK, int CH, int IT, int OT>
 __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_t total_pix_cap) {
+  // the next kernel (a PDL-launched GEMM) may start its prologue as this grid drains
+  if (a.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int32_t total_pix = (int32_t)(eff_n(a.D) * a.D.h * a.D.w);
   (void)total_pix_cap;
   __shared__ float lut[256];
@@ -1047,6 +1051,8 @@ void launch_pool_lrn(const PoolLrnArgs& a, cudaStream_t s) {
     const int64_t ppb = 8 * (32 / CH);
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(total, ppb), 148 * 3);
     PoolLrnArgs ar = a;
+    static const bool lrn_pdl = std::getenv("QNB_NO_LRN_PDL") == nullptr;  // +2 % (AlexNet INT8)
+    ar.pdl = lrn_pdl ? 1 : 0;
     auto magic = [](int64_t d, uint32_t* m, int32_t* sh) {  // exact for numerators < 2^31
       int l = 0;
       while ((int64_t(1) << l) < d) ++l;

@@ -84,6 +84,7 @@ struct PoolLrnArgs {
   // x / d == (x * m) >> sh with sh = 31 + ceil(log2 d), m = floor(2^sh / d) + 1
   uint32_t m_hw, m_w;
   int32_t sh_hw, sh_w;
+  int32_t pdl;  // trigger dependent launch at entry (set by launch_pool_lrn)
 };
 
 enum ConvertOp : int { CVT_CONVERT = 0, CVT_REQUANT = 1, CVT_RELU_Q = 2, CVT_RELU_F = 3, CVT_PSEUDO = 4 };
