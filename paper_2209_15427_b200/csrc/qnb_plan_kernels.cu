@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_
     uint32_t packed[4 * OV];
 #pragma unroll
     for (int i = 0; i < 4 * OV; ++i) packed[i] = 0;
-    uint32_t slow = 0;
+    bool any_slow = false;
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       const float sf = __fadd_rn(__fadd_rn(__fadd_rn(sq[c], sq[c + 1]), __fadd_rn(sq[c + 2], sq[c + 3])), sq[c + 4]);
@@ -761,7 +761,8 @@ __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_
       if constexpr (OT == QNB_INT8Q || OT == QNB_INT16Q) {
         const float t = __fmul_rn(__fmul_rn(e[c + 2], rden), finv);
         const float r = rintf(t);
-        slow |= (fabsf(__fsub_rn(t, r)) < __fsub_rn(0.5f, __fmaf_rn(3e-6f, fabsf(t), 1e-6f)) ? 0u : 1u) << c;
+        // decided unless |t - r| + 3e-6 |t| >= 0.5 - 1e-6 (NaN / inf fail the compare)
+        any_slow |= !(__fmaf_rn(3e-6f, fabsf(t), fabsf(__fsub_rn(t, r))) < 0.499999f);
         if constexpr (OT == QNB_INT8Q) {
           packed[c >> 2] |= sat_u8(r + zf) << (8 * (c & 3));  // INT8Q grid: i_min 0, i_max 255
         } else {
@@ -775,10 +776,15 @@ __global__ void __launch_bounds__(256, 3) pool_lrn5_kernel(PoolLrnArgs a, int32_
       }
     }
     if constexpr (OT == QNB_INT8Q || OT == QNB_INT16Q) {
-      if (slow) {  // rare: the reference's exact double arithmetic decides
+      if (any_slow) {  // rare: the reference's exact double arithmetic decides the flagged values
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
-          if (!((slow >> c) & 1u)) continue;
+          // the same float path recomputed (explicitly rounded intrinsics: bit-identical t)
+          const float sf = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(e[c], e[c]), __fmul_rn(e[c + 1], e[c + 1])),
+                                               __fadd_rn(__fmul_rn(e[c + 2], e[c + 2]), __fmul_rn(e[c + 3], e[c + 3]))),
+                                     __fmul_rn(e[c + 4], e[c + 4]));
+          const float t = __fmul_rn(__fmul_rn(e[c + 2], ex2_ftz(__fmul_rn(nbeta, lg2_ftz(__fmaf_rn(fa_n, sf, fk))))), finv);
+          if (__fmaf_rn(3e-6f, fabsf(t), fabsf(__fsub_rn(t, rintf(t)))) < 0.499999f) continue;
           const uint32_t qv =
               (uint32_t)lrn_exact5(e[c], e[c + 1], e[c + 2], e[c + 3], e[c + 4], a.k, a.a_n, a.beta, a.out_q);
           if constexpr (OT == QNB_INT8Q)
